@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark: GR-KAN group-rational fwd+bwd throughput at KAT-B shape on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--dtype fp32|bf16]
+                    [--config kat-b|kat-s|kat-t] [--mode fast|exact] [--impl b200|reference]
+
+One step = one forward (K1) + one backward (K2 + K3) of the group-rational
+unit over one synthetic [B, L, D] batch (run_bench --include-forward,
+pkg/src/grkan/cli.py:178-185), plus, when N > 1, the NCCL all-reduce of the
+per-group da/db (the path's only exchange).  Weak scaling: every rank owns a
+full KAT-B batch (B=256), so per-GPU work is fixed as N grows.
+
+``value``  elements/s over all ranks, inputs already resident in HBM, device
+           time (CUDA events) max over ranks.
+``e2e``    the same metric through the public torch API (GroupRationalFn
+           forward + autograd backward) with x, dy copied from pinned host
+           memory and y, dx, da, db copied back every step.
+``roofline`` the dominant kernel (the backward call: K2 + its tiny K3 fold),
+           algorithmic bytes 3*s*E per launch / its CUDA-event duration.
+``cpu_baseline`` the oracle port of the reference path (NumPy, all host
+           threads) on a bounded sample of the same workload (rank 0, N=1).
+
+``--impl reference`` times only that CPU path (rank 0; other ranks exit 0).
+Inputs exceed L2 (KAT-B fp32: 620 MB per tensor vs 126 MB L2), so no flush.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "GR-KAN fwd+bwd elements/sec & HBM GB/s (KAT-B shape) at 1/2/4/8 B200 vs CPU"
+UNIT = "elements/s"
+CONFIGS = {  # (batch per GPU, seq, dim, groups)
+    "kat-t": (8, 197, 192, 8),
+    "kat-s": (128, 197, 1536, 8),
+    "kat-b": (256, 197, 3072, 8),
+}
+M1, NDEN = 6, 4
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse_args(argv=None):
+    p = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    p.add_argument("--dtype", choices=("fp32", "bf16"), default="fp32")
+    p.add_argument("--config", choices=tuple(CONFIGS), default="kat-b")
+    p.add_argument("--mode", choices=("fast", "exact"), default="fast")
+    p.add_argument("--scaling", choices=("weak", "strong"), default="weak")
+    p.add_argument("--e2e-steps", type=int, default=None)
+    p.add_argument("--cpu-sample-batch", type=int, default=16)
+    p.add_argument("--cpu-passes", type=int, default=3)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args(argv)
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy bandwidth)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# CPU path: the oracle port of the reference (forward_tensor + backward_blocked)
+# ---------------------------------------------------------------------------
+
+def cpu_reference_rate(cfg, batch, passes, warmup=1):
+    """elements/s of the NumPy restatement of the reference path on this host."""
+    from oracle import grkan_oracle as orc
+
+    _, seq, dim, groups = cfg
+    x, u, num, den = orc.bench_inputs(batch, seq, dim, groups, M1, NDEN, seed=0)
+    workers = os.cpu_count() or 1
+    for _ in range(warmup):
+        orc.cpu_step(x, u, num, den, workers=workers)
+    times = []
+    for _ in range(passes):
+        t0 = time.perf_counter()
+        orc.cpu_step(x, u, num, den, workers=workers)
+        times.append(time.perf_counter() - t0)
+    mean = statistics.fmean(times)
+    return x.size / mean, workers, times
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    batch = min(args.cpu_sample_batch, cfg[0])
+    # each step = one reference-style fwd+bwd pass over a bounded sample
+    rate, workers, times = cpu_reference_rate(cfg, batch, max(1, args.steps), warmup=args.warmup)
+    ms = statistics.fmean(times) * 1e3
+    sample = "%s rows B=%d of %d (E=%d), NumPy port of forward_tensor+backward_blocked, block 256, " \
+             "workers=%d" % (args.config, batch, cfg[0], batch * cfg[1] * cfg[2], workers)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (run_bench draw order, seed 0)",
+        "config": config_block(args, cfg),
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(args, cfg):
+    batch, seq, dim, groups = cfg
+    return {
+        "workload": "GR-KAN group-rational fwd+bwd, %s shape [B=%d, L=%d, D=%d] per GPU, %d groups, "
+                    "degrees (5,4)" % (args.config.upper(), batch, seq, dim, groups),
+        "batch_per_gpu": batch, "seq_len": seq, "dim": dim, "groups": groups,
+        "degrees": [M1 - 1, NDEN], "mode": args.mode, "io_dtype": args.dtype,
+        "parallelism": "dp%d" % args.gpus,
+        "l2": "inputs larger than L2 (no flush): %d MB per tensor vs 126 MB L2"
+              % (batch * seq * dim * (4 if args.dtype == "fp32" else 2) // 2**20),
+    }
+
+
+# ---------------------------------------------------------------------------
+# Clock sampling during the timed region (NVML)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    REASONS = {
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+        0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
+        0x2: "applications_clocks_setting", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._thr = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def start(self):
+        if self._nv is not None:
+            self._thr = threading.Thread(target=self._run, daemon=True)
+            self._thr.start()
+
+    def stop(self):
+        if self._thr is not None:
+            self._stop.set()
+            self._thr.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        reasons = [name for bit, name in self.REASONS.items() if self.reasons & bit and bit != 0x1]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def run_b200(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_13813_b200 import _native as N
+    from paper_2505_13813_b200 import ops
+    from paper_2505_13813_b200.module import GroupRationalFn
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg = CONFIGS[args.config]
+    batch, seq, dim, groups = cfg
+    if args.scaling == "strong":
+        batch = max(1, batch // world)
+    tdt = torch.float32 if args.dtype == "fp32" else torch.bfloat16
+    es = 4 if args.dtype == "fp32" else 2
+    E = batch * seq * dim
+    rows = batch * seq
+    dt_code = N.DT_F32 if args.dtype == "fp32" else N.DT_BF16
+    flags = N.FLAG_EXACT if args.mode == "exact" else N.FLAG_FAST
+
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    x = torch.randn((batch, seq, dim), generator=gen, device=dev, dtype=torch.float32).to(tdt)
+    dy = torch.randn((batch, seq, dim), generator=gen, device=dev, dtype=torch.float32).to(tdt)
+    crng = np.random.default_rng(0)  # identical coefficients on every rank
+    a = torch.from_numpy(crng.standard_normal((groups, M1)).astype(np.float32)).to(dev)
+    b = torch.from_numpy(crng.standard_normal((groups, NDEN)).astype(np.float32)).to(dev)
+    y = torch.empty_like(x)
+    dx = torch.empty_like(x)
+    grads = torch.empty(groups * (M1 + NDEN), dtype=torch.float32, device=dev)  # da || db, one buffer
+    da = grads[: groups * M1].view(groups, M1)
+    db = grads[groups * M1:].view(groups, NDEN)
+    ws_bytes = ops.workspace_bytes(rows, dim, groups, M1, NDEN, tdt)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    L = N.lib()
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+
+    def fwd():
+        rc = L.grkan_fwd(x.data_ptr(), y.data_ptr(), a.data_ptr(), b.data_ptr(), rows, dim, groups,
+                         M1, NDEN, dt_code, flags, None, sp)
+        assert rc == 0, N.last_error()
+
+    def bwd():
+        rc = L.grkan_bwd(x.data_ptr(), dy.data_ptr(), a.data_ptr(), b.data_ptr(), dx.data_ptr(),
+                         da.data_ptr(), db.data_ptr(), ws.data_ptr(), ws_bytes, rows, dim, groups,
+                         M1, NDEN, dt_code, flags, sp)
+        assert rc == 0, N.last_error()
+
+    def allreduce():
+        if world > 1:
+            dist.all_reduce(grads)
+
+    for _ in range(max(3, args.warmup)):
+        fwd(); bwd(); allreduce()
+    torch.cuda.synchronize()
+
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ
+                           else local_rank)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    t_start.record(stream)
+    for k in range(K):
+        ev[k][0].record(stream)
+        fwd()
+        ev[k][1].record(stream)
+        bwd()
+        ev[k][2].record(stream)
+        allreduce()
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    sampler.stop()
+    if world > 1:
+        dist.barrier()
+    ms_total = t_start.elapsed_time(t_end)
+    fwd_ms = statistics.fmean(e[0].elapsed_time(e[1]) for e in ev)
+    bwd_ms = statistics.fmean(e[1].elapsed_time(e[2]) for e in ev)
+    if world > 1:
+        t = torch.tensor([ms_total, fwd_ms, bwd_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total, fwd_ms, bwd_ms = t.tolist()
+    ms_step = ms_total / K
+    value = world * E / (ms_step / 1e3)
+
+    # ---- e2e through the public torch API with host buffers --------------------
+    Ke = args.e2e_steps or min(K, 10)
+    xh = torch.empty((batch, seq, dim), dtype=tdt, pin_memory=True)
+    dyh = torch.empty_like(xh, pin_memory=True)
+    xh.copy_(x.cpu())
+    dyh.copy_(dy.cpu())
+    yh = torch.empty_like(xh, pin_memory=True)
+    dxh = torch.empty_like(xh, pin_memory=True)
+    gh = torch.empty(groups * (M1 + NDEN), dtype=torch.float32, pin_memory=True)
+    ap = torch.nn.Parameter(a.clone())
+    bp = torch.nn.Parameter(b.clone())
+    exact = args.mode == "exact"
+
+    def e2e_step():
+        xd = xh.to(dev, non_blocking=True).requires_grad_(True)
+        dyd = dyh.to(dev, non_blocking=True)
+        yd = GroupRationalFn.apply(xd, ap, bp, exact)
+        yd.backward(dyd)
+        g = torch.cat([ap.grad.reshape(-1), bp.grad.reshape(-1)])
+        if world > 1:
+            dist.all_reduce(g)
+        yh.copy_(yd.detach(), non_blocking=True)
+        dxh.copy_(xd.grad, non_blocking=True)
+        gh.copy_(g, non_blocking=True)
+        ap.grad = None
+        bp.grad = None
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(Ke):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / Ke
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+    e2e_value = world * E / (e2e_ms / 1e3)
+    del xh, dyh, yh, dxh
+
+    if rank != 0:
+        return
+    peak, peak_src = peaks()
+    bwd_bytes = 3 * es * E
+    fwd_bytes = 2 * es * E
+    bwd_gbs = bwd_bytes / (bwd_ms / 1e3) / 1e9
+    fwd_gbs = fwd_bytes / (fwd_ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "f32" if args.dtype == "fp32" else "bf16-io/f32-math",
+        "data": "synthetic: x, dy ~ N(0,1) (torch seeded per rank), coefficients ~ N(0,1) "
+                "(run_bench protocol, pkg/src/grkan/cli.py:146-158)",
+        "config": config_block(args, cfg),
+        "hbm_gbs": (5 * es * E) / (ms_step / 1e3) / 1e9,
+        "roofline": {
+            "bound": "hbm", "kernel": "grkan_bwd (K2 bwd_main + K3 reduce)",
+            "achieved": bwd_gbs, "peak": peak, "unit": "GB/s", "frac": bwd_gbs / peak,
+            "peak_source": peak_src, "traffic": None,
+            "algorithmic_bytes_per_launch": bwd_bytes, "launch_us": bwd_ms * 1e3,
+        },
+        "kernels": {
+            "fwd_us": fwd_ms * 1e3, "fwd_gbs": fwd_gbs, "fwd_frac": fwd_gbs / peak,
+            "bwd_us": bwd_ms * 1e3, "bwd_gbs": bwd_gbs, "bwd_frac": bwd_gbs / peak,
+        },
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * es * E,
+                "d2h_bytes_per_step": 2 * es * E + 4 * groups * (M1 + NDEN),
+                "ms_per_step": e2e_ms, "api": "GroupRationalFn.apply + autograd backward"},
+        "clocks": sampler.summary(),
+        "gpu_launches": 3 * K,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        sb = min(args.cpu_sample_batch, cfg[0])
+        rate, workers, times = cpu_reference_rate(cfg, sb, args.cpu_passes)
+        line["cpu_baseline"] = {
+            "value": rate, "unit": UNIT, "cores": workers, "kind": "port",
+            "sample": "%s with B=%d (E=%d), NumPy port of forward_tensor + backward_blocked "
+                      "(block 256, %d threads), %d timed passes after 1 warm-up"
+                      % (args.config, sb, sb * cfg[1] * cfg[2], workers, len(times)),
+        }
+    print(json.dumps(line), flush=True)
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_b200(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,125 @@
+/*
+ * grkan_b200.h -- C ABI of the B200-native GR-KAN group-rational activation.
+ *
+ * The drop-in boundary for the FlashKAT hot path: plain pointers, sizes and a
+ * CUDA stream handle; no torch or CUDA types in the signatures.  Every call is
+ * stream-ordered, allocation-free, sync-free (except grkan_read_status) and
+ * reentrant; the library keeps no mutable globals besides a once-initialised
+ * device-attribute cache.
+ *
+ * Reference interfaces replaced (all in /root/reference):
+ *   grkan_fwd          forward_tensor(x, params, layout, validate)
+ *                        pkg/src/grkan/rational.py:325-345
+ *                      (element math rational_values, rational.py:218-224)
+ *   grkan_bwd          backward_blocked(x, upstream, params, plan, ...) -> GradBundle
+ *                        pkg/src/grkan/backward.py:275-372
+ *                      (gradient_terms rational.py:227-278, block_partial_totals
+ *                       backward.py:122-139, combine_partials backward.py:142-179,
+ *                       _check_accumulators backward.py:182-184)
+ *   grkan_bwd_workspace_bytes
+ *                      ExecutionPlan.blocked geometry, backward.py:51-98
+ *   grkan_bwd_atomic   backward_naive as the model of the paper's Alg. 1
+ *                        pkg/src/grkan/backward.py:187-246 (comparator only)
+ *   grkan_status       GrkanError taxonomy, pkg/src/grkan/errors.py:4-37
+ *
+ * Tensor layout: x, dy, y, dx are dense row-major [rows, d] (rows = B*L),
+ * element type given by `dtype`.  The feature dim is split into n_groups equal
+ * contiguous groups of width d / n_groups (GroupLayout, rational.py:31-55).
+ * Coefficients: a = [n_groups, m1] (a_0..a_m), b = [n_groups, n] (b_1..b_n),
+ * both float32 for GRKAN_F32 / GRKAN_BF16 tensors and float64 for GRKAN_F64
+ * (the reference casts its fp64 parameters to the tensor dtype at use,
+ * rational.py:220-221).  da/db come back in that same coefficient dtype.
+ */
+#ifndef GRKAN_B200_H_
+#define GRKAN_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GRKAN_API __attribute__((visibility("default")))
+#else
+#define GRKAN_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: the reference's error classes (errors.py:4-37) plus CUDA. */
+typedef enum grkan_status {
+  GRKAN_OK = 0,
+  GRKAN_ERR_LAYOUT = 1,            /* LayoutMismatchError   (rational.py:41-45, 313-322) */
+  GRKAN_ERR_GRID = 2,              /* GridGeometryError     (backward.py:86-98, 298-299) */
+  GRKAN_ERR_NONFINITE_INPUT = 3,   /* NonFiniteInputError   (rational.py:174-179)        */
+  GRKAN_ERR_ACCUM_OVERFLOW = 4,    /* AccumulationOverflowError (backward.py:182-184)    */
+  GRKAN_ERR_UNSUPPORTED = 5,       /* dtype / degree this build does not provide         */
+  GRKAN_ERR_CUDA = 6,              /* a CUDA runtime call failed                         */
+  GRKAN_ERR_INVALID = 7            /* null pointer, short workspace, bad flag            */
+} grkan_status;
+
+/* Element types; 0/1 match the GRKB dump dtype codes (cli.py:54). */
+typedef enum grkan_dtype { GRKAN_F32 = 0, GRKAN_F64 = 1, GRKAN_BF16 = 2 } grkan_dtype;
+
+/* Flags. */
+#define GRKAN_FLAG_FAST 0u         /* FMA + approximate reciprocal; max-scaled <= 1e-5 */
+#define GRKAN_FLAG_EXACT 1u        /* reference op order, IEEE-rounded ops: bitwise y/dx */
+#define GRKAN_FLAG_CHECK_FINITE 2u /* checked mode: flag NaN/Inf inputs (validate=True) */
+
+/* Highest supported degrees (m1 = m + 1 numerator coefficients, n denominator). */
+#define GRKAN_MAX_M1 12
+#define GRKAN_MAX_N 12
+
+GRKAN_API const char* grkan_version(void);
+GRKAN_API const char* grkan_status_string(int status);
+/* Message for the last non-OK status returned on this host thread. */
+GRKAN_API const char* grkan_last_error(void);
+
+/* Device status words written by the kernels (checked mode / overflow). */
+typedef struct grkan_device_status {
+  int32_t nonfinite_input; /* 1 if any x / dy element was NaN or Inf (CHECK_FINITE) */
+  int32_t accum_overflow;  /* 1 if any da / db entry is non-finite                  */
+} grkan_device_status;
+
+/* Forward: y = P(x) / (1 + |A(x)|) per group.  `status` may be NULL unless
+ * GRKAN_FLAG_CHECK_FINITE is set; it is zeroed and then written in-stream. */
+GRKAN_API int grkan_fwd(const void* x, void* y, const void* a, const void* b, int64_t rows, int32_t d,
+              int32_t n_groups, int32_t m1, int32_t n, int32_t dtype, uint32_t flags,
+              grkan_device_status* status, void* stream);
+
+/* Workspace for grkan_bwd: status words + one partial per (row tile, group). */
+GRKAN_API size_t grkan_bwd_workspace_bytes(int64_t rows, int32_t d, int32_t n_groups, int32_t m1,
+                                 int32_t n, int32_t dtype);
+
+/* Backward: dx (like x) and da [n_groups, m1], db [n_groups, n].
+ * Two kernels, no atomics: per-CTA partials, then a fixed-order reduction
+ * (bitwise reproducible run to run).  The device status (overflow, and
+ * non-finite inputs under CHECK_FINITE) lands at the start of `ws`. */
+GRKAN_API int grkan_bwd(const void* x, const void* dy, const void* a, const void* b, void* dx, void* da,
+              void* db, void* ws, size_t ws_bytes, int64_t rows, int32_t d, int32_t n_groups,
+              int32_t m1, int32_t n, int32_t dtype, uint32_t flags, void* stream);
+
+/* The paper's Alg. 1 (per-element global atomicAdd into da/db).  Comparator
+ * for the speed and rounding claims only; not used by the product path.
+ * `status` receives the overflow flag (may be NULL). */
+GRKAN_API int grkan_bwd_atomic(const void* x, const void* dy, const void* a, const void* b, void* dx,
+                     void* da, void* db, int64_t rows, int32_t d, int32_t n_groups, int32_t m1,
+                     int32_t n, int32_t dtype, uint32_t flags, grkan_device_status* status,
+                     void* stream);
+
+/* Synchronise `stream` and copy the device status to the host; maps it to a
+ * status code (NONFINITE_INPUT first, then ACCUM_OVERFLOW, else OK). */
+GRKAN_API int grkan_read_status(const grkan_device_status* status, void* stream,
+                      grkan_device_status* host_out);
+
+/* Launch geometry the library would use (for tests / the access model):
+ * out[0]=vector width, out[1]=threads per CTA, out[2]=rows per tile,
+ * out[3]=row tiles, out[4]=CTAs. */
+GRKAN_API int grkan_plan(int64_t rows, int32_t d, int32_t n_groups, int32_t m1, int32_t n, int32_t dtype,
+               int64_t* out5);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GRKAN_B200_H_ */

@@ -1,0 +1,121 @@
+"""Loader for the in-tree C-ABI library ``_lib/libgrkan_b200.so`` (include/grkan_b200.h).
+
+The library is the product: there is no Python or CPU fallback.  If it is
+missing or fails to load, every entry point raises ``NativeLibraryError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libgrkan_b200.so")
+
+# Status codes and flags (include/grkan_b200.h)
+OK = 0
+ERR_LAYOUT = 1
+ERR_GRID = 2
+ERR_NONFINITE_INPUT = 3
+ERR_ACCUM_OVERFLOW = 4
+ERR_UNSUPPORTED = 5
+ERR_CUDA = 6
+ERR_INVALID = 7
+
+DT_F32 = 0
+DT_F64 = 1
+DT_BF16 = 2
+
+FLAG_FAST = 0
+FLAG_EXACT = 1
+FLAG_CHECK_FINITE = 2
+
+MAX_M1 = 12
+MAX_N = 12
+
+EXPORTS = (
+    "grkan_version", "grkan_status_string", "grkan_last_error", "grkan_fwd",
+    "grkan_bwd_workspace_bytes", "grkan_bwd", "grkan_bwd_atomic", "grkan_read_status",
+    "grkan_plan",
+)
+
+
+class NativeLibraryError(RuntimeError):
+    """The CUDA extension is missing or unusable (no fallback exists)."""
+
+
+class DeviceStatus(ctypes.Structure):
+    _fields_ = [("nonfinite_input", ctypes.c_int32), ("accum_overflow", ctypes.c_int32)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def _declare(L):
+    p, i32, i64, u32, sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
+                            ctypes.c_size_t)
+    L.grkan_version.argtypes = []
+    L.grkan_version.restype = ctypes.c_char_p
+    L.grkan_status_string.argtypes = [ctypes.c_int]
+    L.grkan_status_string.restype = ctypes.c_char_p
+    L.grkan_last_error.argtypes = []
+    L.grkan_last_error.restype = ctypes.c_char_p
+    L.grkan_fwd.argtypes = [p, p, p, p, i64, i32, i32, i32, i32, i32, u32, p, p]
+    L.grkan_fwd.restype = ctypes.c_int
+    L.grkan_bwd_workspace_bytes.argtypes = [i64, i32, i32, i32, i32, i32]
+    L.grkan_bwd_workspace_bytes.restype = sz
+    L.grkan_bwd.argtypes = [p, p, p, p, p, p, p, p, sz, i64, i32, i32, i32, i32, i32, u32, p]
+    L.grkan_bwd.restype = ctypes.c_int
+    L.grkan_bwd_atomic.argtypes = [p, p, p, p, p, p, p, i64, i32, i32, i32, i32, i32, u32, p, p]
+    L.grkan_bwd_atomic.restype = ctypes.c_int
+    L.grkan_read_status.argtypes = [p, p, ctypes.POINTER(DeviceStatus)]
+    L.grkan_read_status.restype = ctypes.c_int
+    L.grkan_plan.argtypes = [i64, i32, i32, i32, i32, i32, ctypes.POINTER(ctypes.c_int64)]
+    L.grkan_plan.restype = ctypes.c_int
+
+
+def lib():
+    """The loaded library (loads on first use; raises NativeLibraryError if absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise NativeLibraryError(
+                    "GR-KAN CUDA library not built: %s is missing "
+                    "(run `python -c 'import __graft_entry__ as g; g.build()'`)" % LIB_PATH)
+            try:
+                L = ctypes.CDLL(LIB_PATH)
+            except OSError as exc:
+                raise NativeLibraryError("cannot load %s: %s" % (LIB_PATH, exc)) from exc
+            for sym in EXPORTS:
+                if not hasattr(L, sym):
+                    raise NativeLibraryError("%s does not export %s" % (LIB_PATH, sym))
+            _declare(L)
+            _lib = L
+    return _lib
+
+
+def version() -> str:
+    return lib().grkan_version().decode()
+
+
+def status_string(code: int) -> str:
+    return lib().grkan_status_string(code).decode()
+
+
+def last_error() -> str:
+    return lib().grkan_last_error().decode()
+
+
+def plan(rows, d, n_groups, m1, n, dtype_code):
+    out = (ctypes.c_int64 * 5)()
+    rc = lib().grkan_plan(rows, d, n_groups, m1, n, dtype_code, out)
+    if rc:
+        from .errors import raise_for_status
+        raise_for_status(rc, last_error())
+    return {"vector_width": out[0], "threads": out[1], "rows_per_tile": out[2],
+            "row_tiles": out[3], "ctas": out[4]}

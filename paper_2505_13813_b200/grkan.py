@@ -1,0 +1,396 @@
+"""Reference-API shim: the ``grkan`` functional interface, executed on the B200.
+
+Same names, argument meaning and error behaviour as the reference package
+(/root/reference/pkg/src/grkan), so code and tests written against
+``grkan.forward_tensor`` / ``grkan.backward_blocked`` run unchanged on the GPU:
+
+    from paper_2505_13813_b200 import grkan
+    y = grkan.forward_tensor(x, params, layout)            # rational.py:325
+    bundle = grkan.backward_blocked(x, up, params, plan)   # backward.py:275
+
+Host NumPy arrays in, host NumPy arrays out (the CPU path's contract); every
+element is computed by the sm_100a kernels.  By default the shim runs the
+EXACT policy (reference op order, IEEE-rounded ops), so ``y`` and ``d_x`` are
+bitwise identical to the reference; ``d_a``/``d_b`` come from the device
+tree reduction (more accurate than either reference strategy, not bitwise).
+Pass ``exact=False`` (or ``set_default_exact(False)``) for the FMA policy.
+
+Differences, all deliberate: ``workers`` is accepted and ignored (the GPU is
+the pool); ``counter``/``coverage`` instrumentation belongs to the reference's
+access model (out of scope) and raises if given; ``backward_naive`` runs the
+paper's Alg. 1 (global atomicAdd), the algorithm the reference's naive
+strategy models, so its d_a/d_b are not bit-reproducible.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Iterator
+
+import numpy as np
+import torch
+
+from . import ops
+from .errors import (  # noqa: F401  (re-exported like grkan/__init__.py)
+    AccumulationOverflowError,
+    ActivationFitError,
+    DegenerateAlphaError,
+    GridGeometryError,
+    GrkanError,
+    LayoutMismatchError,
+    NonFiniteInputError,
+    PartialCoverageError,
+    TailNotCoveredError,
+    UnsupportedError,
+)
+
+STRATEGY_NAIVE = "naive_atomic"           # backward.py:44
+STRATEGY_BLOCKED = "blocked_reduction"    # backward.py:45
+COMBINE_ORDERED = "deterministic_ordered"  # backward.py:46
+COMBINE_UNORDERED = "unordered_scatter"   # backward.py:47
+DEFAULT_BLOCK_SIZE = 256                  # backward.py:48
+
+PRECISION_DTYPES = {"single": np.float32, "double": np.float64}
+DTYPE_PRECISIONS = {np.dtype(np.float32): "single", np.dtype(np.float64): "double"}
+
+_DEFAULT_EXACT = True
+
+
+def set_default_exact(flag: bool) -> None:
+    """Choose the policy used when a call does not pass ``exact=``."""
+    global _DEFAULT_EXACT
+    _DEFAULT_EXACT = bool(flag)
+
+
+def _exact(flag):
+    return _DEFAULT_EXACT if flag is None else bool(flag)
+
+
+def _device():
+    if not torch.cuda.is_available():
+        raise UnsupportedError("the GR-KAN B200 shim needs a CUDA device; there is no CPU path")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+# ---------------------------------------------------------------------------
+# Types (rational.py:31-183, backward.py:51-110)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class GroupLayout:
+    """Equal contiguous groups over the feature dim (rational.py:31-55)."""
+
+    feature_dim: int
+    num_groups: int
+
+    def __post_init__(self):
+        if self.feature_dim < 1 or self.num_groups < 1:
+            raise LayoutMismatchError("layout mismatch: dimensions must be positive")
+        if self.feature_dim % self.num_groups != 0:
+            raise LayoutMismatchError("layout mismatch: feature_dim %d not divisible by num_groups %d"
+                                      % (self.feature_dim, self.num_groups))
+
+    @property
+    def group_width(self) -> int:
+        return self.feature_dim // self.num_groups
+
+    def group_slices(self) -> Iterator[tuple[int, int, int]]:
+        w = self.group_width
+        for g in range(self.num_groups):
+            yield g, g * w, (g + 1) * w
+
+
+@dataclass(frozen=True)
+class GroupRationalParams:
+    """numerator (G, m+1) = a_0..a_m; denominator (G, n) = b_1..b_n; stored fp64 (rational.py:58-129)."""
+
+    numerator: np.ndarray
+    denominator: np.ndarray
+
+    def __post_init__(self):
+        num = np.ascontiguousarray(np.atleast_2d(np.asarray(self.numerator, dtype=np.float64)))
+        den = np.asarray(self.denominator, dtype=np.float64)
+        if den.ndim == 1:
+            den = den.reshape(num.shape[0], -1)
+        den = np.ascontiguousarray(den)
+        if num.ndim != 2 or den.ndim != 2:
+            raise ValueError("coefficient arrays must be 2-D")
+        if num.shape[1] < 1:
+            raise ValueError("numerator needs at least the constant coefficient")
+        if den.shape[0] != num.shape[0]:
+            raise ValueError("numerator and denominator group counts differ")
+        if not (np.isfinite(num).all() and np.isfinite(den).all()):
+            raise NonFiniteInputError("non-finite input: coefficients must be finite")
+        object.__setattr__(self, "numerator", num)
+        object.__setattr__(self, "denominator", den)
+
+    num_groups = property(lambda self: self.numerator.shape[0])
+    num_coeffs = property(lambda self: self.numerator.shape[1])
+    den_coeffs = property(lambda self: self.denominator.shape[1])
+    degrees = property(lambda self: (self.numerator.shape[1] - 1, self.denominator.shape[1]))
+    total_coeffs = property(lambda self: self.numerator.shape[1] + self.denominator.shape[1])
+
+    def group_row(self, g: int):
+        return self.numerator[g], self.denominator[g]
+
+    @classmethod
+    def identity(cls, num_groups: int, degrees=(5, 4)) -> "GroupRationalParams":
+        m, n = degrees
+        if m < 1:
+            raise ValueError("identity needs numerator degree >= 1")
+        num = np.zeros((num_groups, m + 1))
+        num[:, 1] = 1.0
+        return cls(num, np.zeros((num_groups, n)))
+
+    @classmethod
+    def from_row(cls, numerator_row, denominator_row, num_groups: int) -> "GroupRationalParams":
+        num = np.tile(np.asarray(numerator_row, dtype=np.float64), (num_groups, 1))
+        den = np.tile(np.asarray(denominator_row, dtype=np.float64).reshape(1, -1), (num_groups, 1))
+        return cls(num, den)
+
+
+@dataclass
+class ActivationTensor:
+    """Dense (batch, seq, feature) host tensor, f32 or f64 (rational.py:132-183)."""
+
+    data: np.ndarray
+    validated: bool = field(default=False, repr=False)
+
+    def __post_init__(self):
+        arr = np.ascontiguousarray(self.data)
+        if arr.ndim != 3:
+            raise ValueError("activation tensor must be rank 3 (batch, seq, feature)")
+        if arr.dtype not in (np.float32, np.float64):
+            arr = arr.astype(np.float64)
+        self.data = arr
+
+    @classmethod
+    def from_array(cls, arr, validate: bool = True) -> "ActivationTensor":
+        t = cls(np.asarray(arr))
+        if validate:
+            t.check_finite()
+        return t
+
+    batch = property(lambda self: self.data.shape[0])
+    seq = property(lambda self: self.data.shape[1])
+    feature = property(lambda self: self.data.shape[2])
+    num_elements = property(lambda self: self.data.size)
+    precision = property(lambda self: DTYPE_PRECISIONS[self.data.dtype])
+
+    def check_finite(self) -> "ActivationTensor":
+        """Checked mode, evaluated on the device by the forward kernel's finiteness flag."""
+        if not self.validated:
+            if self.data.size:
+                x = torch.from_numpy(self.data).to(_device())
+                a, b = _coeffs(GroupRationalParams.identity(1, (1, 0)), x.dtype, x.device)
+                ops.rational_forward(x.reshape(-1, 1), a, b, exact=False, check_finite=True)
+            self.validated = True
+        return self
+
+    def rows(self) -> np.ndarray:
+        return self.data.reshape(self.batch * self.seq, self.feature)
+
+
+@dataclass(frozen=True)
+class ExecutionPlan:
+    """Grid geometry of one backward pass (backward.py:51-98).
+
+    On the GPU the kernel picks its own tiling; the plan is validated exactly
+    as the reference does so the same inputs raise the same errors.
+    """
+
+    strategy: str
+    block_size: int
+    layout: GroupLayout
+    grid_rows: int
+    grid_cols: int
+
+    def __post_init__(self):
+        if self.strategy not in (STRATEGY_NAIVE, STRATEGY_BLOCKED):
+            raise ValueError("unknown strategy %r" % (self.strategy,))
+        if self.block_size < 1 or self.grid_rows < 1 or self.grid_cols < 1:
+            raise GridGeometryError("grid geometry invalid: non-positive dimension")
+
+    @classmethod
+    def naive(cls, batch, seq, layout, block_size=DEFAULT_BLOCK_SIZE) -> "ExecutionPlan":
+        total = batch * seq * layout.feature_dim
+        return cls(STRATEGY_NAIVE, block_size, layout, -(-total // block_size), 1)
+
+    @classmethod
+    def blocked(cls, batch, seq, layout, block_size=DEFAULT_BLOCK_SIZE) -> "ExecutionPlan":
+        return cls(STRATEGY_BLOCKED, block_size, layout, -(-(batch * seq) // block_size),
+                   layout.num_groups)
+
+    def validate_for(self, x: ActivationTensor) -> None:
+        if self.strategy == STRATEGY_NAIVE:
+            want = (-(-(x.batch * x.seq * x.feature) // self.block_size), 1)
+        else:
+            want = (-(-(x.batch * x.seq) // self.block_size), self.layout.num_groups)
+        if (self.grid_rows, self.grid_cols) != want:
+            raise GridGeometryError("grid geometry invalid: plan %dx%d does not tile tensor (want %dx%d)"
+                                    % (self.grid_rows, self.grid_cols, want[0], want[1]))
+
+
+@dataclass
+class GradBundle:
+    """Backward outputs with provenance (backward.py:101-110)."""
+
+    d_x: ActivationTensor
+    d_a: np.ndarray
+    d_b: np.ndarray
+    strategy: str
+    precision: str
+    combine_mode: str
+
+
+@dataclass(frozen=True)
+class ElementGrads:
+    d_x: float
+    d_a: np.ndarray
+    d_b: np.ndarray
+
+
+# ---------------------------------------------------------------------------
+# Device plumbing
+# ---------------------------------------------------------------------------
+
+def _coeffs(params: GroupRationalParams, tdtype: torch.dtype, device):
+    """Coefficients rounded to the tensor dtype, as the reference casts at use (rational.py:220)."""
+    np_dt = np.float64 if tdtype == torch.float64 else np.float32
+    a = torch.from_numpy(np.ascontiguousarray(params.numerator.astype(np_dt))).to(device)
+    b = torch.from_numpy(np.ascontiguousarray(params.denominator.astype(np_dt))).to(device)
+    return a, b
+
+
+def check_compatible(x: ActivationTensor, params: GroupRationalParams, layout: GroupLayout) -> None:
+    """rational.py:313-322."""
+    if x.feature != layout.feature_dim:
+        raise LayoutMismatchError("layout mismatch: tensor feature dim %d vs layout %d"
+                                  % (x.feature, layout.feature_dim))
+    if params.num_groups != layout.num_groups:
+        raise LayoutMismatchError("layout mismatch: params have %d groups, layout %d"
+                                  % (params.num_groups, layout.num_groups))
+
+
+def _to_device(t: ActivationTensor):
+    return torch.from_numpy(t.data).to(_device(), non_blocking=False)
+
+
+# ---------------------------------------------------------------------------
+# Hot path (rational.py:325-345, backward.py:187-395)
+# ---------------------------------------------------------------------------
+
+def forward_tensor(x: ActivationTensor, params: GroupRationalParams, layout: GroupLayout,
+                   validate: bool = True, exact: bool | None = None) -> ActivationTensor:
+    """Group-wise rational of every element; same shape and precision (rational.py:325-345)."""
+    check_compatible(x, params, layout)
+    xd = _to_device(x)
+    a, b = _coeffs(params, xd.dtype, xd.device)
+    check = validate and not x.validated
+    y = ops.rational_forward(xd, a, b, exact=_exact(exact), check_finite=check)
+    if check:
+        x.validated = True
+    return ActivationTensor(y.cpu().numpy(), validated=False)
+
+
+def _prepare_bwd(x, upstream, params, plan, default_plan):
+    layout = plan.layout if plan is not None else GroupLayout(x.feature, params.num_groups)
+    if plan is None:
+        plan = default_plan(x.batch, x.seq, layout)
+    check_compatible(x, params, layout)
+    if x.data.shape != upstream.data.shape:
+        raise GridGeometryError("grid geometry invalid: x and upstream shapes differ")
+    plan.validate_for(x)
+    return layout, plan
+
+
+def _no_instrumentation(counter, coverage):
+    if counter is not None or coverage is not None:
+        raise UnsupportedError("access-model instrumentation (counter/coverage) is not part of the "
+                               "B200 path; use the reference's access model")
+
+
+def backward_blocked(x: ActivationTensor, upstream: ActivationTensor, params: GroupRationalParams,
+                     plan: ExecutionPlan | None = None, workers: int = 1,
+                     combine_mode: str = COMBINE_ORDERED, validate: bool = True, counter=None,
+                     coverage=None, exact: bool | None = None) -> GradBundle:
+    """Alg. 2 on the B200: dx in one pass, per-CTA partials, fixed-order fold (backward.py:275-372)."""
+    if combine_mode not in (COMBINE_ORDERED, COMBINE_UNORDERED):
+        raise ValueError("unknown combine mode %r" % (combine_mode,))
+    _no_instrumentation(counter, coverage)
+    _prepare_bwd(x, upstream, params, plan, ExecutionPlan.blocked)
+    if upstream.data.dtype != x.data.dtype:
+        upstream = ActivationTensor(upstream.data.astype(x.data.dtype))
+    xd, ud = _to_device(x), _to_device(upstream)
+    a, b = _coeffs(params, xd.dtype, xd.device)
+    check = validate and not (x.validated and upstream.validated)
+    dx, da, db = ops.rational_backward(xd, ud, a, b, exact=_exact(exact), check_finite=check,
+                                       check_overflow=True)
+    if check:
+        x.validated = upstream.validated = True
+    return GradBundle(d_x=ActivationTensor(dx.cpu().numpy()), d_a=da.cpu().numpy(),
+                      d_b=db.cpu().numpy(), strategy=STRATEGY_BLOCKED, precision=x.precision,
+                      combine_mode=combine_mode)
+
+
+def backward_naive(x: ActivationTensor, upstream: ActivationTensor, params: GroupRationalParams,
+                   plan: ExecutionPlan | None = None, validate: bool = True, counter=None,
+                   coverage=None, exact: bool | None = None) -> GradBundle:
+    """The paper's Alg. 1 (per-element atomicAdd), which the reference's naive strategy models
+    (backward.py:187-246).  Comparator only; d_x is identical to backward_blocked's."""
+    _no_instrumentation(counter, coverage)
+    _prepare_bwd(x, upstream, params, plan, ExecutionPlan.naive)
+    if validate and not (x.validated and upstream.validated):
+        x.check_finite()
+        upstream.check_finite()
+    xd, ud = _to_device(x), _to_device(upstream).to(dtype=torch.float64 if x.precision == "double"
+                                                     else torch.float32)
+    a, b = _coeffs(params, xd.dtype, xd.device)
+    dx, da, db = ops.rational_backward_atomic(xd, ud, a, b, exact=_exact(exact), check_overflow=True)
+    return GradBundle(d_x=ActivationTensor(dx.cpu().numpy()), d_a=da.cpu().numpy(),
+                      d_b=db.cpu().numpy(), strategy=STRATEGY_NAIVE, precision=x.precision,
+                      combine_mode=COMBINE_ORDERED)
+
+
+def run_backward(x, upstream, params, plan: ExecutionPlan, workers: int = 1,
+                 combine_mode: str = COMBINE_ORDERED, validate: bool = True, counter=None,
+                 coverage=None, exact: bool | None = None) -> GradBundle:
+    """Dispatch on the plan's strategy tag (backward.py:375-395)."""
+    if plan.strategy == STRATEGY_NAIVE:
+        return backward_naive(x, upstream, params, plan, validate=validate, counter=counter,
+                              coverage=coverage, exact=exact)
+    return backward_blocked(x, upstream, params, plan, workers=workers, combine_mode=combine_mode,
+                            validate=validate, counter=counter, coverage=coverage, exact=exact)
+
+
+# ---------------------------------------------------------------------------
+# Scalar entry points (rational.py:285-310): one-element fp64 tensors on the GPU
+# ---------------------------------------------------------------------------
+
+def _scalar_params(numerator, denominator):
+    num = np.asarray(numerator, dtype=np.float64).reshape(1, -1)
+    den = np.asarray(denominator, dtype=np.float64).reshape(1, -1)
+    return GroupRationalParams(num, den)
+
+
+def eval_rational(x: float, numerator, denominator, validate: bool = True) -> float:
+    if validate and not np.isfinite(x):
+        raise NonFiniteInputError("non-finite input")
+    t = ActivationTensor(np.array([[[x]]], dtype=np.float64), validated=True)
+    y = forward_tensor(t, _scalar_params(numerator, denominator), GroupLayout(1, 1), validate=False,
+                       exact=True)
+    return float(y.data.reshape(-1)[0])
+
+
+def elementwise_grads(x: float, upstream: float, numerator, denominator,
+                      validate: bool = True) -> ElementGrads:
+    if validate and not (np.isfinite(x) and np.isfinite(upstream)):
+        raise NonFiniteInputError("non-finite input")
+    params = _scalar_params(numerator, denominator)
+    t = ActivationTensor(np.array([[[x]]], dtype=np.float64), validated=True)
+    u = ActivationTensor(np.array([[[upstream]]], dtype=np.float64), validated=True)
+    xd, ud = _to_device(t), _to_device(u)
+    a, b = _coeffs(params, xd.dtype, xd.device)
+    dx, da, db = ops.rational_backward(xd, ud, a, b, exact=True)
+    return ElementGrads(d_x=float(dx.reshape(-1)[0]), d_a=da.cpu().numpy().reshape(-1),
+                        d_b=db.cpu().numpy().reshape(-1))

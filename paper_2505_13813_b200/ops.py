@@ -1,0 +1,189 @@
+"""Torch-facing entry points onto the C ABI (include/grkan_b200.h).
+
+PyTorch supplies device memory, the current CUDA stream and the caching
+allocator (for the backward workspace); all arithmetic happens in the sm_100a
+kernels of ``_lib/libgrkan_b200.so``.  Nothing here computes on the CPU and
+there is no fallback: a CPU tensor or a missing library raises.
+
+Public functions
+  rational_forward(x, a, b)            -> y        (grkan_fwd)
+  rational_backward(x, dy, a, b)       -> dx, da, db (grkan_bwd: K2 + K3)
+  rational_backward_atomic(x, dy, a, b)-> dx, da, db (grkan_bwd_atomic, Alg. 1 comparator)
+and the torch.library ops ``grkan_b200::rational_fwd`` / ``rational_bwd``
+(graph-capturable, torch.compile-traceable through their fake kernels).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _native as N
+from .errors import LayoutMismatchError, UnsupportedError, raise_for_status
+
+_DT = {torch.float32: N.DT_F32, torch.bfloat16: N.DT_BF16, torch.float64: N.DT_F64}
+
+
+def coeff_dtype(x_dtype: torch.dtype) -> torch.dtype:
+    """Coefficient / gradient dtype for a tensor dtype (fp64 for fp64, else fp32)."""
+    return torch.float64 if x_dtype == torch.float64 else torch.float32
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream(dev):
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def _validate(x: torch.Tensor, a: torch.Tensor, b: torch.Tensor):
+    if x.dtype not in _DT:
+        raise UnsupportedError("tensor dtype %s not supported (float32, bfloat16, float64)" % x.dtype)
+    if not x.is_cuda:
+        raise UnsupportedError("GR-KAN B200 kernels need CUDA tensors (got %s); there is no CPU path"
+                               % x.device)
+    if x.dim() < 1:
+        raise LayoutMismatchError("layout mismatch: tensor needs a feature dimension")
+    if a.dim() != 2 or b.dim() != 2 or a.shape[0] != b.shape[0]:
+        raise LayoutMismatchError("layout mismatch: a must be [groups, m+1], b [groups, n]")
+    cd = coeff_dtype(x.dtype)
+    if a.dtype != cd or b.dtype != cd:
+        raise UnsupportedError("coefficients must be %s for %s tensors" % (cd, x.dtype))
+    if a.device != x.device or b.device != x.device:
+        raise UnsupportedError("coefficients must live on %s" % x.device)
+    d = x.shape[-1]
+    ng = a.shape[0]
+    if d < 1 or ng < 1 or d % ng:
+        raise LayoutMismatchError("layout mismatch: feature_dim %d not divisible by num_groups %d"
+                                  % (d, ng))
+    rows = x.numel() // d if d else 0
+    return rows, d, ng, a.shape[1], b.shape[1]
+
+
+def _flags(exact: bool, check_finite: bool) -> int:
+    return (N.FLAG_EXACT if exact else N.FLAG_FAST) | (N.FLAG_CHECK_FINITE if check_finite else 0)
+
+
+def _raise(rc):
+    if rc != N.OK:
+        raise_for_status(rc, N.last_error())
+
+
+def read_status(status: torch.Tensor) -> None:
+    """Synchronise and raise NonFiniteInputError / AccumulationOverflowError if flagged."""
+    host = N.DeviceStatus()
+    rc = N.lib().grkan_read_status(status.data_ptr(), _stream(status.device), host)
+    _raise(rc)
+
+
+def rational_forward(x: torch.Tensor, a: torch.Tensor, b: torch.Tensor, exact: bool = False,
+                     check_finite: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
+    """y = P(x)/(1+|A(x)|) per group (forward_tensor, pkg/src/grkan/rational.py:325-345).
+
+    With ``check_finite`` the kernel flags NaN/Inf inputs and this call
+    synchronises to raise NonFiniteInputError (the reference's validate=True).
+    """
+    rows, d, ng, m1, n = _validate(x, a, b)
+    x = x.contiguous()
+    a = a.contiguous()
+    b = b.contiguous()
+    y = torch.empty_like(x) if out is None else out
+    status = torch.zeros(2, dtype=torch.int32, device=x.device) if check_finite else None
+    with torch.cuda.device(x.device):
+        rc = N.lib().grkan_fwd(x.data_ptr(), y.data_ptr(), a.data_ptr(), _ptr(b), rows, d, ng, m1, n,
+                               _DT[x.dtype], _flags(exact, check_finite), _ptr(status),
+                               _stream(x.device))
+        _raise(rc)
+        if check_finite:
+            read_status(status)
+    return y
+
+
+def workspace_bytes(rows: int, d: int, ng: int, m1: int, n: int, dtype: torch.dtype) -> int:
+    nbytes = N.lib().grkan_bwd_workspace_bytes(rows, d, ng, m1, n, _DT[dtype])
+    if nbytes == 0:
+        raise LayoutMismatchError("layout mismatch: cannot size workspace for d=%d groups=%d" % (d, ng))
+    return nbytes
+
+
+def rational_backward(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor, b: torch.Tensor,
+                      exact: bool = False, check_finite: bool = False, check_overflow: bool = False,
+                      workspace: torch.Tensor | None = None):
+    """(dx, da, db) with per-CTA partials and a deterministic second pass.
+
+    Mirrors backward_blocked (pkg/src/grkan/backward.py:275-372).  da/db are
+    in the coefficient dtype (fp32 for fp32/bf16 tensors).  ``check_overflow``
+    synchronises and raises AccumulationOverflowError for non-finite da/db
+    (_check_accumulators, backward.py:182-184); ``check_finite`` also flags
+    NaN/Inf in x / dy (validate=True).
+    """
+    rows, d, ng, m1, n = _validate(x, a, b)
+    if dy.shape != x.shape:
+        from .errors import GridGeometryError
+        raise GridGeometryError("grid geometry invalid: x and upstream shapes differ")
+    if dy.dtype != x.dtype or dy.device != x.device:
+        raise UnsupportedError("upstream must match x in dtype and device")
+    x = x.contiguous()
+    dy = dy.contiguous()
+    a = a.contiguous()
+    b = b.contiguous()
+    dx = torch.empty_like(x)
+    da = torch.empty((ng, m1), dtype=a.dtype, device=x.device)
+    db = torch.empty((ng, n), dtype=a.dtype, device=x.device)
+    nbytes = workspace_bytes(rows, d, ng, m1, n, x.dtype)
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+    with torch.cuda.device(x.device):
+        rc = N.lib().grkan_bwd(x.data_ptr(), dy.data_ptr(), a.data_ptr(), _ptr(b), dx.data_ptr(),
+                               da.data_ptr(), _ptr(db), workspace.data_ptr(), workspace.numel(),
+                               rows, d, ng, m1, n, _DT[x.dtype], _flags(exact, check_finite),
+                               _stream(x.device))
+        _raise(rc)
+        if check_finite or check_overflow:
+            read_status(workspace[:8])
+    return dx, da, db
+
+
+def rational_backward_atomic(x, dy, a, b, exact: bool = False, check_overflow: bool = False):
+    """The paper's Alg. 1 (per-element global atomicAdd): comparator only, not the product path."""
+    rows, d, ng, m1, n = _validate(x, a, b)
+    x = x.contiguous()
+    dy = dy.contiguous()
+    dx = torch.empty_like(x)
+    da = torch.empty((ng, m1), dtype=a.dtype, device=x.device)
+    db = torch.empty((ng, n), dtype=a.dtype, device=x.device)
+    status = torch.zeros(2, dtype=torch.int32, device=x.device)
+    with torch.cuda.device(x.device):
+        rc = N.lib().grkan_bwd_atomic(x.data_ptr(), dy.data_ptr(), a.contiguous().data_ptr(),
+                                      _ptr(b.contiguous()), dx.data_ptr(), da.data_ptr(), _ptr(db),
+                                      rows, d, ng, m1, n, _DT[x.dtype], _flags(exact, False),
+                                      status.data_ptr(), _stream(x.device))
+        _raise(rc)
+        if check_overflow:
+            read_status(status)
+    return dx, da, db
+
+
+# ---------------------------------------------------------------------------
+# torch.library registration (CUDA graphs / torch.compile see opaque ops)
+# ---------------------------------------------------------------------------
+
+@torch.library.custom_op("grkan_b200::rational_fwd", mutates_args=(), device_types="cuda")
+def rational_fwd_op(x: torch.Tensor, a: torch.Tensor, b: torch.Tensor, exact: bool) -> torch.Tensor:
+    return rational_forward(x, a, b, exact=exact)
+
+
+@rational_fwd_op.register_fake
+def _(x, a, b, exact):
+    return torch.empty_like(x)
+
+
+@torch.library.custom_op("grkan_b200::rational_bwd", mutates_args=(), device_types="cuda")
+def rational_bwd_op(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor, b: torch.Tensor,
+                    exact: bool) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    return rational_backward(x, dy, a, b, exact=exact)
+
+
+@rational_bwd_op.register_fake
+def _(x, dy, a, b, exact):
+    return torch.empty_like(x), a.new_empty(a.shape), b.new_empty(b.shape)

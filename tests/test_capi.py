@@ -1,0 +1,99 @@
+"""C-ABI library: loads, exports every symbol include/*.h declares, validates on the host.
+
+CPU-only: nothing here launches a kernel.
+"""
+
+import ctypes
+import glob
+import os
+import re
+
+import pytest
+
+from paper_2505_13813_b200 import _native as N
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        names |= set(re.findall(r"GRKAN_API\s+[\w\s\*]+?\b(grkan_\w+)\s*\(", src))
+    return names
+
+
+def test_header_declares_the_boundary():
+    assert declared_symbols() == set(N.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = N.lib()
+    for sym in declared_symbols():
+        assert hasattr(lib, sym), sym
+    out = os.popen("nm -D --defined-only %s" % N.LIB_PATH).read()
+    for sym in declared_symbols():
+        assert re.search(r"\bT %s\b" % sym, out), sym
+
+
+def test_library_built_for_sm100a():
+    out = os.popen("cuobjdump --list-elf %s 2>&1" % N.LIB_PATH).read()
+    assert "sm_100a" in out, out
+
+
+def test_version_and_status_strings():
+    assert "sm_100a" in N.version()
+    assert N.status_string(N.OK) == "ok"
+    assert N.status_string(N.ERR_LAYOUT) == "layout mismatch"
+    assert N.status_string(N.ERR_ACCUM_OVERFLOW) == "accumulation overflow"
+
+
+def test_host_validation_without_gpu():
+    L = N.lib()
+    # layout mismatch: d not divisible by groups (GroupLayout, rational.py:41-45)
+    rc = L.grkan_fwd(None, None, None, None, 4, 10, 4, 6, 4, N.DT_F32, 0, None, None)
+    assert rc == N.ERR_LAYOUT and "not divisible" in N.last_error()
+    rc = L.grkan_fwd(None, None, None, None, 4, 0, 1, 6, 4, N.DT_F32, 0, None, None)
+    assert rc == N.ERR_LAYOUT
+    rc = L.grkan_fwd(None, None, None, None, 4, 8, 2, 6, 4, 9, 0, None, None)
+    assert rc == N.ERR_UNSUPPORTED
+    rc = L.grkan_fwd(None, None, None, None, 4, 8, 2, 13, 4, N.DT_F32, 0, None, None)
+    assert rc == N.ERR_UNSUPPORTED
+    rc = L.grkan_fwd(None, None, None, None, 4, 8, 2, 0, 4, N.DT_F32, 0, None, None)
+    assert rc == N.ERR_INVALID
+    rc = L.grkan_fwd(None, None, None, None, -1, 8, 2, 6, 4, N.DT_F32, 0, None, None)
+    assert rc == N.ERR_GRID
+    rc = L.grkan_fwd(None, None, None, None, 4, 8, 2, 6, 4, N.DT_F32, 0x10, None, None)
+    assert rc == N.ERR_INVALID
+    rc = L.grkan_fwd(None, None, None, None, 4, 8, 2, 6, 4, N.DT_F32, N.FLAG_CHECK_FINITE, None, None)
+    assert rc == N.ERR_INVALID  # checked mode needs a status block
+    rc = L.grkan_bwd(None, None, None, None, None, None, None, None, 0, 4, 8, 2, 6, 4, N.DT_F32, 0, None)
+    assert rc == N.ERR_INVALID
+    assert L.grkan_bwd_workspace_bytes(4, 10, 4, 6, 4, N.DT_F32) == 0
+
+
+@pytest.mark.parametrize("dtype,es", [(N.DT_F32, 4), (N.DT_BF16, 2), (N.DT_F64, 8)])
+def test_plan_geometry(dtype, es):
+    for rows, d, g in [(256 * 197, 3072, 8), (128 * 197, 1536, 8), (8 * 197, 192, 8), (9, 8, 2),
+                       (5 * 7, 12, 4), (2 * 9, 3072, 1), (10, 64, 64)]:
+        p = N.plan(rows, d, g, 6, 4, dtype)
+        dg = d // g
+        w = p["vector_width"]
+        assert w in (1, 16 // es)
+        if (dg * es) % 16 == 0:
+            assert w == 16 // es
+        assert dg % w == 0
+        assert p["threads"] % 32 == 0 or p["threads"] < 32 or p["threads"] == dg // w * 1
+        assert 0 < p["threads"] <= 512
+        assert p["row_tiles"] * p["rows_per_tile"] >= rows
+        assert (p["row_tiles"] - 1) * p["rows_per_tile"] < rows
+        assert p["ctas"] == p["row_tiles"] * g
+        ws = N.lib().grkan_bwd_workspace_bytes(rows, d, g, 6, 4, dtype)
+        acc = 8 if dtype == N.DT_F64 else 4
+        assert ws >= 256 + p["ctas"] * 10 * acc
+
+
+def test_kat_b_plan_is_wide():
+    p = N.plan(256 * 197, 3072, 8, 6, 4, N.DT_F32)
+    assert p["vector_width"] == 4 and p["threads"] == 288
+    assert p["ctas"] >= 4 * 148 * 4  # many waves: the HW block scheduler balances the tail
