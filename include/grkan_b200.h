@@ -112,11 +112,12 @@ GRKAN_API int grkan_bwd_atomic(const void* x, const void* dy, const void* a, con
 GRKAN_API int grkan_read_status(const grkan_device_status* status, void* stream,
                       grkan_device_status* host_out);
 
-/* Launch geometry the library would use (for tests / the access model):
- * out[0]=vector width, out[1]=threads per CTA, out[2]=rows per tile,
- * out[3]=row tiles, out[4]=CTAs. */
+/* Backward launch geometry for 16-byte-aligned tensors on a 148-SM B200 (for
+ * tests / the access model): out[0]=vector width, out[1]=threads per CTA,
+ * out[2]=rows per tile (direct kernels) or per pipeline stage (staged),
+ * out[3]=partials per group, out[4]=CTAs, out[5]=1 if TMA-staged. */
 GRKAN_API int grkan_plan(int64_t rows, int32_t d, int32_t n_groups, int32_t m1, int32_t n, int32_t dtype,
-               int64_t* out5);
+                         int64_t* out6);
 
 #ifdef __cplusplus
 }

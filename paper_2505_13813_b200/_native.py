@@ -112,10 +112,10 @@ def last_error() -> str:
 
 
 def plan(rows, d, n_groups, m1, n, dtype_code):
-    out = (ctypes.c_int64 * 5)()
+    out = (ctypes.c_int64 * 6)()
     rc = lib().grkan_plan(rows, d, n_groups, m1, n, dtype_code, out)
     if rc:
         from .errors import raise_for_status
         raise_for_status(rc, last_error())
-    return {"vector_width": out[0], "threads": out[1], "rows_per_tile": out[2],
-            "row_tiles": out[3], "ctas": out[4]}
+    return {"vector_width": out[0], "threads": out[1], "rows_per_unit": out[2],
+            "partials_per_group": out[3], "ctas": out[4], "staged": bool(out[5])}

@@ -1,29 +1,30 @@
 """Build the in-tree CUDA library ``_lib/libgrkan_b200.so`` for sm_100a.
 
-    python -m paper_2505_13813_b200.build [--force]
+    python -m paper_2505_13813_b200.build [--force] [--ptxas-v]
 
-nvcc cross-compiles without a GPU; the .so is git-ignored but travels to the
-GPU box with the repo snapshot.
+One nvcc process per translation unit (host C ABI + one kernel TU per I/O
+dtype), run in parallel, then one shared-library link.  nvcc cross-compiles
+without a GPU; the .so is git-ignored but travels to the GPU box with the repo.
 """
 
 from __future__ import annotations
 
+import glob
 import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = os.path.join(HERE, "csrc", "grkan_capi.cu")
-DEPS = [SRC, os.path.join(HERE, "csrc", "grkan_kernels.cuh"), os.path.join(HERE, "csrc", "grkan_math.cuh"),
-        os.path.join(ROOT, "include", "grkan_b200.h")]
+CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib", "libgrkan_b200.so")
+OBJ_DIR = os.path.join(HERE, "_lib", "obj")
 
-NVCC_FLAGS = [
-    "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-    "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-shared",
-]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
+              "-fvisibility=hidden", "-I", os.path.join(ROOT, "include")] + ARCH
 
 
 def nvcc() -> str:
@@ -33,19 +34,45 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+def sources():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+
+
+def deps():
+    return sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
+        [os.path.join(ROOT, "include", "grkan_b200.h"), os.path.abspath(__file__)]
+
+
 def up_to_date() -> bool:
     if not os.path.exists(OUT):
         return False
     t = os.path.getmtime(OUT)
-    return all(os.path.getmtime(p) <= t for p in DEPS)
+    return all(os.path.getmtime(p) <= t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
+def build(force: bool = False, verbose: bool = True, ptxas_v: bool = False) -> str:
     if not force and up_to_date():
         return OUT
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    cc = nvcc()
+    extra = ["-Xptxas", "-v"] if ptxas_v else []
+
+    def compile_one(src):
+        obj = os.path.join(OBJ_DIR, os.path.basename(src) + ".o")
+        cmd = [cc] + NVCC_FLAGS + extra + ["-c", "-o", obj, src]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("nvcc failed for %s:\n%s" % (src, r.stderr))
+        return obj, r.stderr
+
+    with ThreadPoolExecutor(max_workers=len(sources())) as pool:
+        results = list(pool.map(compile_one, sources()))
+    if ptxas_v:
+        with open(os.path.join(OBJ_DIR, "ptxas.log"), "w") as fh:
+            for _, log in results:
+                fh.write(log)
     tmp = OUT + ".tmp"
-    cmd = [nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", tmp, SRC]
+    cmd = [cc] + ARCH + ["-shared", "-o", tmp] + [o for o, _ in results]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
@@ -54,4 +81,4 @@ def build(force: bool = False, verbose: bool = True) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
+    build(force="--force" in sys.argv, ptxas_v="--ptxas-v" in sys.argv)

@@ -1,5 +1,5 @@
 // grkan_capi.cu -- the C ABI (include/grkan_b200.h): validation, launch planning
-// and dispatch onto the sm_100a kernels in grkan_kernels.cuh.
+// and dispatch onto the per-dtype launchers (grkan_inst_*.cu -> grkan_kernels.cuh).
 //
 // Host-side argument checks mirror the reference's synchronous errors:
 //   layout   GroupLayout.__post_init__ / check_compatible (rational.py:38-45, 313-322)
@@ -11,9 +11,10 @@
 #include <cstdio>
 #include <cstring>
 #include <numeric>
+#include <cstdlib>
 
 #include "../../include/grkan_b200.h"
-#include "grkan_kernels.cuh"
+#include "grkan_types.h"
 
 #define GRKAN_VERSION_STRING "grkan_b200 0.1.0 (sm_100a)"
 
@@ -60,62 +61,94 @@ size_t elem_size(int dtype) {
 }
 size_t acc_size(int dtype) { return dtype == GRKAN_F64 ? 8 : 4; }
 
-struct Plan {
-  int W = 1;
-  int threads = 0;
-  int64_t ctas = 0;
-  Geom geo{};
-};
+using grkan::Plan;
 
 constexpr int kEltsPerThread = 64;  // target elements per thread per CTA
-constexpr int kTargetThreads = 256;
 
-Plan make_plan(int64_t rows, int32_t d, int32_t ng, size_t es, bool vec, int sms) {
+// Tile geometry: one CTA per (row tile, group); R rows chosen so each of the
+// kBlock threads handles ~kEltsPerThread elements and, when cheap, so the
+// tile's vector count is a whole number of unrolled steps (no ragged steps).
+// GRKAN_STAGED=0 in the environment selects the register-direct kernels even
+// where the TMA-staged ones apply (A/B measurements; results are identical
+// for y/dx and within fp32 reassociation for da/db).
+// The forward defaults to the register-direct kernel (measured faster: one
+// tensor in, four 16-byte loads in flight per thread already saturate HBM);
+// GRKAN_STAGED_FWD=1 selects the staged forward.
+bool staged_enabled(int nt) {
+  const char* v = getenv(nt == 1 ? "GRKAN_STAGED_FWD" : "GRKAN_STAGED");
+  if (nt == 1) return v && v[0] == '1';
+  return !(v && v[0] == '0');
+}
+
+constexpr int kStagesPerTensorPair = 4;  // backward ring depth (2 tensors)
+constexpr int kStagesSingle = 4;         // forward ring depth (1 tensor)
+constexpr size_t kSmemPerSm = 228 * 1024;
+
+// nt = tensors streamed in (1 forward, 2 backward).
+Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_t es, bool vec, int nt,
+               int sms) {
   Plan p;
   const int dg = d / ng;
+  p.geo.one = 1.0f;
   p.W = vec ? static_cast<int>(16 / es) : 1;
-  const int U = p.W >= 8 ? 2 : 4;  // must match grkan::Unroll
-  const int V = dg / p.W;
-  int CT, RPB;
-  if (V <= 384) {
-    CT = V;
-    const int step = 32 / std::gcd(V, 32);  // makes CT * RPB a multiple of 32
-    long k = lround(static_cast<double>(kTargetThreads) / (static_cast<double>(V) * step));
-    if (k < 1) k = 1;
-    RPB = static_cast<int>(step * k);
-    if (CT * RPB > grkan::kMaxThreads) {
-      CT = 256;
-      RPB = 1;
-    }
-  } else {
-    CT = 256;
-    RPB = 1;
+  if (vec && m1 == 6 && n == 4 && dg / p.W <= grkan::kStageVecsHost && staged_enabled(nt)) {
+    // TMA-staged persistent kernels (grkan_staged.cuh)
+    const int V = dg / p.W;
+    const int RS = grkan::kStageVecsHost / V;
+    const int64_t nsu = rows > 0 ? (rows + RS - 1) / RS : 0;
+    p.staged = true;
+    p.stages = nt == 2 ? kStagesPerTensorPair : kStagesSingle;
+    p.smem = static_cast<size_t>(p.stages) * nt * RS * dg * es;
+    const int occ_regs = nt == 2 ? grkan::kBwdCtasPerSmHost : grkan::kFwdCtasPerSmHost;
+    int occ = static_cast<int>(kSmemPerSm / (p.smem + 2048));
+    occ = occ < 1 ? 1 : (occ > occ_regs ? occ_regs : occ);
+    const int64_t slots = static_cast<int64_t>(sms) * occ;
+    int64_t pg = slots / ng;
+    if (pg > nsu) pg = nsu;
+    if (pg < 1) pg = 1;
+    p.threads = grkan::kStagedThreadsHost;
+    p.geo.rows = rows;
+    p.geo.d = d;
+    p.geo.ng = ng;
+    p.geo.dg = dg;
+    p.geo.V = V;
+    p.geo.R = 0;
+    p.geo.RS = RS;
+    p.geo.nsu = nsu;
+    p.geo.pg = static_cast<int32_t>(pg);
+    p.geo.n_tiles = pg;
+    p.ctas = rows > 0 ? pg * ng : 0;
+    return p;
   }
-  const int col_iters = (V + CT - 1) / CT;
-  auto rows_per_thread = [&](int ept) {
-    int ptr = (ept + p.W * col_iters - 1) / (p.W * col_iters);
-    ptr = ((ptr + U - 1) / U) * U;
-    return ptr < U ? U : ptr;
-  };
-  int ptr = rows_per_thread(kEltsPerThread);
-  int64_t R = static_cast<int64_t>(RPB) * ptr;
-  int64_t n_tiles = (rows + R - 1) / R;
+  const int U = nt == 1 ? 4 : grkan::unroll_for_width(p.W);  // = Engine::UF / Engine::U
+  const int V = dg / p.W;
+  const int64_t step = static_cast<int64_t>(grkan::kBlock) * U;
+  const int64_t target_vecs = static_cast<int64_t>(grkan::kBlock) * kEltsPerThread / p.W;
+  int64_t R = (target_vecs + V - 1) / V;
+  if (R < 1) R = 1;
+  for (int64_t r = R; r <= 2 * R; ++r) {
+    if ((r * V) % step == 0) {
+      R = r;
+      break;
+    }
+  }
+  if (rows > 0 && R > rows) R = rows;
+  int64_t n_tiles = rows > 0 ? (rows + R - 1) / R : 0;
   // small tensors: shrink tiles until there are a few CTAs per SM
-  while (ptr > U && n_tiles * ng < 4LL * sms) {
-    ptr = ((ptr / 2 + U - 1) / U) * U;
-    R = static_cast<int64_t>(RPB) * ptr;
+  while (R > 1 && n_tiles * ng < 4LL * sms) {
+    R = (R + 1) / 2;
     n_tiles = (rows + R - 1) / R;
   }
-  p.threads = CT * RPB;
+  p.threads = grkan::kBlock;
   p.geo.rows = rows;
   p.geo.n_tiles = n_tiles;
   p.geo.d = d;
   p.geo.ng = ng;
   p.geo.dg = dg;
   p.geo.V = V;
-  p.geo.CT = CT;
-  p.geo.RPB = RPB;
   p.geo.R = static_cast<int32_t>(R);
+  p.geo.dr = grkan::kBlock / V;
+  p.geo.dc = grkan::kBlock % V;
   p.ctas = n_tiles * ng;
   return p;
 }
@@ -148,46 +181,22 @@ int check_layout(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, int
   return GRKAN_OK;
 }
 
-// ---------------------------------------------------------------------------
-// Compile-time dispatch: dtype x {fast, exact} x {(6,4) fixed, generic <=12/12}
-// x {128-bit vector, scalar}.
-// ---------------------------------------------------------------------------
-template <typename T>
-struct TT {
-  using type = T;
-};
-template <bool B>
-struct BT {
-  static constexpr bool value = B;
-};
-template <int I>
-struct IT {
-  static constexpr int value = I;
-};
+using grkan::LaunchArgs;
 
-template <typename F>
-cudaError_t dispatch(int dtype, bool exact, bool fixed, bool vec, F&& f) {
-  auto with_t = [&](auto tt) -> cudaError_t {
-    using T = typename decltype(tt)::type;
-    constexpr int WV = static_cast<int>(16 / sizeof(T));
-    auto with_e = [&](auto et) -> cudaError_t {
-      auto with_f = [&](auto ft) -> cudaError_t {
-        return vec ? f(tt, et, ft, IT<WV>{}) : f(tt, et, ft, IT<1>{});
-      };
-      return fixed ? with_f(BT<true>{}) : with_f(BT<false>{});
-    };
-    return exact ? with_e(BT<true>{}) : with_e(BT<false>{});
-  };
+cudaError_t launch(const char* which, int dtype, const LaunchArgs& L) {
+  const bool f = which[0] == 'f', b = which[0] == 'b';
   switch (dtype) {
-    case GRKAN_F32: return with_t(TT<float>{});
-    case GRKAN_BF16: return with_t(TT<__nv_bfloat16>{});
-    case GRKAN_F64: return with_t(TT<double>{});
+    case GRKAN_F32: return f ? grkan::launch_fwd_f32(L) : b ? grkan::launch_bwd_f32(L) : grkan::launch_atomic_f32(L);
+    case GRKAN_BF16: return f ? grkan::launch_fwd_bf16(L) : b ? grkan::launch_bwd_bf16(L) : grkan::launch_atomic_bf16(L);
+    case GRKAN_F64: return f ? grkan::launch_fwd_f64(L) : b ? grkan::launch_bwd_f64(L) : grkan::launch_atomic_f64(L);
     default: return cudaErrorInvalidValue;
   }
 }
 
-constexpr int kFixM1 = 6, kFixN = 4;  // the paper's degrees (5, 4)
-constexpr int kGenM1 = GRKAN_MAX_M1, kGenN = GRKAN_MAX_N;
+bool plan_fits(const Plan& p) {
+  return p.ctas <= 0x7fffffffLL && static_cast<int64_t>(p.geo.R) * p.geo.V <= 0x7fffffffLL &&
+         (!p.staged || p.smem <= 227 * 1024);
+}
 
 size_t ws_bytes_for(const Plan& p, int32_t m1, int32_t n, int32_t dtype) {
   const size_t part = static_cast<size_t>(p.geo.ng) * (m1 + n) * p.geo.n_tiles * acc_size(dtype);
@@ -217,17 +226,18 @@ const char* grkan_status_string(int status) {
 }
 
 int grkan_plan(int64_t rows, int32_t d, int32_t n_groups, int32_t m1, int32_t n, int32_t dtype,
-               int64_t* out5) {
+               int64_t* out6) {
   int rc = check_layout(rows, d, n_groups, m1, n, dtype, 0);
   if (rc) return rc;
-  if (!out5) return fail(GRKAN_ERR_INVALID, "null output");
+  if (!out6) return fail(GRKAN_ERR_INVALID, "null output");
   const size_t es = elem_size(dtype);
-  const Plan p = make_plan(rows, d, n_groups, es, vec_ok(d, n_groups, es, {}), 148);
-  out5[0] = p.W;
-  out5[1] = p.threads;
-  out5[2] = p.geo.R;
-  out5[3] = p.geo.n_tiles;
-  out5[4] = p.ctas;
+  const Plan p = make_plan(rows, d, n_groups, m1, n, es, vec_ok(d, n_groups, es, {}), 2, 148);
+  out6[0] = p.W;
+  out6[1] = p.threads;
+  out6[2] = p.staged ? p.geo.RS : p.geo.R;
+  out6[3] = p.geo.n_tiles;
+  out6[4] = p.ctas;
+  out6[5] = p.staged ? 1 : 0;
   return GRKAN_OK;
 }
 
@@ -241,8 +251,9 @@ size_t grkan_bwd_workspace_bytes(int64_t rows, int32_t d, int32_t n_groups, int3
   // (an SM count no device reaches), which bounds every plan grkan_bwd can pick.
   const int kAnySms = 1 << 20;
   const bool can_vec = vec_ok(d, n_groups, es, {});
-  const size_t a = can_vec ? ws_bytes_for(make_plan(rows, d, n_groups, es, true, kAnySms), m1, n, dtype) : 0;
-  const size_t b = ws_bytes_for(make_plan(rows, d, n_groups, es, false, kAnySms), m1, n, dtype);
+  const size_t a =
+      can_vec ? ws_bytes_for(make_plan(rows, d, n_groups, m1, n, es, true, 2, kAnySms), m1, n, dtype) : 0;
+  const size_t b = ws_bytes_for(make_plan(rows, d, n_groups, m1, n, es, false, 2, kAnySms), m1, n, dtype);
   return a > b ? a : b;
 }
 
@@ -262,23 +273,22 @@ int grkan_fwd(const void* x, void* y, const void* a, const void* b, int64_t rows
   if (!x || !y || !a || (n > 0 && !b)) return fail(GRKAN_ERR_INVALID, "null tensor pointer");
   const size_t es = elem_size(dtype);
   const bool vec = vec_ok(d, n_groups, es, {x, y});
-  const Plan p = make_plan(rows, d, n_groups, es, vec, sm_count());
-  if (p.ctas > 0x7fffffffLL) return fail(GRKAN_ERR_GRID, "grid geometry invalid: %lld CTAs", (long long)p.ctas);
-  const bool fixed = (m1 == kFixM1 && n == kFixN);
-  DevStatus* st = reinterpret_cast<DevStatus*>(status);
-  cudaError_t e = dispatch(dtype, flags & GRKAN_FLAG_EXACT, fixed, vec, [&](auto tt, auto et, auto ft, auto wt) {
-    using T = typename decltype(tt)::type;
-    constexpr bool E = decltype(et)::value;
-    constexpr bool FX = decltype(ft)::value;
-    constexpr int W = decltype(wt)::value;
-    using A = typename grkan::VecIO<T, W>::A;
-    constexpr int MM1 = FX ? kFixM1 : kGenM1;
-    constexpr int MN = FX ? kFixN : kGenN;
-    grkan::k_fwd<T, E, MM1, MN, FX, W><<<static_cast<unsigned>(p.ctas), p.threads, 0, s>>>(
-        static_cast<const T*>(x), static_cast<T*>(y), static_cast<const A*>(a),
-        static_cast<const A*>(b), p.geo, m1, n, check ? 1 : 0, st);
-    return cudaGetLastError();
-  });
+  const Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 1, sm_count());
+  if (!plan_fits(p)) return fail(GRKAN_ERR_GRID, "grid geometry invalid: %lld CTAs", (long long)p.ctas);
+  LaunchArgs L{};
+  L.plan = &p;
+  L.x = x;
+  L.out = y;
+  L.a = a;
+  L.b = b;
+  L.st = reinterpret_cast<DevStatus*>(status);
+  L.m1 = m1;
+  L.n = n;
+  L.exact = (flags & GRKAN_FLAG_EXACT) != 0;
+  L.vec = vec;
+  L.check = check;
+  L.stream = s;
+  cudaError_t e = launch("fwd", dtype, L);
   if (e != cudaSuccess) return cuda_fail(e, "k_fwd launch");
   return GRKAN_OK;
 }
@@ -303,43 +313,29 @@ int grkan_bwd(const void* x, const void* dy, const void* a, const void* b, void*
   if (!x || !dy || !dx || !a || (n > 0 && !b)) return fail(GRKAN_ERR_INVALID, "null tensor pointer");
   const size_t es = elem_size(dtype);
   const bool vec = vec_ok(d, n_groups, es, {x, dy, dx});
-  const Plan p = make_plan(rows, d, n_groups, es, vec, sm_count());
-  if (p.ctas > 0x7fffffffLL) return fail(GRKAN_ERR_GRID, "grid geometry invalid: %lld CTAs", (long long)p.ctas);
+  const Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count());
+  if (!plan_fits(p)) return fail(GRKAN_ERR_GRID, "grid geometry invalid: %lld CTAs", (long long)p.ctas);
   const size_t need = ws_bytes_for(p, m1, n, dtype);
   if (ws_bytes < need)
     return fail(GRKAN_ERR_INVALID, "workspace too small: %zu < %zu bytes", ws_bytes, need);
-  void* part = static_cast<char*>(ws) + 256;
-  const bool fixed = (m1 == kFixM1 && n == kFixN);
-  const bool check = (flags & GRKAN_FLAG_CHECK_FINITE) != 0;
-  e = dispatch(dtype, flags & GRKAN_FLAG_EXACT, fixed, vec, [&](auto tt, auto et, auto ft, auto wt) {
-    using T = typename decltype(tt)::type;
-    constexpr bool E = decltype(et)::value;
-    constexpr bool FX = decltype(ft)::value;
-    constexpr int W = decltype(wt)::value;
-    using A = typename grkan::VecIO<T, W>::A;
-    constexpr int MM1 = FX ? kFixM1 : kGenM1;
-    constexpr int MN = FX ? kFixN : kGenN;
-    grkan::k_bwd_main<T, E, MM1, MN, FX, W><<<static_cast<unsigned>(p.ctas), p.threads, 0, s>>>(
-        static_cast<const T*>(x), static_cast<const T*>(dy), static_cast<T*>(dx),
-        static_cast<const A*>(a), static_cast<const A*>(b), static_cast<A*>(part), p.geo, m1, n,
-        check ? 1 : 0, st);
-    cudaError_t le = cudaGetLastError();
-    if (le != cudaSuccess) return le;
-    // K3 with programmatic dependent launch: its launch overlaps K2's tail,
-    // its griddepcontrol.wait orders it after K2's memory.
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(n_groups * (m1 + n)));
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, grkan::k_bwd_reduce<A>, static_cast<const A*>(part),
-                              p.geo.n_tiles, m1, n, static_cast<A*>(da), static_cast<A*>(db), st);
-  });
+  LaunchArgs L{};
+  L.plan = &p;
+  L.x = x;
+  L.dy = dy;
+  L.out = dx;
+  L.a = a;
+  L.b = b;
+  L.part = static_cast<char*>(ws) + 256;
+  L.da = da;
+  L.db = db;
+  L.st = st;
+  L.m1 = m1;
+  L.n = n;
+  L.exact = (flags & GRKAN_FLAG_EXACT) != 0;
+  L.vec = vec;
+  L.check = (flags & GRKAN_FLAG_CHECK_FINITE) != 0;
+  L.stream = s;
+  e = launch("bwd", dtype, L);
   if (e != cudaSuccess) return cuda_fail(e, "k_bwd launch");
   return GRKAN_OK;
 }
@@ -361,27 +357,25 @@ int grkan_bwd_atomic(const void* x, const void* dy, const void* a, const void* b
   if (!x || !dy || !dx || !a || (n > 0 && !b)) return fail(GRKAN_ERR_INVALID, "null tensor pointer");
   const size_t es = elem_size(dtype);
   const bool vec = vec_ok(d, n_groups, es, {x, dy, dx});
-  const Plan p = make_plan(rows, d, n_groups, es, vec, sm_count());
-  const bool fixed = (m1 == kFixM1 && n == kFixN);
-  DevStatus* st = reinterpret_cast<DevStatus*>(status);
-  e = dispatch(dtype, flags & GRKAN_FLAG_EXACT, fixed, vec, [&](auto tt, auto et, auto ft, auto wt) {
-    using T = typename decltype(tt)::type;
-    constexpr bool E = decltype(et)::value;
-    constexpr bool FX = decltype(ft)::value;
-    constexpr int W = decltype(wt)::value;
-    using A = typename grkan::VecIO<T, W>::A;
-    constexpr int MM1 = FX ? kFixM1 : kGenM1;
-    constexpr int MN = FX ? kFixN : kGenN;
-    grkan::k_bwd_atomic<T, E, MM1, MN, FX, W><<<static_cast<unsigned>(p.ctas), p.threads, 0, s>>>(
-        static_cast<const T*>(x), static_cast<const T*>(dy), static_cast<T*>(dx),
-        static_cast<const A*>(a), static_cast<const A*>(b), static_cast<A*>(da), static_cast<A*>(db),
-        p.geo, m1, n);
-    cudaError_t le = cudaGetLastError();
-    if (le != cudaSuccess || !st) return le;
-    grkan::k_check_finite<A><<<1, 256, 0, s>>>(static_cast<const A*>(da), (int64_t)n_groups * m1, st);
-    if (n > 0) grkan::k_check_finite<A><<<1, 256, 0, s>>>(static_cast<const A*>(db), (int64_t)n_groups * n, st);
-    return cudaGetLastError();
-  });
+  const Plan p = make_plan(rows, d, n_groups, /*m1=*/0, n, es, vec, 2, sm_count());  // never staged
+  if (!plan_fits(p)) return fail(GRKAN_ERR_GRID, "grid geometry invalid: %lld CTAs", (long long)p.ctas);
+  LaunchArgs L{};
+  L.plan = &p;
+  L.x = x;
+  L.dy = dy;
+  L.out = dx;
+  L.a = a;
+  L.b = b;
+  L.da = da;
+  L.db = db;
+  L.st = reinterpret_cast<DevStatus*>(status);
+  L.m1 = m1;
+  L.n = n;
+  L.exact = (flags & GRKAN_FLAG_EXACT) != 0;
+  L.vec = vec;
+  L.check = false;
+  L.stream = s;
+  e = launch("atomic", dtype, L);
   if (e != cudaSuccess) return cuda_fail(e, "k_bwd_atomic launch");
   return GRKAN_OK;
 }

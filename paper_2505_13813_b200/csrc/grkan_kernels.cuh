@@ -9,15 +9,16 @@
 //   K4 k_bwd_atomic   the paper's Alg. 1 (per-element atomicAdd) -- comparator only
 //                     (backward_naive as its model, backward.py:187-246)
 //
-// Work decomposition (shared by K1/K2/K4).  The tensor is [rows, d] row-major;
-// group g owns columns [g*dg, (g+1)*dg).  One CTA owns one (row tile, group):
+// Work decomposition (K1/K2/K4).  The tensor is [rows, d] row-major; group g
+// owns columns [g*dg, (g+1)*dg).  One CTA owns one (row tile, group) block of
 // R rows x dg columns, so its coefficients are CTA-uniform registers and its
 // coefficient gradients reduce to exactly one partial.  Linear CTA id
 // = tile * n_groups + g, so CTAs resident together stream one contiguous row
-// band.  Inside a CTA, thread (tr, tc) owns vector column tc (+CT, ...) and rows
-// tr, tr+RPB, ...; a warp covers consecutive 16-byte vectors of a row segment,
-// i.e. fully coalesced 128-bit loads and stores.  U row-vectors are loaded
-// before any math so each thread keeps 2*U 16-byte loads in flight.
+// band.  Inside the tile the R x V grid of 16-byte vectors is walked in flat
+// order by kBlock threads (thread t takes vectors t, t + kBlock, ...), so a
+// warp always reads 32 consecutive vectors of a row segment: coalesced
+// 128-bit loads/stores whatever the group width.  U vectors per tensor are
+// loaded before any math, giving 2*U 16-byte loads in flight per thread.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -25,30 +26,16 @@
 #include <float.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "grkan_math.cuh"
+#include "grkan_types.h"
 
 namespace grkan {
 
-struct Geom {
-  int64_t rows;     // B*L
-  int64_t n_tiles;  // ceil(rows / R)
-  int32_t d;        // feature dim (row stride, elements)
-  int32_t ng;       // groups
-  int32_t dg;       // group width
-  int32_t V;        // vectors per row segment = dg / W
-  int32_t CT;       // threads along vector columns
-  int32_t RPB;      // threads along rows; blockDim = CT * RPB
-  int32_t R;        // rows per tile (multiple of RPB * U)
-};
-
-struct DevStatus {
-  int32_t nonfinite_input;
-  int32_t accum_overflow;
-};
-
 // ---------------------------------------------------------------------------
-// Vector I/O: W elements of T <-> accumulation type A.  Streaming (.cs) hints:
-// every byte is touched once per kernel, keep it from displacing L2.
+// Vector I/O: W elements of T <-> math type A.  Streaming (.cs) hints: every
+// byte is touched once per kernel, so keep it from displacing L2.
 // ---------------------------------------------------------------------------
 template <typename T, int W>
 struct VecIO;
@@ -92,7 +79,7 @@ struct VecIO<double, 1> {
 };
 
 // bf16: 8 elements per 16-byte vector; widening is a shift / mask per element,
-// narrowing is one round-to-nearest-even pack per pair.
+// narrowing one round-to-nearest-even pack per pair (F2FP.BF16.F32.PACK_AB).
 template <>
 struct VecIO<__nv_bfloat16, 8> {
   using A = float;
@@ -139,90 +126,124 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-constexpr int kMaxThreads = 512;
-
-// Unrolled row-vectors per thread per step.
-template <int W>
-struct Unroll {
-  static constexpr int U = W >= 8 ? 2 : 4;
+// ---------------------------------------------------------------------------
+// Engine selection: packed fp32 pairs for the paper's degrees, scalar otherwise.
+// ---------------------------------------------------------------------------
+template <typename T, bool EXACT, int MM1, int MN, bool FIXED, int W>
+struct Engine {
+  using A = typename VecIO<T, W>::A;
+  static constexpr bool kPacked =
+      std::is_same<A, float>::value && FIXED && MM1 == 6 && MN == 4 && (W % 2 == 0);
+  using Scalar = Rational<A, EXACT, MM1, MN, FIXED>;
+  static constexpr int KC = MM1 + MN;
+  // vectors per tensor per thread per step (backward; = unroll_for_width(W))
+  static constexpr int U = W >= 2 ? 2 : 4;
+  // forward: one tensor in and little math per byte, so more loads in flight
+  static constexpr int UF = 4;
 };
 
-// ---------------------------------------------------------------------------
-// Tile walker: calls body(elem_offset, valid) for the U row-vectors of each
-// step; the common full-tile case is branch-free.
-// ---------------------------------------------------------------------------
-struct TileCtx {
-  int64_t row0;
-  int nr;
-  int tc, tr;
+// Flat walk of one tile: the thread's current (row, vector) position.
+struct Cursor {
+  int r, c;
+  __device__ __forceinline__ void init(int k, int V) {
+    r = k / V;
+    c = k - r * V;
+  }
+  __device__ __forceinline__ void advance(const Geom& g) {
+    c += g.dc;
+    r += g.dr;
+    if (c >= g.V) {
+      c -= g.V;
+      ++r;
+    }
+  }
 };
 
-__device__ __forceinline__ TileCtx tile_ctx(const Geom& geo, int64_t tile) {
-  TileCtx t;
-  t.row0 = tile * geo.R;
-  const int64_t left = geo.rows - t.row0;
-  t.nr = left < geo.R ? static_cast<int>(left) : geo.R;
-  t.tc = threadIdx.x % geo.CT;
-  t.tr = threadIdx.x / geo.CT;
-  return t;
-}
+// NaN / Inf detector for checked mode: x * 0 is NaN exactly when x is not finite.
+template <typename A>
+struct Checker {
+  A acc = A(0);
+  __device__ __forceinline__ void add(A v) { acc = fma(v, A(0), acc); }
+  __device__ __forceinline__ bool bad() const { return nonfinite(acc); }
+};
 
 // ---------------------------------------------------------------------------
 // K1: forward
 // ---------------------------------------------------------------------------
-template <typename T, bool EXACT, int MM1, int MN, bool FIXED, int W>
-__global__ void __launch_bounds__(kMaxThreads, 1)
-    k_fwd(const T* __restrict__ x, T* __restrict__ y, const typename VecIO<T, W>::A* __restrict__ ca,
-          const typename VecIO<T, W>::A* __restrict__ cb, Geom geo, int m1, int n, int check,
+template <typename T, bool EXACT, int MM1, int MN, bool FIXED, int W, bool CHECK>
+__global__ void __launch_bounds__(kBlock, kMinBlocks)
+    k_fwd(const T* __restrict__ x, T* __restrict__ y,
+          const typename VecIO<T, W>::A* __restrict__ ca,
+          const typename VecIO<T, W>::A* __restrict__ cb, Geom geo, int m1, int n,
           DevStatus* __restrict__ st) {
-  using A = typename VecIO<T, W>::A;
+  using E = Engine<T, EXACT, MM1, MN, FIXED, W>;
+  using A = typename E::A;
   using IO = VecIO<T, W>;
-  constexpr int U = Unroll<W>::U;
+  constexpr int U = E::UF;
   const int64_t bid = blockIdx.x;
   const int g = static_cast<int>(bid % geo.ng);
   const int64_t tile = bid / geo.ng;
-  Rational<A, EXACT, MM1, MN, FIXED> rat;
-  rat.load(ca, cb, g, m1, n);
-  const TileCtx tc = tile_ctx(geo, tile);
-  bool bad = false;
-  for (int c = tc.tc; c < geo.V; c += geo.CT) {
-    const int64_t base = (tc.row0 * geo.d) + (int64_t)g * geo.dg + (int64_t)c * W;
-    for (int r = tc.tr; r < tc.nr; r += geo.RPB * U) {
-      A v[U][W];
-      const bool full = r + (U - 1) * geo.RPB < tc.nr;
+  typename E::Scalar rs;
+  RationalX2<EXACT> rp;
+  if constexpr (E::kPacked) rp.load(ca, cb, g, geo.one); else rs.load(ca, cb, g, m1, n);
+  const int64_t row0 = tile * geo.R;
+  const int nr = static_cast<int>(geo.rows - row0 < geo.R ? geo.rows - row0 : geo.R);
+  const int nvec = nr * geo.V;
+  const int64_t tile_off = row0 * geo.d + (int64_t)g * geo.dg;
+  const T* xt = x + tile_off;
+  T* yt = y + tile_off;
+  Checker<A> chk;
+  Cursor cur;
+  cur.init(threadIdx.x, geo.V);
+  for (int k = threadIdx.x; k < nvec; k += U * kBlock) {
+    int64_t off[U];
+    A v[U][W];
 #pragma unroll
-      for (int j = 0; j < U; ++j) {
-        if (full || r + j * geo.RPB < tc.nr) IO::load(x + base + (int64_t)(r + j * geo.RPB) * geo.d, v[j]);
-      }
+    for (int j = 0; j < U; ++j) {
+      off[j] = (int64_t)cur.r * geo.d + cur.c * W;
+      cur.advance(geo);
+    }
 #pragma unroll
-      for (int j = 0; j < U; ++j) {
-        if (full || r + j * geo.RPB < tc.nr) {
-          A o[W];
+    for (int j = 0; j < U; ++j)
+      if (j == 0 || k + j * kBlock < nvec) IO::load(xt + off[j], v[j]);
 #pragma unroll
-          for (int e = 0; e < W; ++e) {
-            if (check) bad |= nonfinite(v[j][e]);
-            o[e] = rat.value(v[j][e]);
+    for (int j = 0; j < U; ++j) {
+      if (j == 0 || k + j * kBlock < nvec) {
+        A o[W];
+        if constexpr (E::kPacked) {
+#pragma unroll
+          for (int e = 0; e < W; e += 2) {
+            const float2 r2 = rp.value(make_float2(v[j][e], v[j][e + 1]));
+            o[e] = r2.x;
+            o[e + 1] = r2.y;
           }
-          IO::store(y + base + (int64_t)(r + j * geo.RPB) * geo.d, o);
+        } else {
+#pragma unroll
+          for (int e = 0; e < W; ++e) o[e] = rs.value(v[j][e]);
         }
+        if constexpr (CHECK) {
+#pragma unroll
+          for (int e = 0; e < W; ++e) chk.add(v[j][e]);
+        }
+        IO::store(yt + off[j], o);
       }
     }
   }
-  if (check && bad) st->nonfinite_input = 1;  // plain store of a constant: no atomic needed
+  if (CHECK && chk.bad()) st->nonfinite_input = 1;  // plain store of a constant: no atomic
 }
 
 // ---------------------------------------------------------------------------
-// Deterministic CTA reduction of KC per-thread accumulators -> one partial.
-// Warp butterfly, then warp 0 folds the per-warp sums in warp order.
-// Partials are stored SoA: part[(g*KC + k) * n_tiles + tile].
+// Deterministic CTA reduction of the accumulators -> one partial per slot.
+// Warp butterfly (fixed), then warp 0 folds the per-warp sums in warp order.
+// Partials are SoA: part[(g * kc + k) * n_tiles + tile], k in [0, m1 + n):
+// slot k < m1 is a_k's term, slot m1 + j is b_{j+1}'s (accumulator MM1 + j).
 // ---------------------------------------------------------------------------
-template <typename A, int KC>
-__device__ __forceinline__ void cta_reduce_store(A (&acc)[KC], int kc_rt, A* __restrict__ part,
+template <typename A, int MM1, int KC>
+__device__ __forceinline__ void cta_reduce_store(A (&acc)[KC], int m1, int n, A* __restrict__ part,
                                                  int g, int64_t tile, int64_t n_tiles) {
-  __shared__ A red[kMaxThreads / 32][KC];
+  __shared__ A red[kBlock / 32][KC];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int nwarps = (blockDim.x + 31) >> 5;
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
     A v = acc[k];
@@ -232,12 +253,15 @@ __device__ __forceinline__ void cta_reduce_store(A (&acc)[KC], int kc_rt, A* __r
   }
   __syncthreads();
   if (warp == 0) {
+    const int kc = m1 + n;
 #pragma unroll
     for (int k = 0; k < KC; ++k) {
-      A v = lane < nwarps ? red[lane][k] : A(0);
+      A v = lane < kBlock / 32 ? red[lane][k] : A(0);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0 && k < kc_rt) part[((int64_t)g * kc_rt + k) * n_tiles + tile] = v;
+      const bool live = k < MM1 ? (k < m1) : (k - MM1 < n);
+      const int slot = k < MM1 ? k : m1 + (k - MM1);
+      if (lane == 0 && live) part[((int64_t)g * kc + slot) * n_tiles + tile] = v;
     }
   }
 }
@@ -245,60 +269,97 @@ __device__ __forceinline__ void cta_reduce_store(A (&acc)[KC], int kc_rt, A* __r
 // ---------------------------------------------------------------------------
 // K2: backward main pass
 // ---------------------------------------------------------------------------
-template <typename T, bool EXACT, int MM1, int MN, bool FIXED, int W>
-__global__ void __launch_bounds__(kMaxThreads, 1)
+template <typename T, bool EXACT, int MM1, int MN, bool FIXED, int W, bool CHECK>
+__global__ void __launch_bounds__(kBlock, kMinBlocks)
     k_bwd_main(const T* __restrict__ x, const T* __restrict__ dy, T* __restrict__ dx,
                const typename VecIO<T, W>::A* __restrict__ ca,
                const typename VecIO<T, W>::A* __restrict__ cb,
-               typename VecIO<T, W>::A* __restrict__ part, Geom geo, int m1, int n, int check,
+               typename VecIO<T, W>::A* __restrict__ part, Geom geo, int m1, int n,
                DevStatus* __restrict__ st) {
-  using A = typename VecIO<T, W>::A;
+  using E = Engine<T, EXACT, MM1, MN, FIXED, W>;
+  using A = typename E::A;
   using IO = VecIO<T, W>;
-  using Rat = Rational<A, EXACT, MM1, MN, FIXED>;
-  constexpr int U = Unroll<W>::U;
-  constexpr int KC = Rat::KC;
+  constexpr int U = E::U;
+  constexpr int KC = E::KC;
   // Let K3 (launched with programmatic stream serialization) get scheduled;
-  // it waits in griddepcontrol.wait until this grid has fully completed.
+  // it waits in griddepcontrol.wait until this whole grid has completed.
   pdl_launch_dependents();
   const int64_t bid = blockIdx.x;
   const int g = static_cast<int>(bid % geo.ng);
   const int64_t tile = bid / geo.ng;
-  Rat rat;
-  rat.load(ca, cb, g, m1, n);
+  typename E::Scalar rs;
+  RationalX2<EXACT> rp;
   A acc[KC];
+  float2 acc2[E::kPacked ? KC : 1];
+  if constexpr (E::kPacked) {
+    rp.load(ca, cb, g, geo.one);
 #pragma unroll
-  for (int k = 0; k < KC; ++k) acc[k] = A(0);
-  const TileCtx tc = tile_ctx(geo, tile);
-  bool bad = false;
-  for (int c = tc.tc; c < geo.V; c += geo.CT) {
-    const int64_t base = (tc.row0 * geo.d) + (int64_t)g * geo.dg + (int64_t)c * W;
-    for (int r = tc.tr; r < tc.nr; r += geo.RPB * U) {
-      A vx[U][W], vu[U][W];
-      const bool full = r + (U - 1) * geo.RPB < tc.nr;
+    for (int k = 0; k < KC; ++k) acc2[k] = make_float2(0.f, 0.f);
+  } else {
+    rs.load(ca, cb, g, m1, n);
 #pragma unroll
-      for (int j = 0; j < U; ++j) {
-        if (full || r + j * geo.RPB < tc.nr) {
-          const int64_t off = base + (int64_t)(r + j * geo.RPB) * geo.d;
-          IO::load(x + off, vx[j]);
-          IO::load(dy + off, vu[j]);
-        }
+    for (int k = 0; k < KC; ++k) acc[k] = A(0);
+  }
+  const int64_t row0 = tile * geo.R;
+  const int nr = static_cast<int>(geo.rows - row0 < geo.R ? geo.rows - row0 : geo.R);
+  const int nvec = nr * geo.V;
+  const int64_t tile_off = row0 * geo.d + (int64_t)g * geo.dg;
+  const T* xt = x + tile_off;
+  const T* ut = dy + tile_off;
+  T* dt = dx + tile_off;
+  Checker<A> chk;
+  Cursor cur;
+  cur.init(threadIdx.x, geo.V);
+  for (int k = threadIdx.x; k < nvec; k += U * kBlock) {
+    int64_t off[U];
+    A vx[U][W], vu[U][W];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      off[j] = (int64_t)cur.r * geo.d + cur.c * W;
+      cur.advance(geo);
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      if (j == 0 || k + j * kBlock < nvec) {
+        IO::load(xt + off[j], vx[j]);
+        IO::load(ut + off[j], vu[j]);
       }
+    }
 #pragma unroll
-      for (int j = 0; j < U; ++j) {
-        if (full || r + j * geo.RPB < tc.nr) {
-          A o[W];
+    for (int j = 0; j < U; ++j) {
+      if (j == 0 || k + j * kBlock < nvec) {
+        A o[W];
+        if constexpr (E::kPacked) {
+#pragma unroll
+          for (int e = 0; e < W; e += 2) {
+            const float2 r2 = rp.grad(make_float2(vx[j][e], vx[j][e + 1]),
+                                      make_float2(vu[j][e], vu[j][e + 1]), acc2);
+            o[e] = r2.x;
+            o[e + 1] = r2.y;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < W; ++e) o[e] = rs.grad(vx[j][e], vu[j][e], acc);
+        }
+        if constexpr (CHECK) {
 #pragma unroll
           for (int e = 0; e < W; ++e) {
-            if (check) bad |= nonfinite(vx[j][e]) | nonfinite(vu[j][e]);
-            o[e] = rat.grad(vx[j][e], vu[j][e], acc);
+            chk.add(vx[j][e]);
+            chk.add(vu[j][e]);
           }
-          IO::store(dx + base + (int64_t)(r + j * geo.RPB) * geo.d, o);
         }
+        IO::store(dt + off[j], o);
       }
     }
   }
-  if (check && bad) st->nonfinite_input = 1;
-  cta_reduce_store<A, KC>(acc, rat.m1 + rat.n, part, g, tile, geo.n_tiles);
+  if (CHECK && chk.bad()) st->nonfinite_input = 1;
+  if constexpr (E::kPacked) {
+#pragma unroll
+    for (int k = 0; k < KC; ++k) acc[k] = acc2[k].x + acc2[k].y;
+    cta_reduce_store<A, MM1, KC>(acc, MM1, MN, part, g, tile, geo.n_tiles);
+  } else {
+    cta_reduce_store<A, MM1, KC>(acc, FIXED ? MM1 : m1, FIXED ? MN : n, part, g, tile, geo.n_tiles);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -340,7 +401,7 @@ __global__ void __launch_bounds__(256)
 // K4: Alg. 1 comparator -- every element atomically adds its m1+n terms.
 // ---------------------------------------------------------------------------
 template <typename T, bool EXACT, int MM1, int MN, bool FIXED, int W>
-__global__ void __launch_bounds__(kMaxThreads, 1)
+__global__ void __launch_bounds__(kBlock)
     k_bwd_atomic(const T* __restrict__ x, const T* __restrict__ dy, T* __restrict__ dx,
                  const typename VecIO<T, W>::A* __restrict__ ca,
                  const typename VecIO<T, W>::A* __restrict__ cb, typename VecIO<T, W>::A* da,
@@ -354,29 +415,32 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   const int64_t tile = bid / geo.ng;
   Rat rat;
   rat.load(ca, cb, g, m1, n);
-  const TileCtx tc = tile_ctx(geo, tile);
-  for (int c = tc.tc; c < geo.V; c += geo.CT) {
-    const int64_t base = (tc.row0 * geo.d) + (int64_t)g * geo.dg + (int64_t)c * W;
-    for (int r = tc.tr; r < tc.nr; r += geo.RPB) {
-      const int64_t off = base + (int64_t)r * geo.d;
-      A vx[W], vu[W], o[W];
-      IO::load(x + off, vx);
-      IO::load(dy + off, vu);
+  const int64_t row0 = tile * geo.R;
+  const int nr = static_cast<int>(geo.rows - row0 < geo.R ? geo.rows - row0 : geo.R);
+  const int nvec = nr * geo.V;
+  const int64_t tile_off = row0 * geo.d + (int64_t)g * geo.dg;
+  Cursor cur;
+  cur.init(threadIdx.x, geo.V);
+  for (int k = threadIdx.x; k < nvec; k += kBlock) {
+    const int64_t off = tile_off + (int64_t)cur.r * geo.d + cur.c * W;
+    cur.advance(geo);
+    A vx[W], vu[W], o[W];
+    IO::load(x + off, vx);
+    IO::load(dy + off, vu);
 #pragma unroll
-      for (int e = 0; e < W; ++e) {
-        A t[KC];
+    for (int e = 0; e < W; ++e) {
+      A t[KC];
 #pragma unroll
-        for (int k = 0; k < KC; ++k) t[k] = A(0);
-        o[e] = rat.grad(vx[e], vu[e], t);
+      for (int i = 0; i < KC; ++i) t[i] = A(0);
+      o[e] = rat.grad(vx[e], vu[e], t);
 #pragma unroll
-        for (int i = 0; i < MM1; ++i)
-          if (FIXED || i < rat.m1) atomicAdd(da + (int64_t)g * rat.m1 + i, t[i]);
+      for (int i = 0; i < MM1; ++i)
+        if (FIXED || i < rat.m1) atomicAdd(da + (int64_t)g * rat.m1 + i, t[i]);
 #pragma unroll
-        for (int j = 0; j < MN; ++j)
-          if (FIXED || j < rat.n) atomicAdd(db + (int64_t)g * rat.n + j, t[MM1 + j]);
-      }
-      IO::store(dx + off, o);
+      for (int j = 0; j < MN; ++j)
+        if (FIXED || j < rat.n) atomicAdd(db + (int64_t)g * rat.n + j, t[MM1 + j]);
     }
+    IO::store(dx + off, o);
   }
 }
 

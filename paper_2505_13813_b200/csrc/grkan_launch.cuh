@@ -1,0 +1,152 @@
+// grkan_launch.cuh -- compile-time dispatch from LaunchArgs onto the kernel
+// instantiations: {fast, exact} x {(5,4) fixed, generic <= 12/12} x
+// {128-bit vector, scalar} x {checked, unchecked}.  Included once per dtype TU.
+#pragma once
+
+#include "grkan_kernels.cuh"
+#include "grkan_staged.cuh"
+#include "grkan_types.h"
+
+namespace grkan {
+
+constexpr int kFixM1 = 6, kFixN = 4;   // the paper's degrees (5, 4)
+constexpr int kGenM1 = 12, kGenN = 12; // GRKAN_MAX_M1 / GRKAN_MAX_N
+
+template <typename T>
+constexpr int vec_width() { return static_cast<int>(16 / sizeof(T)); }
+
+// Calls f(bool_constant<EXACT>, bool_constant<FIXED>, int_constant<W>, bool_constant<CHECK>).
+template <typename T, typename F>
+cudaError_t dispatch(const LaunchArgs& L, bool fixed, F&& f) {
+  auto w = [&](auto e, auto fx, auto ck) -> cudaError_t {
+    if (L.vec) return f(e, fx, std::integral_constant<int, vec_width<T>()>{}, ck);
+    return f(e, fx, std::integral_constant<int, 1>{}, ck);
+  };
+  auto c = [&](auto e, auto fx) -> cudaError_t {
+    return L.check ? w(e, fx, std::true_type{}) : w(e, fx, std::false_type{});
+  };
+  auto x = [&](auto e) -> cudaError_t {
+    return fixed ? c(e, std::true_type{}) : c(e, std::false_type{});
+  };
+  return L.exact ? x(std::true_type{}) : x(std::false_type{});
+}
+
+inline bool is_fixed(const LaunchArgs& L) { return L.m1 == kFixM1 && L.n == kFixN; }
+
+// Opt a kernel into its dynamic shared memory size (static + dynamic > 48 KB
+// needs the attribute).  One cache per kernel instantiation.
+template <auto Kernel>
+cudaError_t allow_smem(size_t bytes) {
+  static size_t granted = 0;  // benign race: concurrent writers store equivalent values
+  if (bytes <= granted) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(bytes));
+  if (e == cudaSuccess) granted = bytes;
+  return e;
+}
+
+template <typename T, typename F>
+cudaError_t dispatch_staged(const LaunchArgs& L, F&& f) {
+  auto c = [&](auto e) -> cudaError_t {
+    return L.check ? f(e, std::true_type{}) : f(e, std::false_type{});
+  };
+  return L.exact ? c(std::true_type{}) : c(std::false_type{});
+}
+
+template <typename T>
+cudaError_t launch_fwd_t(const LaunchArgs& L) {
+  using A = typename VecIO<T, 1>::A;
+  const Plan& p = *L.plan;
+  if (p.staged) {
+    return dispatch_staged<T>(L, [&](auto e, auto ck) -> cudaError_t {
+      constexpr auto kern = k_fwd_staged<T, decltype(e)::value, decltype(ck)::value>;
+      cudaError_t ae = allow_smem<kern>(p.smem);
+      if (ae != cudaSuccess) return ae;
+      kern<<<static_cast<unsigned>(p.ctas), kStagedThreads, p.smem, L.stream>>>(
+          static_cast<const T*>(L.x), static_cast<T*>(L.out), static_cast<const A*>(L.a),
+          static_cast<const A*>(L.b), p.geo, p.stages, L.st);
+      return cudaGetLastError();
+    });
+  }
+  return dispatch<T>(L, is_fixed(L), [&](auto e, auto fx, auto wc, auto ck) -> cudaError_t {
+    constexpr bool FX = decltype(fx)::value;
+    k_fwd<T, decltype(e)::value, FX ? kFixM1 : kGenM1, FX ? kFixN : kGenN, FX, decltype(wc)::value,
+          decltype(ck)::value><<<static_cast<unsigned>(p.ctas), kBlock, 0, L.stream>>>(
+        static_cast<const T*>(L.x), static_cast<T*>(L.out), static_cast<const A*>(L.a),
+        static_cast<const A*>(L.b), p.geo, L.m1, L.n, L.st);
+    return cudaGetLastError();
+  });
+}
+
+template <typename T>
+cudaError_t launch_bwd_t(const LaunchArgs& L) {
+  using A = typename VecIO<T, 1>::A;
+  const Plan& p = *L.plan;
+  cudaError_t e0;
+  if (p.staged) {
+    e0 = dispatch_staged<T>(L, [&](auto e, auto ck) -> cudaError_t {
+      constexpr auto kern = k_bwd_staged<T, decltype(e)::value, decltype(ck)::value>;
+      cudaError_t ae = allow_smem<kern>(p.smem);
+      if (ae != cudaSuccess) return ae;
+      kern<<<static_cast<unsigned>(p.ctas), kStagedThreads, p.smem, L.stream>>>(
+          static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out),
+          static_cast<const A*>(L.a), static_cast<const A*>(L.b), static_cast<A*>(L.part), p.geo,
+          p.stages, L.st);
+      return cudaGetLastError();
+    });
+  } else e0 = dispatch<T>(L, is_fixed(L), [&](auto e, auto fx, auto wc, auto ck) -> cudaError_t {
+    constexpr bool FX = decltype(fx)::value;
+    k_bwd_main<T, decltype(e)::value, FX ? kFixM1 : kGenM1, FX ? kFixN : kGenN, FX,
+               decltype(wc)::value, decltype(ck)::value>
+        <<<static_cast<unsigned>(p.ctas), kBlock, 0, L.stream>>>(
+            static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out),
+            static_cast<const A*>(L.a), static_cast<const A*>(L.b), static_cast<A*>(L.part), p.geo,
+            L.m1, L.n, L.st);
+    return cudaGetLastError();
+  });
+  if (e0 != cudaSuccess) return e0;
+  // K3 with programmatic dependent launch: its launch overlaps K2's tail and
+  // its griddepcontrol.wait orders it after all of K2's memory operations.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(p.geo.ng * (L.m1 + L.n)));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = L.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_bwd_reduce<A>, static_cast<const A*>(L.part), p.geo.n_tiles,
+                            L.m1, L.n, static_cast<A*>(L.da), static_cast<A*>(L.db), L.st);
+}
+
+template <typename T>
+cudaError_t launch_atomic_t(const LaunchArgs& L) {
+  using A = typename VecIO<T, 1>::A;
+  const Plan& p = *L.plan;
+  LaunchArgs L2 = L;
+  L2.check = false;
+  cudaError_t e0 = dispatch<T>(L2, is_fixed(L), [&](auto e, auto fx, auto wc, auto) -> cudaError_t {
+    constexpr bool FX = decltype(fx)::value;
+    k_bwd_atomic<T, decltype(e)::value, FX ? kFixM1 : kGenM1, FX ? kFixN : kGenN, FX, decltype(wc)::value>
+        <<<static_cast<unsigned>(p.ctas), kBlock, 0, L.stream>>>(
+            static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out),
+            static_cast<const A*>(L.a), static_cast<const A*>(L.b), static_cast<A*>(L.da),
+            static_cast<A*>(L.db), p.geo, L.m1, L.n);
+    return cudaGetLastError();
+  });
+  if (e0 != cudaSuccess || !L.st) return e0;
+  k_check_finite<A><<<1, 256, 0, L.stream>>>(static_cast<const A*>(L.da), (int64_t)p.geo.ng * L.m1, L.st);
+  if (L.n > 0) k_check_finite<A><<<1, 256, 0, L.stream>>>(static_cast<const A*>(L.db), (int64_t)p.geo.ng * L.n, L.st);
+  return cudaGetLastError();
+}
+
+}  // namespace grkan
+
+#define GRKAN_DEFINE_LAUNCHERS(T, SUF)                                                       \
+  namespace grkan {                                                                          \
+  cudaError_t launch_fwd_##SUF(const LaunchArgs& L) { return launch_fwd_t<T>(L); }           \
+  cudaError_t launch_bwd_##SUF(const LaunchArgs& L) { return launch_bwd_t<T>(L); }           \
+  cudaError_t launch_atomic_##SUF(const LaunchArgs& L) { return launch_atomic_t<T>(L); }     \
+  }

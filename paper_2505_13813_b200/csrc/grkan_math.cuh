@@ -1,14 +1,22 @@
 // grkan_math.cuh -- per-element GR-KAN math for sm_100a, two precision policies.
 //
 // EXACT: the reference's operation order with every *, +, /, 1/q rounded on its
-//        own (__fmul_rn / __fadd_rn / __fdiv_rn / __frcp_rn; the _rn intrinsics
-//        are never contracted into FMA).  y, dx and each of the m1+n per-element
-//        coefficient-gradient terms are then bitwise equal to the reference
-//        (pkg/src/grkan/rational.py:195-278).
-// FAST:  FMA Horner, one approximate reciprocal (Q >= 1 so rcp.approx is
-//        safe), powers of x shared by the da and db terms.  Restructured but
-//        algebraically identical; gated at max-scaled error <= 1e-5.
+//        own (__fmul_rn / __fadd_rn / __fdiv_rn / __frcp_rn and the packed
+//        __fmul2_rn / __fadd2_rn; none is ever contracted into an FMA).  y, dx
+//        and each of the m1+n per-element coefficient-gradient terms are then
+//        bitwise equal to the reference (pkg/src/grkan/rational.py:195-278;
+//        SURVEY.md Appendix A).
+// FAST:  FMA Horner, one approximate reciprocal (Q >= 1, so rcp.approx has no
+//        denormal corner), powers of x shared by the da and db terms.
+//        Restructured but algebraically identical; gated at max-scaled 1e-5.
 //
+// Two engines:
+//   Rational<...>   scalar; any dtype, any degree up to 12/12 (generic path).
+//   RationalX2      the hot path: fp32 math at the paper's degrees (5, 4) on
+//                   element PAIRS with sm_100a packed FFMA2 / FMUL2 / FADD2,
+//                   both policies (EXACT via xmad2's separately rounded steps).
+//                   Coefficients stay scalar registers (FFMA2 takes a .F32
+//                   broadcast operand), accumulators are float2 pairs.
 // Coefficients are CTA-uniform (one group per CTA) and live in registers.
 #pragma once
 
@@ -42,8 +50,6 @@ struct Op<float, false> {
   static __device__ __forceinline__ float add(float a, float b) { return a + b; }
   static __device__ __forceinline__ float sub(float a, float b) { return a - b; }
   static __device__ __forceinline__ float mad(float a, float b, float c) { return fmaf(a, b, c); }
-  // q >= 1 always (safe Pade denominator), so the MUFU approximation has no
-  // denormal corner; q = inf gives 0 like the IEEE path.
   static __device__ __forceinline__ float rcp(float q) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(q));
@@ -74,10 +80,14 @@ struct Op<double, false> {
   static __device__ __forceinline__ double div(double p, double q) { return p / q; }
 };
 
-// np.sign: +1 / -1 / +0 for +-0 / NaN propagates (rational.py:251)
-template <typename A>
-__device__ __forceinline__ A sign_of(A s) {
-  return s > A(0) ? A(1) : (s < A(0) ? A(-1) : (s == A(0) ? A(0) : s));
+// np.sign for every non-NaN input: +1 / -1, and +0 for both zeros
+// (rational.py:251).  A NaN s makes q, 1/q and every output NaN on all paths,
+// so the value returned for it is irrelevant.
+__device__ __forceinline__ float sign_of(float s) {
+  return s == 0.0f ? 0.0f : copysignf(1.0f, s);
+}
+__device__ __forceinline__ double sign_of(double s) {
+  return s == 0.0 ? 0.0 : copysign(1.0, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -103,8 +113,9 @@ __device__ __forceinline__ A horner(const A (&c)[MAXC], int cnt, A x) {
 }
 
 // ---------------------------------------------------------------------------
-// One coefficient row (one group), held in registers.
+// Scalar engine: one coefficient row (one group) in registers.
 //   MM1 / MN: compile-time capacity; FIXED: m1 == MM1 and n == MN exactly.
+//   Accumulator slot layout: [0, m1) numerator terms, [MM1, MM1 + n) denominator.
 // ---------------------------------------------------------------------------
 template <typename A, bool EXACT, int MM1, int MN, bool FIXED>
 struct Rational {
@@ -137,12 +148,14 @@ struct Rational {
 
   __device__ __forceinline__ int dcount() const { return FIXED ? ND : (m1 > 1 ? m1 - 1 : 1); }
 
-  // A(x) = (b_1 + b_2 x + ...) x, 0 when n == 0 (rational.py:211-215)
+  // A(x) = (b_1 + b_2 x + ...) x, 0 when n == 0 (rational.py:211-215).
+  // ROUNDED: the reference's rounding sequence (needed for sign(A), see grad).
+  template <bool ROUNDED = EXACT>
   __device__ __forceinline__ A series(A x) const {
-    using O = Op<A, EXACT>;
+    using O = Op<A, ROUNDED>;
     if (MN == 0) return A(0);
     if (!FIXED && n == 0) return A(0);
-    return O::mul(horner<A, EXACT, NB, FIXED>(b, n, x), x);
+    return O::mul(horner<A, ROUNDED, NB, FIXED>(b, n, x), x);
   }
 
   // y = P(x) / (1 + |A(x)|)  (rational.py:218-224)
@@ -158,7 +171,8 @@ struct Rational {
   __device__ __forceinline__ A grad(A x, A u, A (&acc)[KC]) const {
     using O = Op<A, EXACT>;
     const A p = horner<A, EXACT, MM1, FIXED>(a, m1, x);
-    const A s = series(x);
+    // sign(A) is discontinuous at A's roots: always the reference's rounding.
+    const A s = series<true>(x);
     const A q = O::add(A(1), fabs(s));
     const A sg = sign_of(s);
     const A iq = O::rcp(q);
@@ -209,6 +223,145 @@ struct Rational {
 #pragma unroll
         for (int j = 0; j < MN; ++j) acc[MM1 + j] = O::mad(w, pw[j + 1], acc[MM1 + j]);
       }
+    }
+    return dx;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Packed fp32 engine for the paper's degrees (m, n) = (5, 4): element pairs.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float2 bc(float s) { return make_float2(s, s); }  // .F32 broadcast operand
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+
+// Separately rounded packed mul + add.  ptxas contracts mul.rn.f32x2 followed
+// by add.rn.f32x2 into one FFMA2 (even with explicit .rn), so the add is issued
+// as FFMA2(m, one, c) with `one` a kernel parameter the compiler cannot see is
+// 1.0: round(m * 1 + c) == round(m + c) exactly (signed zeros included), and the
+// product m = round(a * b) must be materialised because it is a multiplicand.
+__device__ __forceinline__ float2 xmad2(float2 a, float2 b, float2 c, float one) {
+  return fma2(mul2(a, b), bc(one), c);
+}
+__device__ __forceinline__ float2 xadd2(float2 a, float2 b, float one) { return fma2(a, bc(one), b); }
+__device__ __forceinline__ float2 xsub2(float2 a, float2 b, float one) { return fma2(b, bc(-one), a); }
+
+template <bool EXACT>
+struct RationalX2 {
+  static constexpr int KC = 10;
+  float a[6], b[4], da[5], db[4];
+  float one;  // opaque 1.0 (kernel parameter), see xmad2
+
+  __device__ __forceinline__ void load(const float* __restrict__ ga, const float* __restrict__ gb, int g,
+                                       float one_param) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) a[k] = __ldg(ga + g * 6 + k);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) b[k] = __ldg(gb + g * 4 + k);
+    da[0] = a[1];  // 1 * a_1 is exact
+#pragma unroll
+    for (int k = 2; k < 6; ++k) da[k - 1] = __fmul_rn(a[k], float(k));  // fp32 k*a_k, as rational.py:207
+    db[0] = b[0];
+#pragma unroll
+    for (int k = 2; k <= 4; ++k) db[k - 1] = __fmul_rn(b[k - 1], float(k));
+    one = one_param;
+  }
+
+  // -sign(s): -1 / +1 for s > 0 / s < 0, and +0 for s == +-0 (np.sign(0) = 0).
+  // One LOP3 (1.0 with the inverted sign bit of s) and one select.
+  __device__ __forceinline__ static float neg_sign(float s) {
+    const float m = __int_as_float((~__float_as_int(s) & 0x80000000) | 0x3f800000);
+    return s == 0.0f ? 0.0f : m;
+  }
+
+  // Horner on a pair with scalar (broadcast) coefficients: the reference's
+  // separately rounded acc = acc * x + c (ROUNDED) or FMA steps.
+  template <bool ROUNDED, int N>
+  __device__ __forceinline__ float2 horner2(const float (&c)[N], float2 x) const {
+    float2 acc;
+    if (ROUNDED) {
+      acc = bc(c[N - 1]);
+#pragma unroll
+      for (int k = N - 2; k >= 0; --k) acc = xmad2(acc, x, bc(c[k]), one);
+    } else {
+      acc = fma2(bc(c[N - 1]), x, bc(c[N - 2]));
+#pragma unroll
+      for (int k = N - 3; k >= 0; --k) acc = fma2(acc, x, bc(c[k]));
+    }
+    return acc;
+  }
+
+  __device__ __forceinline__ static float rcp(float q) {
+    if (EXACT) return __frcp_rn(q);
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(q));
+    return r;
+  }
+
+  __device__ __forceinline__ float2 value(float2 x) const {
+    const float2 p = horner2<EXACT, 6>(a, x);
+    const float2 s = mul2(horner2<EXACT, 4>(b, x), x);
+    const float qx = __fadd_rn(1.0f, fabsf(s.x));
+    const float qy = __fadd_rn(1.0f, fabsf(s.y));
+    if (EXACT) return make_float2(__fdiv_rn(p.x, qx), __fdiv_rn(p.y, qy));
+    return mul2(p, make_float2(rcp(qx), rcp(qy)));
+  }
+
+  __device__ __forceinline__ float2 grad(float2 x, float2 u, float2 (&acc)[KC]) const {
+    const float2 p = horner2<EXACT, 6>(a, x);
+    // A(x) is always evaluated with the reference's rounding sequence, in FAST
+    // mode too: sign(A) is discontinuous at A's roots, and an FMA-rounded A of
+    // the opposite sign flips dx there by 2 u A' P / Q^2 (seen at KAT-S).
+    const float2 s = mul2(horner2<true, 4>(b, x), x);
+    const float2 iq = make_float2(rcp(__fadd_rn(1.0f, fabsf(s.x))), rcp(__fadd_rn(1.0f, fabsf(s.y))));
+    const float2 dp = horner2<EXACT, 5>(da, x);
+    const float2 ds = horner2<EXACT, 4>(db, x);
+    const float2 pq = mul2(p, iq);
+    float2 dx;
+    if (EXACT) {
+      // dx = u * (dp*iq - ((sg*ds)*pq)*iq); terms t_i = t_{i-1} * x from u*iq;
+      // db chain from ((-(sg*u))*pq)*iq -- the reference's order, signed zeros
+      // included.  (The accumulations may fuse: only the terms are bitwise.)
+      const float2 sg = make_float2(sign_of(s.x), sign_of(s.y));
+      const float2 t1 = mul2(dp, iq);
+      const float2 t2 = mul2(mul2(mul2(sg, ds), pq), iq);
+      dx = mul2(u, xsub2(t1, t2, one));
+      float2 t = mul2(u, iq);
+      acc[0] = add2(acc[0], t);
+#pragma unroll
+      for (int i = 1; i < 6; ++i) {
+        t = mul2(t, x);
+        acc[i] = add2(acc[i], t);
+      }
+      float2 v = mul2(mul2(mul2(neg2(mul2(sg, u)), pq), iq), x);
+      acc[6] = add2(acc[6], v);
+#pragma unroll
+      for (int j = 1; j < 4; ++j) {
+        v = mul2(v, x);
+        acc[6 + j] = add2(acc[6 + j], v);
+      }
+    } else {
+      const float2 nsg = make_float2(neg_sign(s.x), neg_sign(s.y));  // -sign(A)
+      const float2 t0 = mul2(u, iq);
+      const float2 z = mul2(nsg, pq);               // -sign(A) P/q
+      dx = mul2(t0, fma2(ds, z, dp));               // (u/q) (P' - sign(A) A' P/q)
+      const float2 w = mul2(t0, z);                 // -(sign(A) u/q) P/q
+      const float2 x2 = mul2(x, x);
+      const float2 x3 = mul2(x2, x);
+      const float2 x4 = mul2(x2, x2);
+      const float2 x5 = mul2(x4, x);
+      acc[0] = add2(acc[0], t0);
+      acc[1] = fma2(t0, x, acc[1]);
+      acc[2] = fma2(t0, x2, acc[2]);
+      acc[3] = fma2(t0, x3, acc[3]);
+      acc[4] = fma2(t0, x4, acc[4]);
+      acc[5] = fma2(t0, x5, acc[5]);
+      acc[6] = fma2(w, x, acc[6]);
+      acc[7] = fma2(w, x2, acc[7]);
+      acc[8] = fma2(w, x3, acc[8]);
+      acc[9] = fma2(w, x4, acc[9]);
     }
     return dx;
   }

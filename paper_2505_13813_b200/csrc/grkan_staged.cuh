@@ -1,0 +1,407 @@
+// grkan_staged.cuh -- TMA-bulk-staged K1 / K2 for the paper's degrees (5, 4).
+//
+// The register-direct kernels (grkan_kernels.cuh) keep their loads in
+// registers, so bytes in flight per SM are bounded by register pressure and
+// the backward stalls on L1TEX (ncu: ~55% of DRAM peak, 62% of stall cycles
+// on long scoreboard).  Here a producer warp streams the CTA's rows into a
+// shared-memory ring with cp.async.bulk (the sm_90+/sm_100a TMA bulk-copy
+// engine: one instruction per contiguous row segment, completion counted in
+// bytes on an mbarrier), and eight consumer warps compute out of shared memory.
+// Bytes in flight per SM = stages x stage bytes x resident CTAs (~150 KB),
+// independent of registers.
+//
+// Stage = RS rows of the group's columns, RS = floor(768 / V) so a stage is at
+// most 768 16-byte vectors per tensor: exactly 3 per consumer thread when V
+// divides 768 (KAT-S/B, fp32 and bf16).  Each consumer thread owns the same 3
+// (row, vector) slots in every stage, so its smem and global offsets are fixed
+// per thread.  dx / y leave straight from registers with 128-bit streaming
+// stores (coalesced: consecutive threads write consecutive 16-byte vectors).
+#pragma once
+
+#include "grkan_kernels.cuh"
+
+namespace grkan {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kStagedThreads = 32 * (kConsumerWarps + 1);  // + 1 producer warp
+constexpr int kStageVecs = 768;                            // per tensor per stage
+constexpr int kVPT = kStageVecs / (32 * kConsumerWarps);   // 3 vectors per consumer thread
+constexpr int kMaxStages = 4;
+constexpr int kBwdCtasPerSm = 2;  // register cap 113: no spills, 16 consumer warps per SM
+constexpr int kFwdCtasPerSm = 3;
+
+// ---- PTX helpers: shared addresses, mbarriers, bulk copies ------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      "  .reg .pred p;\n"
+      "WAIT_%=:\n"
+      "  mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "  @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy (TMA engine), completion counted on `bar`;
+// L2 evict-first: every byte is read exactly once.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// ---- raw 16-byte vector <-> W math values ------------------------------------
+template <typename T>
+struct Raw16;
+
+template <>
+struct Raw16<float> {
+  static constexpr int W = 4;
+  static __device__ __forceinline__ void unpack(const uint4& r, float (&v)[4]) {
+    v[0] = __uint_as_float(r.x); v[1] = __uint_as_float(r.y);
+    v[2] = __uint_as_float(r.z); v[3] = __uint_as_float(r.w);
+  }
+  static __device__ __forceinline__ uint4 pack(const float (&v)[4]) {
+    return make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]),
+                      __float_as_uint(v[3]));
+  }
+};
+
+template <>
+struct Raw16<__nv_bfloat16> {
+  static constexpr int W = 8;
+  static __device__ __forceinline__ void unpack(const uint4& r, float (&v)[8]) {
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+  static __device__ __forceinline__ uint4 pack(const float (&v)[8]) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+      w[i] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+
+template <>
+struct Raw16<double> {
+  static constexpr int W = 2;
+  static __device__ __forceinline__ void unpack(const uint4& r, double (&v)[2]) {
+    v[0] = __hiloint2double(static_cast<int>(r.y), static_cast<int>(r.x));
+    v[1] = __hiloint2double(static_cast<int>(r.w), static_cast<int>(r.z));
+  }
+  static __device__ __forceinline__ uint4 pack(const double (&v)[2]) {
+    return make_uint4(static_cast<uint32_t>(__double2loint(v[0])), static_cast<uint32_t>(__double2hiint(v[0])),
+                      static_cast<uint32_t>(__double2loint(v[1])), static_cast<uint32_t>(__double2hiint(v[1])));
+  }
+};
+
+// Deterministic reduction for the staged CTA (9 warps; the producer warp adds zeros).
+template <typename A, int KC, int NWARPS>
+__device__ __forceinline__ void cta_reduce_store_n(A (&acc)[KC], A* __restrict__ part, int g,
+                                                   int64_t tile, int64_t n_tiles) {
+  __shared__ A red[NWARPS][KC];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < KC; ++k) {
+    A v = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][k] = v;
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+      A v = lane < NWARPS ? red[lane][k] : A(0);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) part[((int64_t)g * KC + k) * n_tiles + tile] = v;
+    }
+  }
+}
+
+// Persistent, statically balanced partition: CTA (g, j) of pg per group owns
+// stage units [j*nsu/pg, (j+1)*nsu/pg) of group g -- every CTA gets the same
+// number of RS-row stages to within one, so there is no tail wave.  Linear
+// id = j * ng + g: resident CTAs of all groups stream the same row band.
+__device__ __forceinline__ void staged_range(const Geom& geo, int& g, int64_t& j, int64_t& row0, int& nr) {
+  const int64_t bid = blockIdx.x;
+  g = static_cast<int>(bid % geo.ng);
+  j = bid / geo.ng;
+  const int64_t s0 = (j * geo.nsu) / geo.pg;
+  const int64_t s1 = ((j + 1) * geo.nsu) / geo.pg;
+  row0 = s0 * geo.RS;
+  const int64_t r1 = s1 * geo.RS < geo.rows ? s1 * geo.RS : geo.rows;
+  nr = static_cast<int>(r1 - row0);
+}
+
+// ---------------------------------------------------------------------------
+// Producer: lane 0 of the last warp fills the ring, one bulk copy per row
+// segment per tensor.  `nt` tensors (1 forward, 2 backward).
+// ---------------------------------------------------------------------------
+template <typename T, int NT>
+__device__ __forceinline__ void produce(const T* const (&src)[NT], T* const (&ring)[NT], const Geom& geo,
+                                        int64_t row0, int nr, int stages, uint64_t* full,
+                                        uint64_t* empty, int g) {
+  const uint64_t policy = evict_first_policy();
+  const int RS = geo.RS;
+  const int nst = (nr + RS - 1) / RS;
+  const uint32_t seg = static_cast<uint32_t>(geo.dg * sizeof(T));
+  for (int s = 0; s < nst; ++s) {
+    const int slot = s % stages;
+    if (s >= stages) mbar_wait(&empty[slot], ((s / stages) - 1) & 1);
+    const int rows_here = min(RS, nr - s * RS);
+    mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(rows_here) * seg * NT);
+    for (int r = 0; r < rows_here; ++r) {
+      const int64_t goff = (row0 + s * RS + r) * geo.d + (int64_t)g * geo.dg;
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+        bulk_g2s(ring[t] + ((size_t)slot * RS + r) * geo.dg, src[t] + goff, seg, &full[slot], policy);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2 staged: backward main pass, degrees (5, 4).
+// ---------------------------------------------------------------------------
+template <typename T, bool EXACT, bool CHECK>
+__global__ void __launch_bounds__(kStagedThreads, kBwdCtasPerSm)
+    k_bwd_staged(const T* __restrict__ x, const T* __restrict__ dy, T* __restrict__ dx,
+                 const typename VecIO<T, 1>::A* __restrict__ ca,
+                 const typename VecIO<T, 1>::A* __restrict__ cb,
+                 typename VecIO<T, 1>::A* __restrict__ part, Geom geo, int stages,
+                 DevStatus* __restrict__ st) {
+  using A = typename VecIO<T, 1>::A;
+  using RW = Raw16<T>;
+  constexpr int W = RW::W;
+  constexpr bool PK = std::is_same<A, float>::value;
+  constexpr int KC = 10;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
+  pdl_launch_dependents();
+
+  int g;
+  int64_t tile, row0;
+  int nr;
+  staged_range(geo, g, tile, row0, nr);
+  const size_t ring_elems = (size_t)stages * geo.RS * geo.dg;
+  T* const sx = reinterpret_cast<T*>(smem_raw);
+  T* const su = sx + ring_elems;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  A acc[KC];
+#pragma unroll
+  for (int k = 0; k < KC; ++k) acc[k] = A(0);
+  Checker<A> chk;
+
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      const T* const src[2] = {x, dy};
+      T* const ring[2] = {sx, su};
+      produce<T, 2>(src, ring, geo, row0, nr, stages, full, empty, g);
+    }
+  } else {
+    RationalX2<EXACT> rp;
+    Rational<A, EXACT, 6, 4, true> rs;
+    float2 acc2[KC];
+    if constexpr (PK) {
+      rp.load(reinterpret_cast<const float*>(ca), reinterpret_cast<const float*>(cb), g, geo.one);
+#pragma unroll
+      for (int k = 0; k < KC; ++k) acc2[k] = make_float2(0.f, 0.f);
+    } else {
+      rs.load(ca, cb, g, 6, 4);
+    }
+    // this thread's fixed (row, vector) slots in every stage
+    int sr[kVPT], so[kVPT];
+    T* gp[kVPT];  // running global pointers: advance by RS rows per stage
+    const int svecs = geo.RS * geo.V;
+#pragma unroll
+    for (int j = 0; j < kVPT; ++j) {
+      const int k = threadIdx.x + j * 32 * kConsumerWarps;
+      const int r = k / geo.V, c = (k - (k / geo.V) * geo.V) * W;
+      sr[j] = k < svecs ? r : 0x7fffffff;  // never valid outside the stage
+      so[j] = r * geo.dg + c;
+      gp[j] = dx + (row0 + r) * geo.d + (int64_t)g * geo.dg + c;
+    }
+    const int64_t gstep = (int64_t)geo.RS * geo.d;
+    const int slot_elems = geo.RS * geo.dg;
+    const int nst = (nr + geo.RS - 1) / geo.RS;
+    for (int s = 0; s < nst; ++s) {
+      const int slot = s % stages;
+      mbar_wait(&full[slot], (s / stages) & 1);
+      const int rows_here = min(geo.RS, nr - s * geo.RS);
+      const T* xs = sx + slot * slot_elems;
+      const T* us = su + slot * slot_elems;
+#pragma unroll
+      for (int j = 0; j < kVPT; ++j) {
+        if (sr[j] < rows_here) {
+          A vx[W], vu[W], o[W];
+          RW::unpack(*reinterpret_cast<const uint4*>(xs + so[j]), vx);
+          RW::unpack(*reinterpret_cast<const uint4*>(us + so[j]), vu);
+          if constexpr (PK) {
+#pragma unroll
+            for (int e = 0; e < W; e += 2) {
+              const float2 r2 = rp.grad(make_float2(vx[e], vx[e + 1]), make_float2(vu[e], vu[e + 1]), acc2);
+              o[e] = r2.x;
+              o[e + 1] = r2.y;
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < W; ++e) o[e] = rs.grad(vx[e], vu[e], acc);
+          }
+          if constexpr (CHECK) {
+#pragma unroll
+            for (int e = 0; e < W; ++e) {
+              chk.add(vx[e]);
+              chk.add(vu[e]);
+            }
+          }
+          __stcs(reinterpret_cast<uint4*>(gp[j]), RW::pack(o));
+        }
+        gp[j] += gstep;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
+    }
+    if constexpr (PK) {
+#pragma unroll
+      for (int k = 0; k < KC; ++k) acc[k] = acc2[k].x + acc2[k].y;
+    }
+  }
+  if (CHECK && chk.bad()) st->nonfinite_input = 1;
+  cta_reduce_store_n<A, KC, kConsumerWarps + 1>(acc, part, g, tile, geo.pg);
+}
+
+// ---------------------------------------------------------------------------
+// K1 staged: forward, degrees (5, 4).
+// ---------------------------------------------------------------------------
+template <typename T, bool EXACT, bool CHECK>
+__global__ void __launch_bounds__(kStagedThreads, kFwdCtasPerSm)
+    k_fwd_staged(const T* __restrict__ x, T* __restrict__ y, const typename VecIO<T, 1>::A* __restrict__ ca,
+                 const typename VecIO<T, 1>::A* __restrict__ cb, Geom geo, int stages,
+                 DevStatus* __restrict__ st) {
+  using A = typename VecIO<T, 1>::A;
+  using RW = Raw16<T>;
+  constexpr int W = RW::W;
+  constexpr bool PK = std::is_same<A, float>::value;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
+
+  int g;
+  int64_t tile, row0;
+  int nr;
+  staged_range(geo, g, tile, row0, nr);
+  T* const sx = reinterpret_cast<T*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      const T* const src[1] = {x};
+      T* const ring[1] = {sx};
+      produce<T, 1>(src, ring, geo, row0, nr, stages, full, empty, g);
+    }
+    return;
+  }
+  RationalX2<EXACT> rp;
+  Rational<A, EXACT, 6, 4, true> rs;
+  if constexpr (PK)
+    rp.load(reinterpret_cast<const float*>(ca), reinterpret_cast<const float*>(cb), g, geo.one);
+  else
+    rs.load(ca, cb, g, 6, 4);
+  int sr[kVPT], soff[kVPT];
+  int64_t goff[kVPT];
+  const int svecs = geo.RS * geo.V;
+#pragma unroll
+  for (int j = 0; j < kVPT; ++j) {
+    const int k = threadIdx.x + j * 32 * kConsumerWarps;
+    const int r = k / geo.V, c = k - (k / geo.V) * geo.V;
+    sr[j] = k < svecs ? r : 0x7fffffff;
+    soff[j] = r * geo.dg + c * W;
+    goff[j] = (int64_t)r * geo.d + (int64_t)g * geo.dg + c * W;
+  }
+  Checker<A> chk;
+  const int nst = (nr + geo.RS - 1) / geo.RS;
+  for (int s = 0; s < nst; ++s) {
+    const int slot = s % stages;
+    mbar_wait(&full[slot], (s / stages) & 1);
+    const int rows_here = min(geo.RS, nr - s * geo.RS);
+    const T* xs = sx + (size_t)slot * geo.RS * geo.dg;
+    T* ys = y + (row0 + (int64_t)s * geo.RS) * geo.d;
+    uint4 rx[kVPT];
+#pragma unroll
+    for (int j = 0; j < kVPT; ++j)
+      if (sr[j] < rows_here) rx[j] = *reinterpret_cast<const uint4*>(xs + soff[j]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+#pragma unroll
+    for (int j = 0; j < kVPT; ++j) {
+      if (sr[j] < rows_here) {
+        A v[W], o[W];
+        RW::unpack(rx[j], v);
+        if constexpr (PK) {
+#pragma unroll
+          for (int e = 0; e < W; e += 2) {
+            const float2 r2 = rp.value(make_float2(v[e], v[e + 1]));
+            o[e] = r2.x;
+            o[e + 1] = r2.y;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < W; ++e) o[e] = rs.value(v[e]);
+        }
+        if constexpr (CHECK) {
+#pragma unroll
+          for (int e = 0; e < W; ++e) chk.add(v[e]);
+        }
+        __stcs(reinterpret_cast<uint4*>(ys + goff[j]), RW::pack(o));
+      }
+    }
+  }
+  if (CHECK && chk.bad()) st->nonfinite_input = 1;
+}
+
+}  // namespace grkan

@@ -1,0 +1,78 @@
+// grkan_types.h -- plain types shared by the host launch code and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace grkan {
+
+struct Geom {
+  int64_t rows;     // B*L
+  int64_t n_tiles;  // ceil(rows / R)
+  int32_t d;        // feature dim (row stride, elements)
+  int32_t ng;       // groups
+  int32_t dg;       // group width
+  int32_t V;        // 16-byte vectors per row segment = dg / W
+  int32_t R;        // rows per tile (direct kernels)
+  int32_t dr, dc;   // kBlock = dr * V + dc: flat-index step in (row, vector) units
+  // staged kernels: persistent, statically balanced partition
+  int32_t RS;       // rows per pipeline stage
+  int32_t pg;       // CTAs per group (= partials per group = n_tiles)
+  int64_t nsu;      // stage units per group = ceil(rows / RS)
+  float one;        // 1.0f, opaque to ptxas (see grkan_math.cuh xmad2)
+};
+
+struct DevStatus {
+  int32_t nonfinite_input;
+  int32_t accum_overflow;
+};
+
+constexpr int kBlock = 256;    // threads per CTA for K1 / K2 / K4
+constexpr int kMinBlocks = 3;  // register cap 85 / thread -> 24 warps per SM
+
+// Vectors per tensor each thread loads before computing (must match Engine::U).
+inline int unroll_for_width(int W) { return W >= 2 ? 2 : 4; }
+
+struct Plan {
+  int W = 1;          // elements per 16-byte vector (1 = scalar path)
+  int threads = kBlock;
+  int64_t ctas = 0;
+  Geom geo{};
+  bool staged = false;  // TMA-bulk-staged persistent kernels (grkan_staged.cuh)
+  int stages = 0;       // shared-memory ring depth
+  size_t smem = 0;      // dynamic shared memory per CTA
+};
+
+constexpr int kStagedThreadsHost = 288;  // = grkan::kStagedThreads
+constexpr int kStageVecsHost = 768;      // = grkan::kStageVecs
+constexpr int kBwdCtasPerSmHost = 2;     // = grkan::kBwdCtasPerSm
+constexpr int kFwdCtasPerSmHost = 3;     // = grkan::kFwdCtasPerSm
+
+struct LaunchArgs {
+  const Plan* plan;
+  const void* x;
+  const void* dy;   // backward only
+  void* out;        // y (forward) or dx (backward)
+  const void* a;
+  const void* b;
+  void* part;       // backward partials (SoA)
+  void* da;
+  void* db;
+  DevStatus* st;
+  int m1, n;
+  bool exact, vec, check;
+  cudaStream_t stream;
+};
+
+// One entry per I/O dtype; each lives in its own translation unit.
+cudaError_t launch_fwd_f32(const LaunchArgs&);
+cudaError_t launch_fwd_bf16(const LaunchArgs&);
+cudaError_t launch_fwd_f64(const LaunchArgs&);
+cudaError_t launch_bwd_f32(const LaunchArgs&);
+cudaError_t launch_bwd_bf16(const LaunchArgs&);
+cudaError_t launch_bwd_f64(const LaunchArgs&);
+cudaError_t launch_atomic_f32(const LaunchArgs&);
+cudaError_t launch_atomic_bf16(const LaunchArgs&);
+cudaError_t launch_atomic_f64(const LaunchArgs&);
+
+}  // namespace grkan

@@ -108,14 +108,16 @@ def workspace_bytes(rows: int, d: int, ng: int, m1: int, n: int, dtype: torch.dt
 
 def rational_backward(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor, b: torch.Tensor,
                       exact: bool = False, check_finite: bool = False, check_overflow: bool = False,
-                      workspace: torch.Tensor | None = None):
+                      workspace: torch.Tensor | None = None, da_out: torch.Tensor | None = None,
+                      db_out: torch.Tensor | None = None):
     """(dx, da, db) with per-CTA partials and a deterministic second pass.
 
     Mirrors backward_blocked (pkg/src/grkan/backward.py:275-372).  da/db are
     in the coefficient dtype (fp32 for fp32/bf16 tensors).  ``check_overflow``
     synchronises and raises AccumulationOverflowError for non-finite da/db
     (_check_accumulators, backward.py:182-184); ``check_finite`` also flags
-    NaN/Inf in x / dy (validate=True).
+    NaN/Inf in x / dy (validate=True).  ``da_out``/``db_out`` may be views of
+    one flat buffer (parallel.coeff_grad_buffer) so the all-reduce needs no copy.
     """
     rows, d, ng, m1, n = _validate(x, a, b)
     if dy.shape != x.shape:
@@ -128,8 +130,11 @@ def rational_backward(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor, b: tor
     a = a.contiguous()
     b = b.contiguous()
     dx = torch.empty_like(x)
-    da = torch.empty((ng, m1), dtype=a.dtype, device=x.device)
-    db = torch.empty((ng, n), dtype=a.dtype, device=x.device)
+    da = torch.empty((ng, m1), dtype=a.dtype, device=x.device) if da_out is None else da_out
+    db = torch.empty((ng, n), dtype=a.dtype, device=x.device) if db_out is None else db_out
+    for t, shp in ((da, (ng, m1)), (db, (ng, n))):
+        if tuple(t.shape) != shp or t.dtype != a.dtype or not t.is_contiguous():
+            raise ValueError("gradient output must be a contiguous %s tensor of shape %s" % (a.dtype, shp))
     nbytes = workspace_bytes(rows, d, ng, m1, n, x.dtype)
     if workspace is None or workspace.numel() < nbytes:
         workspace = torch.empty(nbytes, dtype=torch.uint8, device=x.device)

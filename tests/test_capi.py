@@ -82,18 +82,31 @@ def test_plan_geometry(dtype, es):
         assert w in (1, 16 // es)
         if (dg * es) % 16 == 0:
             assert w == 16 // es
+            assert p["staged"] == (dg // w <= 768)
+        else:
+            assert not p["staged"]
         assert dg % w == 0
-        assert p["threads"] % 32 == 0 or p["threads"] < 32 or p["threads"] == dg // w * 1
-        assert 0 < p["threads"] <= 512
-        assert p["row_tiles"] * p["rows_per_tile"] >= rows
-        assert (p["row_tiles"] - 1) * p["rows_per_tile"] < rows
-        assert p["ctas"] == p["row_tiles"] * g
+        assert p["ctas"] == p["partials_per_group"] * g
+        if p["staged"]:
+            assert p["threads"] == 288
+            rs = p["rows_per_unit"]
+            assert rs == 768 // (dg // w)
+            stage_units = -(-rows // rs)
+            assert 1 <= p["partials_per_group"] <= stage_units
+            assert p["ctas"] <= 3 * 148 or p["partials_per_group"] == 1
+        else:
+            assert p["threads"] == 256
+            R = p["rows_per_unit"]
+            assert p["partials_per_group"] * R >= rows > (p["partials_per_group"] - 1) * R
         ws = N.lib().grkan_bwd_workspace_bytes(rows, d, g, 6, 4, dtype)
         acc = 8 if dtype == N.DT_F64 else 4
         assert ws >= 256 + p["ctas"] * 10 * acc
+        # generic degrees never take the staged path
+        assert not N.plan(rows, d, g, 4, 2, dtype)["staged"]
 
 
-def test_kat_b_plan_is_wide():
+def test_kat_b_plan_is_persistent_and_balanced():
     p = N.plan(256 * 197, 3072, 8, 6, 4, N.DT_F32)
-    assert p["vector_width"] == 4 and p["threads"] == 288
-    assert p["ctas"] >= 4 * 148 * 4  # many waves: the HW block scheduler balances the tail
+    assert p["vector_width"] == 4 and p["staged"] and p["threads"] == 288
+    assert p["rows_per_unit"] == 8  # 8 rows x 96 float4 = 768 vectors per stage
+    assert p["ctas"] == 8 * (2 * 148 // 8)  # one persistent CTA per resident slot
