@@ -66,6 +66,16 @@ def parse_args(argv=None):
     return p.parse_args(argv)
 
 
+def ncu_traffic(args, kind):
+    """DRAM bytes per launch for this workload from the committed ncu capture, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            d = json.load(fh)
+        return d["%s/%s/%s/%s" % (args.config, args.dtype, args.mode, kind)]["bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -191,6 +201,10 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+
+def world_ok(args):
+    return args.scaling == "weak" or args.gpus == 1
+
 
 def run_b200(args, rank, world, local_rank):
     import numpy as np
@@ -350,11 +364,12 @@ def run_b200(args, rank, world, local_rank):
         "roofline": {
             "bound": "hbm", "kernel": "grkan_bwd (K2 bwd_main + K3 reduce)",
             "achieved": bwd_gbs, "peak": peak, "unit": "GB/s", "frac": bwd_gbs / peak,
-            "peak_source": peak_src, "traffic": None,
+            "peak_source": peak_src, "traffic": ncu_traffic(args, "bwd") if world_ok(args) else None,
             "algorithmic_bytes_per_launch": bwd_bytes, "launch_us": bwd_ms * 1e3,
         },
         "kernels": {
             "fwd_us": fwd_ms * 1e3, "fwd_gbs": fwd_gbs, "fwd_frac": fwd_gbs / peak,
+            "fwd_traffic": ncu_traffic(args, "fwd"),
             "bwd_us": bwd_ms * 1e3, "bwd_gbs": bwd_gbs, "bwd_frac": bwd_gbs / peak,
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * es * E,
