@@ -116,7 +116,11 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
     p.geo.RS = RS;
     p.geo.nsu = nsu;
     p.geo.pg = static_cast<int32_t>(pg);
-    p.geo.n_tiles = pg;
+    p.geo.flush = grkan::kFlushStages;
+    const int64_t max_st = (nsu + pg - 1) / pg;  // most stages any CTA owns
+    p.geo.nflush = static_cast<int32_t>(max_st > 0 ? (max_st + p.geo.flush - 1) / p.geo.flush : 1);
+    // partials per (group, coefficient) for K3 (backward: one per warp flush)
+    p.geo.n_tiles = nt == 2 ? pg * grkan::kConsumerWarpsHost * p.geo.nflush : pg;
     p.ctas = rows > 0 ? pg * ng : 0;
     return p;
   }

@@ -123,29 +123,30 @@ struct Raw16<double> {
   }
 };
 
-// Deterministic reduction for the staged CTA (9 warps; the producer warp adds zeros).
-template <typename A, int KC, int NWARPS>
-__device__ __forceinline__ void cta_reduce_store_n(A (&acc)[KC], A* __restrict__ part, int g,
-                                                   int64_t tile, int64_t n_tiles) {
-  __shared__ A red[NWARPS][KC];
+// Warp-level flush: fold this warp's per-lane accumulators (fixed butterfly)
+// into partial slot (CTA j, warp w, flush f) of every coefficient and zero
+// them.  Partials: part[((g * KC + k) * pg + j) * (8 * nflush) + w * nflush + f],
+// i.e. n_tiles = pg * 8 * nflush partials per (group, coefficient) for K3.
+template <typename A, int KC, bool PK>
+__device__ __forceinline__ void warp_flush(A (&acc)[KC], float2 (&acc2)[KC], A* __restrict__ part, int g,
+                                           int64_t j, int warp, int f, const Geom& geo) {
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+  const int64_t per_cta = (int64_t)kConsumerWarps * geo.nflush;
+  const int64_t n_tiles = (int64_t)geo.pg * per_cta;
+  const int64_t slot = j * per_cta + (int64_t)warp * geo.nflush + f;
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
-    A v = acc[k];
+    A v;
+    if constexpr (PK) {
+      v = acc2[k].x + acc2[k].y;
+      acc2[k] = make_float2(0.f, 0.f);
+    } else {
+      v = acc[k];
+      acc[k] = A(0);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) red[warp][k] = v;
-  }
-  __syncthreads();
-  if (warp == 0) {
-#pragma unroll
-    for (int k = 0; k < KC; ++k) {
-      A v = lane < NWARPS ? red[lane][k] : A(0);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) part[((int64_t)g * KC + k) * n_tiles + tile] = v;
-    }
+    if (lane == 0) part[((int64_t)g * KC + k) * n_tiles + slot] = v;
   }
 }
 
@@ -299,14 +300,20 @@ __global__ void __launch_bounds__(kStagedThreads, kBwdCtasPerSm)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
+      // Every geo.flush stages (and at the end) the warp folds its lanes'
+      // accumulators into one partial and restarts them: per-lane sequential
+      // fp32 sums stay short (<= 48 terms at F = 8), which keeps the da/db
+      // rounding error near the fp32 term-evaluation floor.
+      if ((s + 1) % geo.flush == 0 || s + 1 == nst) {
+        warp_flush<A, KC, PK>(acc, acc2, part, g, tile, warp, s / geo.flush, geo);
+      }
     }
-    if constexpr (PK) {
-#pragma unroll
-      for (int k = 0; k < KC; ++k) acc[k] = acc2[k].x + acc2[k].y;
-    }
+    // unused flush slots of this warp (CTAs own nst or nst - 1 stages... any
+    // count up to geo.nflush * geo.flush): write zeros so K3 can sum every slot
+    for (int f = (nst + geo.flush - 1) / geo.flush; f < geo.nflush; ++f)
+      warp_flush<A, KC, PK>(acc, acc2, part, g, tile, warp, f, geo);
   }
   if (CHECK && chk.bad()) st->nonfinite_input = 1;
-  cta_reduce_store_n<A, KC, kConsumerWarps + 1>(acc, part, g, tile, geo.pg);
 }
 
 // ---------------------------------------------------------------------------

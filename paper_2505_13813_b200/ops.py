@@ -88,6 +88,8 @@ def rational_forward(x: torch.Tensor, a: torch.Tensor, b: torch.Tensor, exact: b
     a = a.contiguous()
     b = b.contiguous()
     y = torch.empty_like(x) if out is None else out
+    if y.shape != x.shape or y.dtype != x.dtype or not y.is_contiguous():
+        raise ValueError("out must be a contiguous tensor like x")
     status = torch.zeros(2, dtype=torch.int32, device=x.device) if check_finite else None
     with torch.cuda.device(x.device):
         rc = N.lib().grkan_fwd(x.data_ptr(), y.data_ptr(), a.data_ptr(), _ptr(b), rows, d, ng, m1, n,
@@ -109,7 +111,7 @@ def workspace_bytes(rows: int, d: int, ng: int, m1: int, n: int, dtype: torch.dt
 def rational_backward(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor, b: torch.Tensor,
                       exact: bool = False, check_finite: bool = False, check_overflow: bool = False,
                       workspace: torch.Tensor | None = None, da_out: torch.Tensor | None = None,
-                      db_out: torch.Tensor | None = None):
+                      db_out: torch.Tensor | None = None, dx_out: torch.Tensor | None = None):
     """(dx, da, db) with per-CTA partials and a deterministic second pass.
 
     Mirrors backward_blocked (pkg/src/grkan/backward.py:275-372).  da/db are
@@ -129,7 +131,9 @@ def rational_backward(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor, b: tor
     dy = dy.contiguous()
     a = a.contiguous()
     b = b.contiguous()
-    dx = torch.empty_like(x)
+    dx = torch.empty_like(x) if dx_out is None else dx_out
+    if dx.shape != x.shape or dx.dtype != x.dtype or not dx.is_contiguous():
+        raise ValueError("dx_out must be a contiguous tensor like x")
     da = torch.empty((ng, m1), dtype=a.dtype, device=x.device) if da_out is None else da_out
     db = torch.empty((ng, n), dtype=a.dtype, device=x.device) if db_out is None else db_out
     for t, shp in ((da, (ng, m1)), (db, (ng, n))):

@@ -86,15 +86,19 @@ def test_plan_geometry(dtype, es):
         else:
             assert not p["staged"]
         assert dg % w == 0
-        assert p["ctas"] == p["partials_per_group"] * g
         if p["staged"]:
             assert p["threads"] == 288
             rs = p["rows_per_unit"]
             assert rs == 768 // (dg // w)
             stage_units = -(-rows // rs)
-            assert 1 <= p["partials_per_group"] <= stage_units
-            assert p["ctas"] <= 3 * 148 or p["partials_per_group"] == 1
+            pg = p["ctas"] // g  # persistent CTAs per group
+            assert p["ctas"] == pg * g and 1 <= pg <= stage_units
+            assert p["ctas"] <= 2 * 148 or pg == 1
+            # one partial per consumer warp per flush of 8 stages
+            nflush = -(-(-(-stage_units // pg)) // 8)
+            assert p["partials_per_group"] == pg * 8 * nflush
         else:
+            assert p["ctas"] == p["partials_per_group"] * g
             assert p["threads"] == 256
             R = p["rows_per_unit"]
             assert p["partials_per_group"] * R >= rows > (p["partials_per_group"] - 1) * R

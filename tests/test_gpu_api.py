@@ -357,3 +357,28 @@ def test_torch_compile_traces_the_custom_ops():
     assert torch.equal(out, eager)
     out.sum().backward()
     assert x.grad is not None
+
+
+def test_host_pipeline_matches_one_shot():
+    """streaming.HostPipeline: chunked pinned-host fwd+bwd == one-shot device results."""
+    from paper_2505_13813_b200 import ops
+    from paper_2505_13813_b200.streaming import HostPipeline
+    torch.manual_seed(6)
+    x = torch.randn(7, 197, 768)
+    dy = torch.randn_like(x)
+    a = torch.randn(8, 6, device=DEV)
+    b = torch.randn(8, 4, device=DEV)
+    xh, dyh = x.pin_memory(), dy.pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    dxh = torch.empty_like(xh).pin_memory()
+    pipe = HostPipeline(DEV, 768, 8, chunk_rows=300)  # 1379 rows -> 5 chunks, ragged tail
+    for exact in (False, True):
+        da, db = pipe.fwd_bwd(xh, dyh, a, b, yh, dxh, exact=exact)
+        torch.cuda.synchronize()
+        y_ref = ops.rational_forward(x.to(DEV), a, b, exact=exact)
+        dx_ref, da_ref, db_ref = ops.rational_backward(x.to(DEV), dy.to(DEV), a, b, exact=exact)
+        assert torch.equal(yh, y_ref.cpu()) and torch.equal(dxh, dx_ref.cpu())
+        rel = lambda u, v: ((u - v).abs().max() / v.abs().max()).item()  # noqa: E731
+        assert rel(da, da_ref) <= 1e-6 and rel(db, db_ref) <= 1e-6
+        da2, db2 = pipe.fwd_bwd(xh, dyh, a, b, yh, dxh, exact=exact)
+        assert torch.equal(da, da2) and torch.equal(db, db2)  # deterministic
