@@ -46,6 +46,8 @@ CONFIGS = {  # (batch per GPU, seq, dim, groups)
     "kat-s": (128, 197, 1536, 8),
     "kat-b": (256, 197, 3072, 8),
 }
+TRAIN_CONFIGS = {"kat-b-train": "kat_b", "kat-s-train": "kat_s", "kat-t-train": "kat_t"}
+TRAIN_METRIC = "KAT training throughput, images/s (synthetic 224x224 batch, bf16 autocast, AdamW)"
 M1, NDEN = 6, 4
 FALLBACK_HBM_GBS = 6650.0
 
@@ -57,7 +59,8 @@ def parse_args(argv=None):
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=("b200", "reference"), default="b200")
     p.add_argument("--dtype", choices=("fp32", "bf16"), default="fp32")
-    p.add_argument("--config", choices=tuple(CONFIGS), default="kat-b")
+    p.add_argument("--config", choices=tuple(CONFIGS) + tuple(TRAIN_CONFIGS), default="kat-b")
+    p.add_argument("--batch", type=int, default=128, help="images per GPU for the *-train configs")
     p.add_argument("--mode", choices=("fast", "exact"), default="fast")
     p.add_argument("--scaling", choices=("weak", "strong"), default="weak")
     p.add_argument("--e2e-steps", type=int, default=None)
@@ -415,6 +418,70 @@ def run_b200(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# Config 4: full KAT training step -- images/s, not the headline
+# ---------------------------------------------------------------------------
+
+def run_train(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_13813_b200 import kat
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    torch.manual_seed(1234 + rank)
+    model = getattr(kat, TRAIN_CONFIGS[args.config])().to(dev)
+    if world > 1:
+        model = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local_rank])
+    opt = torch.optim.AdamW(model.parameters(), lr=1e-4, weight_decay=0.05, fused=True)
+    B = args.batch
+    imgs = torch.randn(B, 3, 224, 224, device=dev)
+    labels = torch.randint(0, 1000, (B,), device=dev)
+    loss_fn = torch.nn.CrossEntropyLoss()
+
+    def step():
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = loss_fn(model(imgs), labels)
+        loss.backward()
+        opt.step()
+        opt.zero_grad(set_to_none=True)
+        return loss
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    e0.record()
+    for _ in range(args.steps):
+        loss = step()
+    e1.record()
+    torch.cuda.synchronize()
+    sampler.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    if rank == 0:
+        n_params = sum(p.numel() for p in model.parameters())
+        print(json.dumps({
+            "metric": TRAIN_METRIC, "value": world * B / (ms / 1e3), "unit": "images/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic images N(0,1), random labels",
+            "config": {"workload": args.config, "model": TRAIN_CONFIGS[args.config], "params": n_params,
+                       "batch_per_gpu": B, "global_batch": B * world, "parallelism": "ddp%d" % world},
+            "final_loss": float(loss.item()), "clocks": sampler.summary(),
+            "paper_h200_images_s": {"kat_b": 1801.75, "kat_s": 3741.91, "kat_t": 6317.90}[TRAIN_CONFIGS[args.config]],
+        }), flush=True)
+
+
 def main(argv=None):
     args = parse_args(argv)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -430,6 +497,9 @@ def main(argv=None):
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
+        if args.config in TRAIN_CONFIGS:
+            run_train(args, rank, world, local_rank)
+            return
         run_b200(args, rank, world, local_rank)
     finally:
         if world > 1:

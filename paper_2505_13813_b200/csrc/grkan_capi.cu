@@ -99,6 +99,8 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
     p.staged = true;
     p.stages = nt == 2 ? kStagesPerTensorPair : kStagesSingle;
     p.smem = static_cast<size_t>(p.stages) * nt * RS * dg * es;
+    if (nt == 2)  // + per-lane accumulator totals [10][256] in the accumulation type
+      p.smem += static_cast<size_t>(m1 + n) * 32 * grkan::kConsumerWarpsHost * (es == 8 ? 8 : 4);
     const int occ_regs = nt == 2 ? grkan::kBwdCtasPerSmHost : grkan::kFwdCtasPerSmHost;
     int occ = static_cast<int>(kSmemPerSm / (p.smem + 2048));
     occ = occ < 1 ? 1 : (occ > occ_regs ? occ_regs : occ);
@@ -117,10 +119,9 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
     p.geo.nsu = nsu;
     p.geo.pg = static_cast<int32_t>(pg);
     p.geo.flush = grkan::kFlushStages;
-    const int64_t max_st = (nsu + pg - 1) / pg;  // most stages any CTA owns
-    p.geo.nflush = static_cast<int32_t>(max_st > 0 ? (max_st + p.geo.flush - 1) / p.geo.flush : 1);
-    // partials per (group, coefficient) for K3 (backward: one per warp flush)
-    p.geo.n_tiles = nt == 2 ? pg * grkan::kConsumerWarpsHost * p.geo.nflush : pg;
+    p.geo.nflush = 0;
+    // partials per (group, coefficient) for K3 (backward: one per consumer warp)
+    p.geo.n_tiles = nt == 2 ? pg * grkan::kConsumerWarpsHost : pg;
     p.ctas = rows > 0 ? pg * ng : 0;
     return p;
   }

@@ -123,17 +123,12 @@ struct Raw16<double> {
   }
 };
 
-// Warp-level flush: fold this warp's per-lane accumulators (fixed butterfly)
-// into partial slot (CTA j, warp w, flush f) of every coefficient and zero
-// them.  Partials: part[((g * KC + k) * pg + j) * (8 * nflush) + w * nflush + f],
-// i.e. n_tiles = pg * 8 * nflush partials per (group, coefficient) for K3.
+// Accumulator flush: every geo.flush stages each lane folds its register
+// accumulators into a private fp32 slot in shared memory ([k][thread], bank-
+// conflict free) and restarts them, so per-lane fp32 chains stay short
+// (<= 6 * flush terms) at ~40 instructions per flush.
 template <typename A, int KC, bool PK>
-__device__ __forceinline__ void warp_flush(A (&acc)[KC], float2 (&acc2)[KC], A* __restrict__ part, int g,
-                                           int64_t j, int warp, int f, const Geom& geo) {
-  const int lane = threadIdx.x & 31;
-  const int64_t per_cta = (int64_t)kConsumerWarps * geo.nflush;
-  const int64_t n_tiles = (int64_t)geo.pg * per_cta;
-  const int64_t slot = j * per_cta + (int64_t)warp * geo.nflush + f;
+__device__ __forceinline__ void lane_flush(A (&acc)[KC], float2 (&acc2)[KC], A* __restrict__ sacc) {
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
     A v;
@@ -144,9 +139,24 @@ __device__ __forceinline__ void warp_flush(A (&acc)[KC], float2 (&acc2)[KC], A* 
       v = acc[k];
       acc[k] = A(0);
     }
+    sacc[k * (32 * kConsumerWarps) + threadIdx.x] += v;
+  }
+}
+
+// End of CTA: each consumer warp folds its lanes' shared-memory totals with a
+// fixed butterfly into partial slot (CTA j, warp w):
+// part[((g * KC + k) * pg + j) * 8 + w]  ->  n_tiles = pg * 8 per (group, coefficient).
+template <typename A, int KC>
+__device__ __forceinline__ void warp_store(const A* __restrict__ sacc, A* __restrict__ part, int g, int64_t j,
+                                           int warp, const Geom& geo) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_tiles = (int64_t)geo.pg * kConsumerWarps;
+#pragma unroll
+  for (int k = 0; k < KC; ++k) {
+    A v = sacc[k * (32 * kConsumerWarps) + threadIdx.x];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) part[((int64_t)g * KC + k) * n_tiles + slot] = v;
+    if (lane == 0) part[((int64_t)g * KC + k) * n_tiles + j * kConsumerWarps + warp] = v;
   }
 }
 
@@ -217,6 +227,8 @@ __global__ void __launch_bounds__(kStagedThreads, kBwdCtasPerSm)
   const size_t ring_elems = (size_t)stages * geo.RS * geo.dg;
   T* const sx = reinterpret_cast<T*>(smem_raw);
   T* const su = sx + ring_elems;
+  // per-consumer-lane accumulator totals, [KC][256], after the two rings
+  A* const sacc = reinterpret_cast<A*>(su + ring_elems);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -224,6 +236,10 @@ __global__ void __launch_bounds__(kStagedThreads, kBwdCtasPerSm)
       mbar_init(&empty[s], kConsumerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 32 * kConsumerWarps) {
+#pragma unroll
+    for (int k = 0; k < 10; ++k) sacc[k * (32 * kConsumerWarps) + threadIdx.x] = 0;
   }
   __syncthreads();
 
@@ -300,18 +316,12 @@ __global__ void __launch_bounds__(kStagedThreads, kBwdCtasPerSm)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
-      // Every geo.flush stages (and at the end) the warp folds its lanes'
-      // accumulators into one partial and restarts them: per-lane sequential
-      // fp32 sums stay short (<= 48 terms at F = 8), which keeps the da/db
-      // rounding error near the fp32 term-evaluation floor.
-      if ((s + 1) % geo.flush == 0 || s + 1 == nst) {
-        warp_flush<A, KC, PK>(acc, acc2, part, g, tile, warp, s / geo.flush, geo);
-      }
+      // Short per-lane fp32 chains keep the da/db rounding error near the fp32
+      // term-evaluation floor (see lane_flush).
+      if ((s + 1) % geo.flush == 0 || s + 1 == nst) lane_flush<A, KC, PK>(acc, acc2, sacc);
     }
-    // unused flush slots of this warp (CTAs own nst or nst - 1 stages... any
-    // count up to geo.nflush * geo.flush): write zeros so K3 can sum every slot
-    for (int f = (nst + geo.flush - 1) / geo.flush; f < geo.nflush; ++f)
-      warp_flush<A, KC, PK>(acc, acc2, part, g, tile, warp, f, geo);
+    __syncwarp();
+    warp_store<A, KC>(sacc, part, g, tile, warp, geo);
   }
   if (CHECK && chk.bad()) st->nonfinite_input = 1;
 }

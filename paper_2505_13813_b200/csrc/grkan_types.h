@@ -20,8 +20,8 @@ struct Geom {
   int32_t pg;       // CTAs per group (= partials per group = n_tiles)
   int64_t nsu;      // stage units per group = ceil(rows / RS)
   float one;        // 1.0f, opaque to ptxas (see grkan_math.cuh xmad2)
-  int32_t flush;    // staged backward: stages between per-warp accumulator flushes
-  int32_t nflush;   // flush slots per warp = ceil(max stages per CTA / flush)
+  int32_t flush;    // staged backward: stages between per-lane accumulator flushes
+  int32_t nflush;   // (unused, kept 0)
 };
 
 struct DevStatus {
@@ -50,7 +50,7 @@ constexpr int kStageVecsHost = 768;      // = grkan::kStageVecs
 constexpr int kBwdCtasPerSmHost = 2;     // = grkan::kBwdCtasPerSm
 constexpr int kFwdCtasPerSmHost = 3;     // = grkan::kFwdCtasPerSm
 constexpr int kConsumerWarpsHost = 8;    // = grkan::kConsumerWarps
-constexpr int kFlushStages = 8;          // per-lane fp32 chains <= 8 stages x 6 terms
+constexpr int kFlushStages = 4;          // per-lane fp32 register chains <= 4 stages x 6 terms
 
 struct LaunchArgs {
   const Plan* plan;
