@@ -302,6 +302,21 @@ def run_b200(args, rank, world, local_rank):
     ms_step = ms_total / K
     value = world * E / (ms_step / 1e3)
 
+    # ---- the paper's Alg. 1 comparator (per-element atomicAdd), same inputs ----------------
+    alg1_us = None
+    if world == 1:
+        st = torch.zeros(2, dtype=torch.int32, device=dev)
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for it in range(2):
+            ea.record(stream)
+            rc = L.grkan_bwd_atomic(x.data_ptr(), dy.data_ptr(), a.data_ptr(), b.data_ptr(), dx.data_ptr(),
+                                    da.data_ptr(), db.data_ptr(), rows, dim, groups, M1, NDEN, dt_code,
+                                    flags, st.data_ptr(), sp)
+            eb.record(stream)
+            assert rc == 0, N.last_error()
+        torch.cuda.synchronize()
+        alg1_us = ea.elapsed_time(eb) * 1e3
+
     # ---- e2e with host buffers: pinned x, dy in; y, dx, da, db out every step ----------
     # (a) streaming API: chunked, copy-in / compute / copy-out overlapped on 3 streams
     # (b) plain autograd on the whole tensor (GroupRationalFn.apply + backward)
@@ -405,6 +420,9 @@ def run_b200(args, rank, world, local_rank):
                 "autograd_value": world * E / (e2e_auto_ms / 1e3)},
         "clocks": sampler.summary(),
         "gpu_launches": 3 * K,
+        "alg1_atomic_comparator": None if alg1_us is None else {
+            "bwd_us": alg1_us, "speedup_of_staged_bwd": alg1_us / (bwd_ms * 1e3),
+            "note": "paper: FlashKAT bwd 140.5x faster than KAT's atomic bwd on RTX 4060 Ti (PAPER.md:402)"},
     }
     if world == 1 and not args.no_cpu_baseline:
         sb = min(args.cpu_sample_batch, cfg[0])

@@ -382,3 +382,24 @@ def test_host_pipeline_matches_one_shot():
         assert rel(da, da_ref) <= 1e-6 and rel(db, db_ref) <= 1e-6
         da2, db2 = pipe.fwd_bwd(xh, dyh, a, b, yh, dxh, exact=exact)
         assert torch.equal(da, da2) and torch.equal(db, db2)  # deterministic
+
+
+def test_kat_training_smoke():
+    """KAT-T (GR-KAN MLPs on the B200 unit) fits a fixed tiny batch (cf. pkg/tests/test_acceptance.py:174-229)."""
+    from paper_2505_13813_b200 import kat
+    torch.manual_seed(7)
+    model = kat.KAT(img=32, patch=8, dim=96, depth=2, heads=3, classes=10).to(DEV)
+    imgs = torch.randn(16, 3, 32, 32, device=DEV)
+    labels = torch.randint(0, 10, (16,), device=DEV)
+    opt = torch.optim.AdamW(model.parameters(), lr=3e-3)
+    losses = []
+    for _ in range(60):
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = torch.nn.functional.cross_entropy(model(imgs), labels)
+        loss.backward()
+        opt.step()
+        opt.zero_grad(set_to_none=True)
+        losses.append(loss.item())
+    assert losses[-1] < 0.1 * losses[0]
+    act = model.blocks[0].mlp.act2
+    assert not torch.equal(act.a.detach().cpu(), kat.GroupRational(8, init="swish").a.detach())  # trained

@@ -121,3 +121,16 @@ def test_module_construction_cpu():
     m2 = GroupRational(4, init="identity", degrees=(3, 2))
     assert m2.a.shape == (4, 4) and m2.b.shape == (4, 2)
     assert "num_groups=4" in repr(m2)
+
+
+def test_kat_model_shapes_and_init_cpu():
+    from paper_2505_13813_b200 import kat
+    m = kat.kat_t()
+    assert abs(sum(p.numel() for p in m.parameters()) - 5.7e6) < 0.1e6  # PAPER.md Table: 5.7 M
+    mlp = m.blocks[0].mlp
+    assert mlp.act1.init == "identity" and mlp.act2.init == "swish"
+    # variance-preserving: std(W) = 1 / sqrt(alpha * d_in) (pkg/src/grkan/layer.py:293-315)
+    alpha = kat.rational_alpha(mlp.act2)
+    std = mlp.fc2.weight.std().item()
+    assert abs(std - (alpha * mlp.fc2.in_features) ** -0.5) < 0.02 * std
+    assert abs(kat.rational_alpha(mlp.act1) - 1.0) < 0.02
