@@ -67,6 +67,9 @@ def parse_args(argv=None):
     p.add_argument("--cpu-sample-batch", type=int, default=16)
     p.add_argument("--cpu-passes", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--dist-backend", default="nccl",
+                   help="torch.distributed backend for N > 1 (gloo only to exercise the multi-rank "
+                        "code path when several ranks share one GPU)")
     return p.parse_args(argv)
 
 
@@ -151,6 +154,15 @@ def config_block(args, cfg):
 # ---------------------------------------------------------------------------
 # Clock sampling during the timed region (NVML)
 # ---------------------------------------------------------------------------
+
+def nvml_index(dev):
+    """NVML index of a torch CUDA device (honours CUDA_VISIBLE_DEVICES)."""
+    import torch
+    try:
+        return torch.cuda._get_nvml_device_index(dev)
+    except Exception:
+        return dev.index or 0
+
 
 class ClockSampler:
     REASONS = {
@@ -273,8 +285,7 @@ def run_b200(args, rank, world, local_rank):
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ
-                           else local_rank)
+    sampler = ClockSampler(nvml_index(dev))
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -473,7 +484,7 @@ def run_train(args, rank, world, local_rank):
         dist.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(nvml_index(dev))
     sampler.start()
     e0.record()
     for _ in range(args.steps):
@@ -512,8 +523,13 @@ def main(argv=None):
         import torch
         import torch.distributed as dist
 
+        ngpu = torch.cuda.device_count()
+        local_rank = local_rank % ngpu  # ranks may share a GPU when testing with gloo
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(args.dist_backend)
     try:
         if args.config in TRAIN_CONFIGS:
             run_train(args, rank, world, local_rank)

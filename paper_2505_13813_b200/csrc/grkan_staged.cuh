@@ -27,7 +27,15 @@ constexpr int kStagedThreads = 32 * (kConsumerWarps + 1);  // + 1 producer warp
 constexpr int kStageVecs = 768;                            // per tensor per stage
 constexpr int kVPT = kStageVecs / (32 * kConsumerWarps);   // 3 vectors per consumer thread
 constexpr int kMaxStages = 4;
-constexpr int kBwdCtasPerSm = 2;  // register cap 113: no spills, 16 consumer warps per SM
+// Backward CTAs per SM (register cap = 64K / (288 * MINB)).  Measured at
+// KAT-B: 2 CTAs, 4-stage ring, unrolled vectors is best for both fp32 and
+// bf16 (bf16 with 3 CTAs at 72 registers, 2-stage ring, serial vectors:
+// 311 us vs 279 us -- the bf16 backward is FMA-pipe bound, not warp bound).
+template <typename T>
+struct BwdCfg {
+  static constexpr int kMinBlocks = 2;
+  static constexpr bool kSerialVectors = false;
+};
 constexpr int kFwdCtasPerSm = 3;
 
 // ---- PTX helpers: shared addresses, mbarriers, bulk copies ------------------
@@ -205,7 +213,7 @@ __device__ __forceinline__ void produce(const T* const (&src)[NT], T* const (&ri
 // K2 staged: backward main pass, degrees (5, 4).
 // ---------------------------------------------------------------------------
 template <typename T, bool EXACT, bool CHECK>
-__global__ void __launch_bounds__(kStagedThreads, kBwdCtasPerSm)
+__global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
     k_bwd_staged(const T* __restrict__ x, const T* __restrict__ dy, T* __restrict__ dx,
                  const typename VecIO<T, 1>::A* __restrict__ ca,
                  const typename VecIO<T, 1>::A* __restrict__ cb,
@@ -286,7 +294,7 @@ __global__ void __launch_bounds__(kStagedThreads, kBwdCtasPerSm)
       const int rows_here = min(geo.RS, nr - s * geo.RS);
       const T* xs = sx + slot * slot_elems;
       const T* us = su + slot * slot_elems;
-#pragma unroll
+#pragma unroll(BwdCfg<T>::kSerialVectors ? 1 : kVPT)
       for (int j = 0; j < kVPT; ++j) {
         if (sr[j] < rows_here) {
           A vx[W], vu[W], o[W];

@@ -47,7 +47,7 @@ struct Plan {
 
 constexpr int kStagedThreadsHost = 288;  // = grkan::kStagedThreads
 constexpr int kStageVecsHost = 768;      // = grkan::kStageVecs
-constexpr int kBwdCtasPerSmHost = 2;     // = grkan::kBwdCtasPerSm
+constexpr int kBwdCtasPerSmHost = 2;     // = grkan::BwdCfg<T>::kMinBlocks
 constexpr int kFwdCtasPerSmHost = 3;     // = grkan::kFwdCtasPerSm
 constexpr int kConsumerWarpsHost = 8;    // = grkan::kConsumerWarps
 constexpr int kFlushStages = 4;          // per-lane fp32 register chains <= 4 stages x 6 terms
