@@ -394,3 +394,18 @@ def elementwise_grads(x: float, upstream: float, numerator, denominator,
     dx, da, db = ops.rational_backward(xd, ud, a, b, exact=True)
     return ElementGrads(d_x=float(dx.reshape(-1)[0]), d_a=da.cpu().numpy().reshape(-1),
                         d_b=db.cpu().numpy().reshape(-1))
+
+
+# ---------------------------------------------------------------------------
+# GRKB dumps (cli.py:104-129)
+# ---------------------------------------------------------------------------
+
+def write_tensor_dump(path: str, tensor: ActivationTensor) -> None:
+    from . import grkb
+    grkb.save(path, tensor.data)
+
+
+def read_tensor_dump(path: str) -> ActivationTensor:
+    from . import grkb
+    return ActivationTensor(grkb.load(path))
+

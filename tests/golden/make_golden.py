@@ -229,6 +229,13 @@ def main():
         scalar(float(rng.uniform(-5, 5)), float(rng.standard_normal()),
                list(rng.standard_normal(6)), list(rng.standard_normal(4)), "random %d" % k)
 
+    # --- GRKB tensor dumps written by the reference (cli.py:104-129) ------------------
+    from grkan.cli import write_tensor_dump
+    for case, key, fname in (("f32_2x4x16_g2", "dx", "dx_f32_2x4x16.grkb"),
+                             ("f64_2x3x8_g2", "x", "x_f64_2x3x8.grkb")):
+        write_tensor_dump(os.path.join(HERE, fname), g.ActivationTensor(arrays["%s/%s" % (case, key)]))
+        manifest.setdefault("grkb", {})[fname] = {"case": case, "key": key}
+
     np.savez_compressed(os.path.join(HERE, "grkan_golden.npz"), **arrays)
     with open(os.path.join(HERE, "grkan_golden.json"), "w") as fh:
         json.dump(manifest, fh, indent=1, sort_keys=True)

@@ -403,3 +403,18 @@ def test_kat_training_smoke():
     assert losses[-1] < 0.1 * losses[0]
     act = model.blocks[0].mlp.act2
     assert not torch.equal(act.a.detach().cpu(), kat.GroupRational(8, init="swish").a.detach())  # trained
+
+
+def test_grkb_dump_of_gpu_dx_is_byte_identical(golden, tmp_path):
+    """SURVEY 8f #4: the device dx, dumped as GRKB, equals the reference CLI's dump byte for byte."""
+    import os
+    from paper_2505_13813_b200 import grkb
+    g = G()
+    case = "f32_2x4x16_g2"
+    x, u, num, den = golden.inputs(case)
+    b = g.backward_blocked(g.ActivationTensor(x), g.ActivationTensor(u), g.GroupRationalParams(num, den))
+    out = tmp_path / "dx.grkb"
+    g.write_tensor_dump(str(out), b.d_x)
+    ref = os.path.join(os.path.dirname(__file__), "golden", "dx_f32_2x4x16.grkb")
+    assert out.read_bytes() == open(ref, "rb").read()
+    assert np.array_equal(grkb.load(str(out)), b.d_x.data)

@@ -134,3 +134,27 @@ def test_kat_model_shapes_and_init_cpu():
     std = mlp.fc2.weight.std().item()
     assert abs(std - (alpha * mlp.fc2.in_features) ** -0.5) < 0.02 * std
     assert abs(kat.rational_alpha(mlp.act1) - 1.0) < 0.02
+
+
+def test_grkb_reads_and_writes_reference_dumps(golden, tmp_path):
+    """GRKB interop (cli.py:104-129): dumps written by the reference load, and ours are byte-identical."""
+    import os
+    from paper_2505_13813_b200 import grkb
+    for fname, meta in golden.manifest["grkb"].items():
+        path = os.path.join(os.path.dirname(__file__), "golden", fname)
+        arr = grkb.load(path)
+        want = golden.get(meta["case"], meta["key"])
+        assert arr.dtype == want.dtype and np.array_equal(arr, want)
+        out = tmp_path / fname
+        grkb.save(str(out), want)
+        assert out.read_bytes() == open(path, "rb").read()
+        t = grkan.read_tensor_dump(path)
+        assert t.data.shape == want.shape
+        grkan.write_tensor_dump(str(out), t)
+        assert out.read_bytes() == open(path, "rb").read()
+    with pytest.raises(ValueError):
+        grkb.loads(b"XXXX" + bytes(29))
+    with pytest.raises(ValueError):
+        grkb.dumps(np.zeros((2, 2), np.float32))
+    with pytest.raises(ValueError):
+        grkb.dumps(np.zeros((1, 1, 2), np.int32))
