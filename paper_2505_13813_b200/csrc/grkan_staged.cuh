@@ -195,9 +195,10 @@ __device__ __forceinline__ void produce(const T* const (&src)[NT], T* const (&ri
   const int RS = geo.RS;
   const int nst = (nr + RS - 1) / RS;
   const uint32_t seg = static_cast<uint32_t>(geo.dg * sizeof(T));
+  int slot = 0;
+  uint32_t phase = 0;  // parity of the current pass over the ring
   for (int s = 0; s < nst; ++s) {
-    const int slot = s % stages;
-    if (s >= stages) mbar_wait(&empty[slot], ((s / stages) - 1) & 1);
+    if (s >= stages) mbar_wait(&empty[slot], phase ^ 1);  // released by the previous pass
     const int rows_here = min(RS, nr - s * RS);
     mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(rows_here) * seg * NT);
     for (int r = 0; r < rows_here; ++r) {
@@ -205,6 +206,10 @@ __device__ __forceinline__ void produce(const T* const (&src)[NT], T* const (&ri
 #pragma unroll
       for (int t = 0; t < NT; ++t)
         bulk_g2s(ring[t] + ((size_t)slot * RS + r) * geo.dg, src[t] + goff, seg, &full[slot], policy);
+    }
+    if (++slot == stages) {
+      slot = 0;
+      phase ^= 1;
     }
   }
 }
@@ -288,9 +293,10 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
     const int64_t gstep = (int64_t)geo.RS * geo.d;
     const int slot_elems = geo.RS * geo.dg;
     const int nst = (nr + geo.RS - 1) / geo.RS;
+    int slot = 0, since_flush = 0;
+    uint32_t phase = 0;
     for (int s = 0; s < nst; ++s) {
-      const int slot = s % stages;
-      mbar_wait(&full[slot], (s / stages) & 1);
+      mbar_wait(&full[slot], phase);
       const int rows_here = min(geo.RS, nr - s * geo.RS);
       const T* xs = sx + slot * slot_elems;
       const T* us = su + slot * slot_elems;
@@ -326,7 +332,14 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
       if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
       // Short per-lane fp32 chains keep the da/db rounding error near the fp32
       // term-evaluation floor (see lane_flush).
-      if ((s + 1) % geo.flush == 0 || s + 1 == nst) lane_flush<A, KC, PK>(acc, acc2, sacc);
+      if (++since_flush == geo.flush || s + 1 == nst) {
+        lane_flush<A, KC, PK>(acc, acc2, sacc);
+        since_flush = 0;
+      }
+      if (++slot == stages) {
+        slot = 0;
+        phase ^= 1;
+      }
     }
     __syncwarp();
     warp_store<A, KC>(sacc, part, g, tile, warp, geo);
@@ -390,9 +403,10 @@ __global__ void __launch_bounds__(kStagedThreads, kFwdCtasPerSm)
   }
   Checker<A> chk;
   const int nst = (nr + geo.RS - 1) / geo.RS;
+  int slot = 0;
+  uint32_t phase = 0;
   for (int s = 0; s < nst; ++s) {
-    const int slot = s % stages;
-    mbar_wait(&full[slot], (s / stages) & 1);
+    mbar_wait(&full[slot], phase);
     const int rows_here = min(geo.RS, nr - s * geo.RS);
     const T* xs = sx + (size_t)slot * geo.RS * geo.dg;
     T* ys = y + (row0 + (int64_t)s * geo.RS) * geo.d;
@@ -424,6 +438,10 @@ __global__ void __launch_bounds__(kStagedThreads, kFwdCtasPerSm)
         }
         __stcs(reinterpret_cast<uint4*>(ys + goff[j]), RW::pack(o));
       }
+    }
+    if (++slot == stages) {
+      slot = 0;
+      phase ^= 1;
     }
   }
   if (CHECK && chk.bad()) st->nonfinite_input = 1;
