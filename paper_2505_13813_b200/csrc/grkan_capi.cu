@@ -71,13 +71,14 @@ constexpr int kEltsPerThread = 64;  // target elements per thread per CTA
 // GRKAN_STAGED=0 in the environment selects the register-direct kernels even
 // where the TMA-staged ones apply (A/B measurements; results are identical
 // for y/dx and within fp32 reassociation for da/db).
-// The forward defaults to the register-direct kernel (measured faster: one
-// tensor in, four 16-byte loads in flight per thread already saturate HBM);
-// GRKAN_STAGED_FWD=1 selects the staged forward.
-bool staged_enabled(int nt) {
+// Forward: fp32 defaults to the register-direct kernel (measured 99.7% of
+// copy bandwidth at KAT-B vs 87% staged); 2-byte I/O carries twice the math
+// per byte and runs faster staged (84% vs 72%).  GRKAN_STAGED_FWD=0/1 forces;
+// GRKAN_STAGED=0 selects the register-direct backward.
+bool staged_enabled(int nt, size_t es) {
   const char* v = getenv(nt == 1 ? "GRKAN_STAGED_FWD" : "GRKAN_STAGED");
-  if (nt == 1) return v && v[0] == '1';
-  return !(v && v[0] == '0');
+  if (v && (v[0] == '0' || v[0] == '1')) return v[0] == '1';
+  return nt == 2 || es == 2;
 }
 
 constexpr int kStagesPerTensorPair = 4;  // backward ring depth (2 tensors)
@@ -91,7 +92,7 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
   const int dg = d / ng;
   p.geo.one = 1.0f;
   p.W = vec ? static_cast<int>(16 / es) : 1;
-  if (vec && m1 == 6 && n == 4 && dg / p.W <= grkan::kStageVecsHost && staged_enabled(nt)) {
+  if (vec && m1 == 6 && n == 4 && dg / p.W <= grkan::kStageVecsHost && staged_enabled(nt, es)) {
     // TMA-staged persistent kernels (grkan_staged.cuh)
     const int V = dg / p.W;
     const int RS = grkan::kStageVecsHost / V;
