@@ -1,0 +1,33 @@
+"""Small fwd/bwd runs for compute-sanitizer (memcheck / racecheck / synccheck / initcheck).
+
+    compute-sanitizer --tool racecheck python tools/sanitize_run.py
+Exercises every kernel family on small shapes: staged (fp32/bf16/fp64, fast/exact, checked),
+register-direct (unaligned), generic degrees, the reduce and the atomic comparator.
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2505_13813_b200 import ops  # noqa: E402
+
+dev = torch.device("cuda", 0)
+torch.manual_seed(0)
+for dtype in (torch.float32, torch.bfloat16, torch.float64):
+    cd = torch.float64 if dtype == torch.float64 else torch.float32
+    for shape, g, m1, n in [((3, 37, 384), 8, 6, 4), ((2, 5, 48), 4, 6, 4), ((2, 3, 12), 4, 6, 4),
+                            ((2, 9, 64), 2, 4, 2)]:
+        x = torch.randn(shape, device=dev).to(dtype)
+        u = torch.randn(shape, device=dev).to(dtype)
+        a = torch.randn(g, m1, device=dev, dtype=cd)
+        b = torch.randn(g, n, device=dev, dtype=cd)
+        for exact in (False, True):
+            ops.rational_forward(x, a, b, exact=exact, check_finite=True)
+            ops.rational_backward(x, u, a, b, exact=exact, check_finite=True, check_overflow=True)
+        ops.rational_backward_atomic(x, u, a, b)
+        xs = torch.randn(x.numel() + 1, device=dev).to(dtype)[1:].view(shape)  # unaligned
+        ops.rational_forward(xs, a, b)
+        ops.rational_backward(xs, u, a, b)
+torch.cuda.synchronize()
+print("sanitize run ok")
