@@ -11,7 +11,8 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libgrkan_b200.so")
+# GRKAN_LIB points at an alternative build (tuning variants from tools/build_variant.py)
+LIB_PATH = os.environ.get("GRKAN_LIB") or os.path.join(HERE, "_lib", "libgrkan_b200.so")
 
 # Status codes and flags (include/grkan_b200.h)
 OK = 0

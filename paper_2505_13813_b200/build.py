@@ -50,15 +50,19 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = True, ptxas_v: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = True, ptxas_v: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Compile the library.  ``out`` / ``defines`` make tuning variants (tools/build_variant.py)."""
+    target = out or OUT
+    if not force and out is None and up_to_date():
         return OUT
-    os.makedirs(OBJ_DIR, exist_ok=True)
+    obj_dir = OBJ_DIR if out is None else os.path.join(os.path.dirname(target), "obj")
+    os.makedirs(obj_dir, exist_ok=True)
     cc = nvcc()
-    extra = ["-Xptxas", "-v"] if ptxas_v else []
+    extra = (["-Xptxas", "-v"] if ptxas_v else []) + ["-D%s" % d for d in defines]
 
     def compile_one(src):
-        obj = os.path.join(OBJ_DIR, os.path.basename(src) + ".o")
+        obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
         cmd = [cc] + NVCC_FLAGS + extra + ["-c", "-o", obj, src]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -68,16 +72,16 @@ def build(force: bool = False, verbose: bool = True, ptxas_v: bool = False) -> s
     with ThreadPoolExecutor(max_workers=len(sources())) as pool:
         results = list(pool.map(compile_one, sources()))
     if ptxas_v:
-        with open(os.path.join(OBJ_DIR, "ptxas.log"), "w") as fh:
+        with open(os.path.join(obj_dir, "ptxas.log"), "w") as fh:
             for _, log in results:
                 fh.write(log)
-    tmp = OUT + ".tmp"
+    tmp = target + ".tmp"
     cmd = [cc] + ARCH + ["-shared", "-o", tmp] + [o for o, _ in results]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -81,7 +81,7 @@ bool staged_enabled(int nt, size_t es) {
   return nt == 2 || es == 2;
 }
 
-constexpr int kStagesPerTensorPair = 4;  // backward ring depth (2 tensors)
+constexpr int kStagesPerTensorPair = GRKAN_BWD_STAGES;  // backward ring depth (2 tensors)
 constexpr int kStagesSingle = 4;         // forward ring depth (1 tensor)
 constexpr size_t kSmemPerSm = 228 * 1024;
 

@@ -22,9 +22,9 @@
 
 namespace grkan {
 
-constexpr int kConsumerWarps = 8;
+constexpr int kConsumerWarps = GRKAN_CONSUMER_WARPS;
 constexpr int kStagedThreads = 32 * (kConsumerWarps + 1);  // + 1 producer warp
-constexpr int kStageVecs = 768;                            // per tensor per stage
+constexpr int kStageVecs = GRKAN_STAGE_VECS;               // per tensor per stage
 constexpr int kVPT = kStageVecs / (32 * kConsumerWarps);   // 3 vectors per consumer thread
 constexpr int kMaxStages = 4;
 // Backward CTAs per SM (register cap = 64K / (288 * MINB)).  Measured at
@@ -33,10 +33,10 @@ constexpr int kMaxStages = 4;
 // 311 us vs 279 us -- the bf16 backward is FMA-pipe bound, not warp bound).
 template <typename T>
 struct BwdCfg {
-  static constexpr int kMinBlocks = 2;
+  static constexpr int kMinBlocks = GRKAN_BWD_CTAS;
   static constexpr bool kSerialVectors = false;
 };
-constexpr int kFwdCtasPerSm = 3;
+constexpr int kFwdCtasPerSm = GRKAN_FWD_CTAS;
 
 // ---- PTX helpers: shared addresses, mbarriers, bulk copies ------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -45,11 +45,29 @@ struct Plan {
   size_t smem = 0;      // dynamic shared memory per CTA
 };
 
-constexpr int kStagedThreadsHost = 288;  // = grkan::kStagedThreads
-constexpr int kStageVecsHost = 768;      // = grkan::kStageVecs
-constexpr int kBwdCtasPerSmHost = 2;     // = grkan::BwdCfg<T>::kMinBlocks
-constexpr int kFwdCtasPerSmHost = 3;     // = grkan::kFwdCtasPerSm
-constexpr int kConsumerWarpsHost = 8;    // = grkan::kConsumerWarps
+// Staged-kernel geometry (compile-time; overridable with -D for tuning builds,
+// see tools/build_variant.py).  Shared by the host planner and the kernels.
+#ifndef GRKAN_CONSUMER_WARPS
+#define GRKAN_CONSUMER_WARPS 8     // consumer warps per staged CTA (+1 producer warp)
+#endif
+#ifndef GRKAN_STAGE_VECS
+#define GRKAN_STAGE_VECS 768       // 16-byte vectors per tensor per pipeline stage
+#endif
+#ifndef GRKAN_BWD_CTAS
+#define GRKAN_BWD_CTAS 2           // staged backward CTAs per SM (register cap)
+#endif
+#ifndef GRKAN_BWD_STAGES
+#define GRKAN_BWD_STAGES 4         // staged backward ring depth
+#endif
+#ifndef GRKAN_FWD_CTAS
+#define GRKAN_FWD_CTAS 3
+#endif
+constexpr int kConsumerWarpsHost = GRKAN_CONSUMER_WARPS;
+constexpr int kStagedThreadsHost = 32 * (GRKAN_CONSUMER_WARPS + 1);
+constexpr int kStageVecsHost = GRKAN_STAGE_VECS;
+constexpr int kBwdCtasPerSmHost = GRKAN_BWD_CTAS;
+constexpr int kFwdCtasPerSmHost = GRKAN_FWD_CTAS;
+static_assert(GRKAN_STAGE_VECS % (32 * GRKAN_CONSUMER_WARPS) == 0, "stage must split evenly over consumers");
 constexpr int kFlushStages = 4;          // per-lane fp32 register chains <= 4 stages x 6 terms
 
 struct LaunchArgs {
