@@ -120,7 +120,6 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
     p.geo.nsu = nsu;
     p.geo.pg = static_cast<int32_t>(pg);
     p.geo.flush = grkan::kFlushStages;
-    p.geo.nflush = 0;
     // partials per (group, coefficient) for K3 (backward: one per consumer warp)
     p.geo.n_tiles = nt == 2 ? pg * grkan::kConsumerWarpsHost : pg;
     p.ctas = rows > 0 ? pg * ng : 0;

@@ -3,6 +3,8 @@
 // {128-bit vector, scalar} x {checked, unchecked}.  Included once per dtype TU.
 #pragma once
 
+#include <atomic>
+
 #include "grkan_kernels.cuh"
 #include "grkan_staged.cuh"
 #include "grkan_types.h"
@@ -34,14 +36,22 @@ cudaError_t dispatch(const LaunchArgs& L, bool fixed, F&& f) {
 inline bool is_fixed(const LaunchArgs& L) { return L.m1 == kFixM1 && L.n == kFixN; }
 
 // Opt a kernel into its dynamic shared memory size (static + dynamic > 48 KB
-// needs the attribute).  One cache per kernel instantiation.
+// needs the attribute).  The attribute is per device: one cache per kernel
+// instantiation and device.
 template <auto Kernel>
 cudaError_t allow_smem(size_t bytes) {
-  static size_t granted = 0;  // benign race: concurrent writers store equivalent values
-  if (bytes <= granted) return cudaSuccess;
+  static std::atomic<size_t> granted_per_dev[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<size_t>& granted = granted_per_dev[dev & 63];
+  if (bytes <= granted.load(std::memory_order_relaxed)) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(bytes));
-  if (e == cudaSuccess) granted = bytes;
+  if (e == cudaSuccess) {
+    size_t cur = granted.load(std::memory_order_relaxed);
+    while (cur < bytes && !granted.compare_exchange_weak(cur, bytes, std::memory_order_relaxed)) {
+    }
+  }
   return e;
 }
 

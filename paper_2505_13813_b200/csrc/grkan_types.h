@@ -21,7 +21,6 @@ struct Geom {
   int64_t nsu;      // stage units per group = ceil(rows / RS)
   float one;        // 1.0f, opaque to ptxas (see grkan_math.cuh xmad2)
   int32_t flush;    // staged backward: stages between per-lane accumulator flushes
-  int32_t nflush;   // (unused, kept 0)
 };
 
 struct DevStatus {
