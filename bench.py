@@ -344,7 +344,8 @@ def run_b200(args, rank, world, local_rank):
     exact = args.mode == "exact"
     del y, dx, ws
     torch.cuda.empty_cache()
-    pipe = HostPipeline(dev, dim, groups, M1, NDEN, tdt, chunk_rows=max(seq, rows // 16))
+    pipe = HostPipeline(dev, dim, groups, M1, NDEN, tdt,
+                        chunk_rows=max(rows // 16, -(-HostPipeline.AUTO_CHUNK_BYTES // (dim * es))))
 
     def e2e_stream():
         da_, db_ = pipe.fwd_bwd(xh, dyh, a, b, yh, dxh, exact=exact)

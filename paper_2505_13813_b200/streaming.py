@@ -20,12 +20,15 @@ from . import ops
 
 
 class HostPipeline:
+    AUTO_CHUNK_BYTES = 32 << 20  # smaller chunks pay more per-chunk launch overhead than they overlap
+
     def __init__(self, device, d: int, n_groups: int, m1: int = 6, n: int = 4,
-                 dtype: torch.dtype = torch.float32, chunk_rows: int = 8192):
+                 dtype: torch.dtype = torch.float32, chunk_rows: int | None = None):
         self.device = torch.device(device)
         self.d, self.ng, self.m1, self.n = d, n_groups, m1, n
         self.dtype = dtype
-        self.chunk_rows = int(chunk_rows)
+        row_bytes = d * torch.empty((), dtype=dtype).element_size()
+        self.chunk_rows = int(chunk_rows) if chunk_rows else -(-self.AUTO_CHUNK_BYTES // row_bytes)
         shape = (self.chunk_rows, d)
         mk = lambda: torch.empty(shape, dtype=dtype, device=self.device)  # noqa: E731
         self.x = [mk(), mk()]
