@@ -276,6 +276,13 @@ struct RationalX2 {
     return s == 0.0f ? 0.0f : m;
   }
 
+  // -sign(s) * v without a multiply: flip v's sign bit where s > 0, zero where
+  // s == +-0 (np.sign(0) = 0).  One LOP3 and one select.
+  __device__ __forceinline__ static float neg_sign_times(float s, float v) {
+    const float m = __int_as_float(__float_as_int(v) ^ (~__float_as_int(s) & 0x80000000));
+    return s == 0.0f ? 0.0f : m;
+  }
+
   // Horner on a pair with scalar (broadcast) coefficients: the reference's
   // separately rounded acc = acc * x + c (ROUNDED) or FMA steps.
   template <bool ROUNDED, int N>
@@ -343,9 +350,9 @@ struct RationalX2 {
         acc[6 + j] = add2(acc[6 + j], v);
       }
     } else {
-      const float2 nsg = make_float2(neg_sign(s.x), neg_sign(s.y));  // -sign(A)
       const float2 t0 = mul2(u, iq);
-      const float2 z = mul2(nsg, pq);               // -sign(A) P/q
+      // z = -sign(A) P/q on the ALU pipe (sign flip + select), not the FMA pipe
+      const float2 z = make_float2(neg_sign_times(s.x, pq.x), neg_sign_times(s.y, pq.y));
       dx = mul2(t0, fma2(ds, z, dp));               // (u/q) (P' - sign(A) A' P/q)
       const float2 w = mul2(t0, z);                 // -(sign(A) u/q) P/q
       const float2 x2 = mul2(x, x);
