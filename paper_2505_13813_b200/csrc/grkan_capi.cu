@@ -82,7 +82,7 @@ bool staged_enabled(int nt, size_t es) {
 }
 
 constexpr int kStagesPerTensorPair = GRKAN_BWD_STAGES;  // backward ring depth (2 tensors)
-constexpr int kStagesSingle = 4;         // forward ring depth (1 tensor)
+constexpr int kStagesSingle = GRKAN_FWD_STAGES;  // forward ring depth (1 tensor)
 constexpr size_t kSmemPerSm = 228 * 1024;
 
 // nt = tensors streamed in (1 forward, 2 backward).
@@ -92,10 +92,11 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
   const int dg = d / ng;
   p.geo.one = 1.0f;
   p.W = vec ? static_cast<int>(16 / es) : 1;
-  if (vec && m1 == 6 && n == 4 && dg / p.W <= grkan::kStageVecsHost && staged_enabled(nt, es)) {
+  const int stage_vecs = nt == 2 ? grkan::kStageVecsHost : grkan::kFwdStageVecsHost;
+  if (vec && m1 == 6 && n == 4 && dg / p.W <= stage_vecs && staged_enabled(nt, es)) {
     // TMA-staged persistent kernels (grkan_staged.cuh)
     const int V = dg / p.W;
-    const int RS = grkan::kStageVecsHost / V;
+    const int RS = stage_vecs / V;
     const int64_t nsu = rows > 0 ? (rows + RS - 1) / RS : 0;
     p.staged = true;
     p.stages = nt == 2 ? kStagesPerTensorPair : kStagesSingle;
@@ -109,7 +110,7 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
     int64_t pg = slots / ng;
     if (pg > nsu) pg = nsu;
     if (pg < 1) pg = 1;
-    p.threads = grkan::kStagedThreadsHost;
+    p.threads = nt == 2 ? grkan::kStagedThreadsHost : grkan::kFwdThreadsHost;
     p.geo.rows = rows;
     p.geo.d = d;
     p.geo.ng = ng;

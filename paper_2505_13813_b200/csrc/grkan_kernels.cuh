@@ -88,7 +88,7 @@ struct VecIO<__nv_bfloat16, 8> {
     const uint32_t w[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i] = __uint_as_float(__byte_perm(w[i], 0u, 0x1044));  // w << 16 on the ALU pipe (PRMT)
       v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
     }
   }
@@ -120,6 +120,10 @@ template <typename A>
 __device__ __forceinline__ bool nonfinite(A v) {
   return !(fabs(v) <= (sizeof(A) == 4 ? A(FLT_MAX) : A(DBL_MAX)));
 }
+
+// FAST sign guard per I/O type (RationalX2::grad_n): on for fp32, off for bf16.
+template <typename T>
+constexpr bool kGuard = GRKAN_BF16_GUARD || !std::is_same<T, __nv_bfloat16>::value;
 
 __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -330,13 +334,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
       if (j == 0 || k + j * kBlock < nvec) {
         A o[W];
         if constexpr (E::kPacked) {
-#pragma unroll
-          for (int e = 0; e < W; e += 2) {
-            const float2 r2 = rp.grad(make_float2(vx[j][e], vx[j][e + 1]),
-                                      make_float2(vu[j][e], vu[j][e + 1]), acc2);
-            o[e] = r2.x;
-            o[e + 1] = r2.y;
-          }
+rp.template grad_n<W / 2, kGuard<T>>(vx[j], vu[j], o, acc2);
         } else {
 #pragma unroll
           for (int e = 0; e < W; ++e) o[e] = rs.grad(vx[j][e], vu[j][e], acc);

@@ -72,7 +72,7 @@ cudaError_t launch_fwd_t(const LaunchArgs& L) {
       constexpr auto kern = k_fwd_staged<T, decltype(e)::value, decltype(ck)::value>;
       cudaError_t ae = allow_smem<kern>(p.smem);
       if (ae != cudaSuccess) return ae;
-      kern<<<static_cast<unsigned>(p.ctas), kStagedThreads, p.smem, L.stream>>>(
+      kern<<<static_cast<unsigned>(p.ctas), kFwdThreads, p.smem, L.stream>>>(
           static_cast<const T*>(L.x), static_cast<T*>(L.out), static_cast<const A*>(L.a),
           static_cast<const A*>(L.b), p.geo, p.stages, L.st);
       return cudaGetLastError();

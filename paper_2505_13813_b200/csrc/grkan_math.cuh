@@ -24,6 +24,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include "grkan_types.h"
+
 namespace grkan {
 
 // ---------------------------------------------------------------------------
@@ -253,6 +255,7 @@ struct RationalX2 {
   static constexpr int KC = 10;
   float a[6], b[4], da[5], db[4];
   float one;  // opaque 1.0 (kernel parameter), see xmad2
+  int goff;   // sign-guard scale (FAST): see sign_unsafe
 
   __device__ __forceinline__ void load(const float* __restrict__ ga, const float* __restrict__ gb, int g,
                                        float one_param) {
@@ -267,6 +270,27 @@ struct RationalX2 {
 #pragma unroll
     for (int k = 2; k <= 4; ++k) db[k - 1] = __fmul_rn(b[k - 1], float(k));
     one = one_param;
+    // sign_unsafe threshold 2^e >= 2^-17 * (|b1| + |b2| + |b3| + |b4|), as an
+    // exponent offset in float bits; b == 0 (A == 0 exactly) disables it.
+    const float bsum = fabsf(b[0]) + fabsf(b[1]) + fabsf(b[2]) + fabsf(b[3]);
+    const int eb = static_cast<int>((__float_as_uint(bsum) >> 23) & 0xff) - 126;  // 2^eb > bsum
+    goff = bsum > 0.0f ? (eb - 17) * (1 << 23) : -0x7f000000;
+  }
+
+  // FAST mode evaluates h = b1 + b2 x + b3 x^2 + b4 x^3 with FMAs, but sign(A)
+  // = sign(h x) must be the reference's (sign is discontinuous at A's roots,
+  // and a flipped sign moves dx by 2 u A' P / Q^2).  Both Horner forms are
+  // within gamma_6 * H(|x|) ~ 3.6e-7 * H of the exact cubic, H(|x|) =
+  // sum |b_k| |x|^(k-1) <= bsum * max(1, |x|^3), so their signs can differ
+  // only when |h_fma| <= 7.2e-7 * bsum * max(1, |x|^3).  This flags
+  // |h| < 2^goff * max(1, |x|^3) (>= 10x margin) with integer compares on the
+  // float bits (ALU pipe); flagged pairs recompute h with the reference's
+  // separately rounded steps.  Conservative for tiny or huge |h| (wraps to
+  // "unsafe").
+  __device__ __forceinline__ bool sign_unsafe(float h, float x3) const {
+    const float m = fmaxf(fabsf(x3), 1.0f);
+    return static_cast<int>((__float_as_uint(h) & 0x7fffffffu) - static_cast<uint32_t>(goff)) <
+           static_cast<int>(__float_as_uint(m));
   }
 
   // -sign(s): -1 / +1 for s > 0 / s < 0, and +0 for s == +-0 (np.sign(0) = 0).
@@ -316,12 +340,19 @@ struct RationalX2 {
     return mul2(p, make_float2(rcp(qx), rcp(qy)));
   }
 
-  __device__ __forceinline__ float2 grad(float2 x, float2 u, float2 (&acc)[KC]) const {
+  // FAST: A(x) = h(x) x with h by FMA Horner; `bad` collects sign_unsafe.
+  __device__ __forceinline__ float2 series_fast(float2 x, float2 x3, bool& bad) const {
+    const float2 h = horner2<false, 4>(b, x);
+    bad |= sign_unsafe(h.x, x3.x) | sign_unsafe(h.y, x3.y);
+    return mul2(h, x);
+  }
+  // The reference's separately rounded A(x) (EXACT, and FAST's guarded pairs).
+  __device__ __forceinline__ float2 series_ref(float2 x) const { return mul2(horner2<true, 4>(b, x), x); }
+
+  // dx and the ten coefficient terms of one pair, given A(x) = s.
+  __device__ __forceinline__ float2 grad_given(float2 x, float2 u, float2 s, float2 x2, float2 x3,
+                                               float2 (&acc)[KC]) const {
     const float2 p = horner2<EXACT, 6>(a, x);
-    // A(x) is always evaluated with the reference's rounding sequence, in FAST
-    // mode too: sign(A) is discontinuous at A's roots, and an FMA-rounded A of
-    // the opposite sign flips dx there by 2 u A' P / Q^2 (seen at KAT-S).
-    const float2 s = mul2(horner2<true, 4>(b, x), x);
     const float2 iq = make_float2(rcp(__fadd_rn(1.0f, fabsf(s.x))), rcp(__fadd_rn(1.0f, fabsf(s.y))));
     const float2 dp = horner2<EXACT, 5>(da, x);
     const float2 ds = horner2<EXACT, 4>(db, x);
@@ -355,8 +386,6 @@ struct RationalX2 {
       const float2 z = make_float2(neg_sign_times(s.x, pq.x), neg_sign_times(s.y, pq.y));
       dx = mul2(t0, fma2(ds, z, dp));               // (u/q) (P' - sign(A) A' P/q)
       const float2 w = mul2(t0, z);                 // -(sign(A) u/q) P/q
-      const float2 x2 = mul2(x, x);
-      const float2 x3 = mul2(x2, x);
       const float2 x4 = mul2(x2, x2);
       const float2 x5 = mul2(x4, x);
       acc[0] = add2(acc[0], t0);
@@ -371,6 +400,58 @@ struct RationalX2 {
       acc[9] = fma2(w, x4, acc[9]);
     }
     return dx;
+  }
+
+  // dx for NP pairs (one 16-byte vector) and their terms folded into acc.
+  // FAST: the guard is evaluated for all NP pairs first and resolved by ONE
+  // (rarely taken) branch, so the straight-line math of the NP pairs stays in
+  // one basic block the scheduler can interleave.
+  // GRKAN_GUARD_NP pairs share one guard branch (tuning knob; the pairs'
+  // x^2 / x^3 stay live across it).  GUARD = false evaluates A(x) with the
+  // reference's rounding in FAST mode too: measured faster for bf16 I/O, whose
+  // backward is latency-bound and loses more to the guard's branches than it
+  // gains from 3 fewer FMUL2 per pair (fp32: 323 -> 307 us with the guard,
+  // bf16: 260 -> 273 us at KAT-B).
+  template <int NP, bool GUARD = true>
+  __device__ __forceinline__ void grad_n(const float (&vx)[2 * NP], const float (&vu)[2 * NP],
+                                         float (&o)[2 * NP], float2 (&acc)[KC]) const {
+    constexpr int G = GRKAN_GUARD_NP < NP ? GRKAN_GUARD_NP : NP;
+    static_assert(NP % G == 0, "guard group must divide the pair count");
+#pragma unroll
+    for (int i0 = 0; i0 < NP; i0 += G) {
+      float2 x[G], s[G], x2[G], x3[G];
+#pragma unroll
+      for (int i = 0; i < G; ++i) x[i] = make_float2(vx[2 * (i0 + i)], vx[2 * (i0 + i) + 1]);
+      if (EXACT || !GUARD || !GRKAN_SIGN_GUARD) {
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+          s[i] = series_ref(x[i]);
+          if (!EXACT) {
+            x2[i] = mul2(x[i], x[i]);
+            x3[i] = mul2(x2[i], x[i]);
+          }
+        }
+      } else {
+        bool bad = false;
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+          x2[i] = mul2(x[i], x[i]);
+          x3[i] = mul2(x2[i], x[i]);
+          s[i] = series_fast(x[i], x3[i], bad);
+        }
+        if (bad) {
+#pragma unroll
+          for (int i = 0; i < G; ++i) s[i] = series_ref(x[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        const int e = 2 * (i0 + i);
+        const float2 r = grad_given(x[i], make_float2(vu[e], vu[e + 1]), s[i], x2[i], x3[i], acc);
+        o[e] = r.x;
+        o[e + 1] = r.y;
+      }
+    }
   }
 };
 

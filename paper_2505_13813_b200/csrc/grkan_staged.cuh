@@ -26,7 +26,7 @@ constexpr int kConsumerWarps = GRKAN_CONSUMER_WARPS;
 constexpr int kStagedThreads = 32 * (kConsumerWarps + 1);  // + 1 producer warp
 constexpr int kStageVecs = GRKAN_STAGE_VECS;               // per tensor per stage
 constexpr int kVPT = kStageVecs / (32 * kConsumerWarps);   // 3 vectors per consumer thread
-constexpr int kMaxStages = 4;
+constexpr int kMaxStages = 8;
 // Backward CTAs per SM (register cap = 64K / (288 * MINB)).  Measured at
 // KAT-B: 2 CTAs, 4-stage ring, unrolled vectors is best for both fp32 and
 // bf16 (bf16 with 3 CTAs at 72 registers, 2-stage ring, serial vectors:
@@ -37,6 +37,10 @@ struct BwdCfg {
   static constexpr bool kSerialVectors = false;
 };
 constexpr int kFwdCtasPerSm = GRKAN_FWD_CTAS;
+// Forward geometry (separately tunable: one tensor in, little math per byte).
+constexpr int kFwdConsumerWarps = GRKAN_FWD_CONSUMER_WARPS;
+constexpr int kFwdThreads = 32 * (kFwdConsumerWarps + 1);
+constexpr int kFwdVPT = GRKAN_FWD_STAGE_VECS / (32 * kFwdConsumerWarps);
 
 // ---- PTX helpers: shared addresses, mbarriers, bulk copies ------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -103,7 +107,7 @@ struct Raw16<__nv_bfloat16> {
     const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i] = __uint_as_float(__byte_perm(w[i], 0u, 0x1044));  // w << 16 on the ALU pipe (PRMT)
       v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
     }
   }
@@ -307,12 +311,7 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
           RW::unpack(*reinterpret_cast<const uint4*>(xs + so[j]), vx);
           RW::unpack(*reinterpret_cast<const uint4*>(us + so[j]), vu);
           if constexpr (PK) {
-#pragma unroll
-            for (int e = 0; e < W; e += 2) {
-              const float2 r2 = rp.grad(make_float2(vx[e], vx[e + 1]), make_float2(vu[e], vu[e + 1]), acc2);
-              o[e] = r2.x;
-              o[e + 1] = r2.y;
-            }
+rp.template grad_n<W / 2, kGuard<T>>(vx, vu, o, acc2);
           } else {
 #pragma unroll
             for (int e = 0; e < W; ++e) o[e] = rs.grad(vx[e], vu[e], acc);
@@ -351,7 +350,7 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
 // K1 staged: forward, degrees (5, 4).
 // ---------------------------------------------------------------------------
 template <typename T, bool EXACT, bool CHECK>
-__global__ void __launch_bounds__(kStagedThreads, kFwdCtasPerSm)
+__global__ void __launch_bounds__(kFwdThreads, kFwdCtasPerSm)
     k_fwd_staged(const T* __restrict__ x, T* __restrict__ y, const typename VecIO<T, 1>::A* __restrict__ ca,
                  const typename VecIO<T, 1>::A* __restrict__ cb, Geom geo, int stages,
                  DevStatus* __restrict__ st) {
@@ -371,12 +370,12 @@ __global__ void __launch_bounds__(kStagedThreads, kFwdCtasPerSm)
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&empty[s], kFwdConsumerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (warp == kConsumerWarps) {
+  if (warp == kFwdConsumerWarps) {
     if (lane == 0) {
       const T* const src[1] = {x};
       T* const ring[1] = {sx};
@@ -390,12 +389,12 @@ __global__ void __launch_bounds__(kStagedThreads, kFwdCtasPerSm)
     rp.load(reinterpret_cast<const float*>(ca), reinterpret_cast<const float*>(cb), g, geo.one);
   else
     rs.load(ca, cb, g, 6, 4);
-  int sr[kVPT], soff[kVPT];
-  int64_t goff[kVPT];
+  int sr[kFwdVPT], soff[kFwdVPT];
+  int64_t goff[kFwdVPT];
   const int svecs = geo.RS * geo.V;
 #pragma unroll
-  for (int j = 0; j < kVPT; ++j) {
-    const int k = threadIdx.x + j * 32 * kConsumerWarps;
+  for (int j = 0; j < kFwdVPT; ++j) {
+    const int k = threadIdx.x + j * 32 * kFwdConsumerWarps;
     const int r = k / geo.V, c = k - (k / geo.V) * geo.V;
     sr[j] = k < svecs ? r : 0x7fffffff;
     soff[j] = r * geo.dg + c * W;
@@ -410,14 +409,14 @@ __global__ void __launch_bounds__(kStagedThreads, kFwdCtasPerSm)
     const int rows_here = min(geo.RS, nr - s * geo.RS);
     const T* xs = sx + (size_t)slot * geo.RS * geo.dg;
     T* ys = y + (row0 + (int64_t)s * geo.RS) * geo.d;
-    uint4 rx[kVPT];
+    uint4 rx[kFwdVPT];
 #pragma unroll
-    for (int j = 0; j < kVPT; ++j)
+    for (int j = 0; j < kFwdVPT; ++j)
       if (sr[j] < rows_here) rx[j] = *reinterpret_cast<const uint4*>(xs + soff[j]);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
 #pragma unroll
-    for (int j = 0; j < kVPT; ++j) {
+    for (int j = 0; j < kFwdVPT; ++j) {
       if (sr[j] < rows_here) {
         A v[W], o[W];
         RW::unpack(rx[j], v);

@@ -58,15 +58,36 @@ struct Plan {
 #ifndef GRKAN_BWD_STAGES
 #define GRKAN_BWD_STAGES 4         // staged backward ring depth
 #endif
+#ifndef GRKAN_SIGN_GUARD
+#define GRKAN_SIGN_GUARD 1        // FAST: FMA-evaluated A(x) with the sign guard (0: reference-rounded A)
+#endif
+#ifndef GRKAN_BF16_GUARD
+#define GRKAN_BF16_GUARD 0        // sign guard for bf16 I/O too
+#endif
+#ifndef GRKAN_GUARD_NP
+#define GRKAN_GUARD_NP 2          // FAST sign guard: element pairs per guard branch
+#endif
+#ifndef GRKAN_FWD_CONSUMER_WARPS
+#define GRKAN_FWD_CONSUMER_WARPS 2 // consumer warps per staged forward CTA
+#endif
+#ifndef GRKAN_FWD_STAGE_VECS
+#define GRKAN_FWD_STAGE_VECS 192   // 16-byte vectors per forward pipeline stage
+#endif
+#ifndef GRKAN_FWD_STAGES
+#define GRKAN_FWD_STAGES 4         // staged forward ring depth
+#endif
 #ifndef GRKAN_FWD_CTAS
-#define GRKAN_FWD_CTAS 3
+#define GRKAN_FWD_CTAS 8
 #endif
 constexpr int kConsumerWarpsHost = GRKAN_CONSUMER_WARPS;
 constexpr int kStagedThreadsHost = 32 * (GRKAN_CONSUMER_WARPS + 1);
 constexpr int kStageVecsHost = GRKAN_STAGE_VECS;
 constexpr int kBwdCtasPerSmHost = GRKAN_BWD_CTAS;
 constexpr int kFwdCtasPerSmHost = GRKAN_FWD_CTAS;
+constexpr int kFwdThreadsHost = 32 * (GRKAN_FWD_CONSUMER_WARPS + 1);
+constexpr int kFwdStageVecsHost = GRKAN_FWD_STAGE_VECS;
 static_assert(GRKAN_STAGE_VECS % (32 * GRKAN_CONSUMER_WARPS) == 0, "stage must split evenly over consumers");
+static_assert(GRKAN_FWD_STAGE_VECS % (32 * GRKAN_FWD_CONSUMER_WARPS) == 0, "stage must split evenly over consumers");
 constexpr int kFlushStages = 4;          // per-lane fp32 register chains <= 4 stages x 6 terms
 
 struct LaunchArgs {
