@@ -65,6 +65,7 @@ typedef enum grkan_dtype { GRKAN_F32 = 0, GRKAN_F64 = 1, GRKAN_BF16 = 2 } grkan_
 #define GRKAN_FLAG_FAST 0u         /* FMA + approximate reciprocal; max-scaled <= 1e-5 */
 #define GRKAN_FLAG_EXACT 1u        /* reference op order, IEEE-rounded ops: bitwise y/dx */
 #define GRKAN_FLAG_CHECK_FINITE 2u /* checked mode: flag NaN/Inf inputs (validate=True) */
+#define GRKAN_FLAG_DETERMINISTIC 4u /* grkan_bwd: partials per global row block (see below) */
 
 /* Highest supported degrees (m1 = m + 1 numerator coefficients, n denominator). */
 #define GRKAN_MAX_M1 12
@@ -106,6 +107,34 @@ GRKAN_API int grkan_bwd_atomic(const void* x, const void* dy, const void* a, con
                      void* da, void* db, int64_t rows, int32_t d, int32_t n_groups, int32_t m1,
                      int32_t n, int32_t dtype, uint32_t flags, grkan_device_status* status,
                      void* stream);
+
+/* Deterministic (row-sharding-invariant) coefficient gradients.
+ *
+ * The multi-GPU analogue of backward_blocked's worker-count invariance
+ * (backward.py:275-372 with combine_partials' ordered fold, 142-179;
+ * pkg/tests/test_acceptance.py:232-252): rows are cut into global blocks of
+ * grkan_det_block_rows() rows; each block's m1 + n partial sums are computed in
+ * a fixed order that depends only on the block's data, stored slot-major
+ * part[(block * n_groups + g) * (m1 + n) + k], and folded by
+ * grkan_reduce_partials in global block order.  A run sharded over any number
+ * of ranks at block-aligned row boundaries, with the per-rank partial arrays
+ * concatenated in rank order (an all-gather), gives bitwise the da / db of
+ * grkan_bwd(..., GRKAN_FLAG_DETERMINISTIC) on the whole tensor (for one
+ * kernel family: 16-byte-aligned tensors on every rank).  dx is unaffected. */
+GRKAN_API int64_t grkan_det_block_rows(int32_t d, int32_t n_groups, int32_t dtype);
+GRKAN_API size_t grkan_det_partials_bytes(int64_t rows, int32_t d, int32_t n_groups, int32_t m1, int32_t n,
+                                          int32_t dtype);
+/* dx plus this shard's per-block partials (no reduction).  `status` may be
+ * NULL unless GRKAN_FLAG_CHECK_FINITE is set. */
+GRKAN_API int grkan_bwd_partials(const void* x, const void* dy, const void* a, const void* b, void* dx,
+                                 void* part, size_t part_bytes, int64_t rows, int32_t d, int32_t n_groups,
+                                 int32_t m1, int32_t n, int32_t dtype, uint32_t flags,
+                                 grkan_device_status* status, void* stream);
+/* Fixed-order fp64 fold of n_blocks slot-major partials into da / db; the
+ * overflow flag lands in `status` (required). */
+GRKAN_API int grkan_reduce_partials(const void* part, int64_t n_blocks, int32_t n_groups, int32_t m1,
+                                    int32_t n, void* da, void* db, int32_t dtype, grkan_device_status* status,
+                                    void* stream);
 
 /* Synchronise `stream` and copy the device status to the host; maps it to a
  * status code (NONFINITE_INPUT first, then ACCUM_OVERFLOW, else OK). */

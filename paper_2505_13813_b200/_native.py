@@ -31,6 +31,7 @@ DT_BF16 = 2
 FLAG_FAST = 0
 FLAG_EXACT = 1
 FLAG_CHECK_FINITE = 2
+FLAG_DETERMINISTIC = 4
 
 MAX_M1 = 12
 MAX_N = 12
@@ -38,7 +39,8 @@ MAX_N = 12
 EXPORTS = (
     "grkan_version", "grkan_status_string", "grkan_last_error", "grkan_fwd",
     "grkan_bwd_workspace_bytes", "grkan_bwd", "grkan_bwd_atomic", "grkan_read_status",
-    "grkan_plan",
+    "grkan_plan", "grkan_det_block_rows", "grkan_det_partials_bytes", "grkan_bwd_partials",
+    "grkan_reduce_partials",
 )
 
 
@@ -75,6 +77,14 @@ def _declare(L):
     L.grkan_read_status.restype = ctypes.c_int
     L.grkan_plan.argtypes = [i64, i32, i32, i32, i32, i32, ctypes.POINTER(ctypes.c_int64)]
     L.grkan_plan.restype = ctypes.c_int
+    L.grkan_det_block_rows.argtypes = [i32, i32, i32]
+    L.grkan_det_block_rows.restype = i64
+    L.grkan_det_partials_bytes.argtypes = [i64, i32, i32, i32, i32, i32]
+    L.grkan_det_partials_bytes.restype = sz
+    L.grkan_bwd_partials.argtypes = [p, p, p, p, p, p, sz, i64, i32, i32, i32, i32, i32, u32, p, p]
+    L.grkan_bwd_partials.restype = ctypes.c_int
+    L.grkan_reduce_partials.argtypes = [p, i64, i32, i32, i32, p, p, i32, p, p]
+    L.grkan_reduce_partials.restype = ctypes.c_int
 
 
 def lib():

@@ -85,11 +85,25 @@ constexpr int kStagesPerTensorPair = GRKAN_BWD_STAGES;  // backward ring depth (
 constexpr int kStagesSingle = GRKAN_FWD_STAGES;  // forward ring depth (1 tensor)
 constexpr size_t kSmemPerSm = 228 * 1024;
 
-// nt = tensors streamed in (1 forward, 2 backward).
+// Deterministic mode's global row block RB: a whole number of staged
+// pipeline stages (RS = stage vectors / V rows) of >= 128 rows.  Depends only
+// on (d, n_groups, element size), so every rank of a sharded run agrees on it.
+int64_t det_rows(int32_t d, int32_t ng, size_t es) {
+  const int dg = d / ng;
+  const int W = static_cast<int>(16 / es);
+  const int V = dg % W == 0 ? dg / W : 0;
+  const int RS = (V >= 1 && V <= grkan::kStageVecsHost) ? grkan::kStageVecsHost / V : 1;
+  return static_cast<int64_t>(RS) * ((128 + RS - 1) / RS);
+}
+
+// nt = tensors streamed in (1 forward, 2 backward).  det: one partial per
+// global RB-row block (slot-major), independent of the launch geometry.
 Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_t es, bool vec, int nt,
-               int sms) {
+               int sms, bool det = false) {
   Plan p;
   const int dg = d / ng;
+  const int64_t RB = det ? det_rows(d, ng, es) : 0;
+  p.geo.det = det ? 1 : 0;
   p.geo.one = 1.0f;
   p.W = vec ? static_cast<int>(16 / es) : 1;
   const int stage_vecs = nt == 2 ? grkan::kStageVecsHost : grkan::kFwdStageVecsHost;
@@ -97,7 +111,8 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
     // TMA-staged persistent kernels (grkan_staged.cuh)
     const int V = dg / p.W;
     const int RS = stage_vecs / V;
-    const int64_t nsu = rows > 0 ? (rows + RS - 1) / RS : 0;
+    const int64_t RU = det ? RB : RS;  // rows per partition unit
+    const int64_t nsu = rows > 0 ? (rows + RU - 1) / RU : 0;
     p.staged = true;
     p.stages = nt == 2 ? kStagesPerTensorPair : kStagesSingle;
     p.smem = static_cast<size_t>(p.stages) * nt * RS * dg * es;
@@ -121,8 +136,11 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
     p.geo.nsu = nsu;
     p.geo.pg = static_cast<int32_t>(pg);
     p.geo.flush = grkan::kFlushStages;
-    // partials per (group, coefficient) for K3 (backward: one per consumer warp)
-    p.geo.n_tiles = nt == 2 ? pg * grkan::kConsumerWarpsHost : pg;
+    p.geo.RU = static_cast<int32_t>(RU);
+    p.geo.spb = static_cast<int32_t>(RU / RS);
+    // partials per (group, coefficient) for K3 (backward: one per consumer
+    // warp; deterministic: one per RB-row block)
+    p.geo.n_tiles = det ? nsu : (nt == 2 ? pg * grkan::kConsumerWarpsHost : pg);
     p.ctas = rows > 0 ? pg * ng : 0;
     return p;
   }
@@ -141,9 +159,13 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
   if (rows > 0 && R > rows) R = rows;
   int64_t n_tiles = rows > 0 ? (rows + R - 1) / R : 0;
   // small tensors: shrink tiles until there are a few CTAs per SM
-  while (R > 1 && n_tiles * ng < 4LL * sms) {
+  while (!det && R > 1 && n_tiles * ng < 4LL * sms) {
     R = (R + 1) / 2;
     n_tiles = (rows + R - 1) / R;
+  }
+  if (det) {  // fixed global row blocks, whatever the shard size
+    R = RB;
+    n_tiles = rows > 0 ? (rows + R - 1) / R : 0;
   }
   p.threads = grkan::kBlock;
   p.geo.rows = rows;
@@ -182,12 +204,18 @@ int check_layout(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, int
   if (m1 > GRKAN_MAX_M1 || n > GRKAN_MAX_N)
     return fail(GRKAN_ERR_UNSUPPORTED, "degrees (m1=%d, n=%d) exceed this build (max %d, %d)", m1, n,
                 GRKAN_MAX_M1, GRKAN_MAX_N);
-  if (flags & ~(GRKAN_FLAG_EXACT | GRKAN_FLAG_CHECK_FINITE))
+  if (flags & ~(GRKAN_FLAG_EXACT | GRKAN_FLAG_CHECK_FINITE | GRKAN_FLAG_DETERMINISTIC))
     return fail(GRKAN_ERR_INVALID, "unknown flag bits 0x%x", flags);
   return GRKAN_OK;
 }
 
 using grkan::LaunchArgs;
+
+cudaError_t launch_reduce(int dtype, const void* part, int64_t n_tiles, int64_t slot_stride, int ng, int m1,
+                          int n, void* da, void* db, DevStatus* st, cudaStream_t s) {
+  if (dtype == GRKAN_F64) return grkan::launch_reduce_f64(part, n_tiles, slot_stride, ng, m1, n, da, db, st, s);
+  return grkan::launch_reduce_f32(part, n_tiles, slot_stride, ng, m1, n, da, db, st, s);
+}
 
 cudaError_t launch(const char* which, int dtype, const LaunchArgs& L) {
   const bool f = which[0] == 'f', b = which[0] == 'b';
@@ -260,7 +288,10 @@ size_t grkan_bwd_workspace_bytes(int64_t rows, int32_t d, int32_t n_groups, int3
   const size_t a =
       can_vec ? ws_bytes_for(make_plan(rows, d, n_groups, m1, n, es, true, 2, kAnySms), m1, n, dtype) : 0;
   const size_t b = ws_bytes_for(make_plan(rows, d, n_groups, m1, n, es, false, 2, kAnySms), m1, n, dtype);
-  return a > b ? a : b;
+  // GRKAN_FLAG_DETERMINISTIC: one partial per global row block
+  const size_t c = ws_bytes_for(make_plan(rows, d, n_groups, m1, n, es, false, 2, kAnySms, true), m1, n, dtype);
+  const size_t ab = a > b ? a : b;
+  return ab > c ? ab : c;
 }
 
 int grkan_fwd(const void* x, void* y, const void* a, const void* b, int64_t rows, int32_t d,
@@ -319,7 +350,8 @@ int grkan_bwd(const void* x, const void* dy, const void* a, const void* b, void*
   if (!x || !dy || !dx || !a || (n > 0 && !b)) return fail(GRKAN_ERR_INVALID, "null tensor pointer");
   const size_t es = elem_size(dtype);
   const bool vec = vec_ok(d, n_groups, es, {x, dy, dx});
-  const Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count());
+  const bool det = (flags & GRKAN_FLAG_DETERMINISTIC) != 0;
+  const Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count(), det);
   if (!plan_fits(p)) return fail(GRKAN_ERR_GRID, "grid geometry invalid: %lld CTAs", (long long)p.ctas);
   const size_t need = ws_bytes_for(p, m1, n, dtype);
   if (ws_bytes < need)
@@ -343,6 +375,83 @@ int grkan_bwd(const void* x, const void* dy, const void* a, const void* b, void*
   L.stream = s;
   e = launch("bwd", dtype, L);
   if (e != cudaSuccess) return cuda_fail(e, "k_bwd launch");
+  return GRKAN_OK;
+}
+
+int64_t grkan_det_block_rows(int32_t d, int32_t n_groups, int32_t dtype) {
+  if (elem_size(dtype) == 0 || d < 1 || n_groups < 1 || d % n_groups) return 0;
+  return det_rows(d, n_groups, elem_size(dtype));
+}
+
+size_t grkan_det_partials_bytes(int64_t rows, int32_t d, int32_t n_groups, int32_t m1, int32_t n,
+                                int32_t dtype) {
+  if (check_layout(rows, d, n_groups, m1, n, dtype, 0) != GRKAN_OK) return 0;
+  const int64_t rb = det_rows(d, n_groups, elem_size(dtype));
+  const int64_t blocks = (rows + rb - 1) / rb;
+  return static_cast<size_t>(blocks) * n_groups * (m1 + n) * acc_size(dtype);
+}
+
+int grkan_bwd_partials(const void* x, const void* dy, const void* a, const void* b, void* dx, void* part,
+                       size_t part_bytes, int64_t rows, int32_t d, int32_t n_groups, int32_t m1, int32_t n,
+                       int32_t dtype, uint32_t flags, grkan_device_status* status, void* stream) {
+  int rc = check_layout(rows, d, n_groups, m1, n, dtype, flags);
+  if (rc) return rc;
+  const bool check = (flags & GRKAN_FLAG_CHECK_FINITE) != 0;
+  if (check && !status) return fail(GRKAN_ERR_INVALID, "CHECK_FINITE needs a status block");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (check) {
+    cudaError_t e = cudaMemsetAsync(status, 0, sizeof(grkan_device_status), s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(status)");
+  }
+  if (rows == 0) return GRKAN_OK;
+  const size_t need = grkan_det_partials_bytes(rows, d, n_groups, m1, n, dtype);
+  if (!part || part_bytes < need)
+    return fail(GRKAN_ERR_INVALID, "partials buffer too small: %zu < %zu bytes", part ? part_bytes : 0, need);
+  if (!x || !dy || !dx || !a || (n > 0 && !b)) return fail(GRKAN_ERR_INVALID, "null tensor pointer");
+  const size_t es = elem_size(dtype);
+  const bool vec = vec_ok(d, n_groups, es, {x, dy, dx});
+  const Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count(), true);
+  if (!plan_fits(p)) return fail(GRKAN_ERR_GRID, "grid geometry invalid: %lld CTAs", (long long)p.ctas);
+  LaunchArgs L{};
+  L.plan = &p;
+  L.x = x;
+  L.dy = dy;
+  L.out = dx;
+  L.a = a;
+  L.b = b;
+  L.part = part;
+  L.st = reinterpret_cast<DevStatus*>(status);
+  L.m1 = m1;
+  L.n = n;
+  L.exact = (flags & GRKAN_FLAG_EXACT) != 0;
+  L.vec = vec;
+  L.check = check;
+  L.partials_only = true;
+  L.stream = s;
+  cudaError_t e = launch("bwd", dtype, L);
+  if (e != cudaSuccess) return cuda_fail(e, "k_bwd (partials) launch");
+  return GRKAN_OK;
+}
+
+int grkan_reduce_partials(const void* part, int64_t n_blocks, int32_t n_groups, int32_t m1, int32_t n,
+                          void* da, void* db, int32_t dtype, grkan_device_status* status, void* stream) {
+  int rc = check_layout(0, n_groups, n_groups, m1, n, dtype, 0);
+  if (rc) return rc;
+  if (n_blocks < 0) return fail(GRKAN_ERR_GRID, "grid geometry invalid: negative block count");
+  if (!da || (n > 0 && !db) || !status) return fail(GRKAN_ERR_INVALID, "null gradient / status pointer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(status, 0, sizeof(grkan_device_status), s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(status)");
+  if (n_blocks == 0) {
+    const size_t as = acc_size(dtype);
+    e = cudaMemsetAsync(da, 0, static_cast<size_t>(n_groups) * m1 * as, s);
+    if (e == cudaSuccess && n > 0) e = cudaMemsetAsync(db, 0, static_cast<size_t>(n_groups) * n * as, s);
+    return e == cudaSuccess ? GRKAN_OK : cuda_fail(e, "cudaMemsetAsync(da/db)");
+  }
+  if (!part) return fail(GRKAN_ERR_INVALID, "null partials pointer");
+  e = launch_reduce(dtype, part, n_blocks, static_cast<int64_t>(n_groups) * (m1 + n), n_groups, m1, n, da, db,
+                    reinterpret_cast<DevStatus*>(status), s);
+  if (e != cudaSuccess) return cuda_fail(e, "k_bwd_reduce launch");
   return GRKAN_OK;
 }
 

@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
 // ---------------------------------------------------------------------------
 template <typename A, int MM1, int KC>
 __device__ __forceinline__ void cta_reduce_store(A (&acc)[KC], int m1, int n, A* __restrict__ part,
-                                                 int g, int64_t tile, int64_t n_tiles) {
+                                                 int g, int64_t tile, int64_t n_tiles, int ng, bool det) {
   __shared__ A red[kBlock / 32][KC];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -265,7 +265,8 @@ __device__ __forceinline__ void cta_reduce_store(A (&acc)[KC], int m1, int n, A*
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       const bool live = k < MM1 ? (k < m1) : (k - MM1 < n);
       const int slot = k < MM1 ? k : m1 + (k - MM1);
-      if (lane == 0 && live) part[((int64_t)g * kc + slot) * n_tiles + tile] = v;
+      if (lane == 0 && live)
+        part[det ? (tile * ng + g) * kc + slot : ((int64_t)g * kc + slot) * n_tiles + tile] = v;
     }
   }
 }
@@ -354,9 +355,9 @@ rp.template grad_n<W / 2, kGuard<T>>(vx[j], vu[j], o, acc2);
   if constexpr (E::kPacked) {
 #pragma unroll
     for (int k = 0; k < KC; ++k) acc[k] = acc2[k].x + acc2[k].y;
-    cta_reduce_store<A, MM1, KC>(acc, MM1, MN, part, g, tile, geo.n_tiles);
+    cta_reduce_store<A, MM1, KC>(acc, MM1, MN, part, g, tile, geo.n_tiles, geo.ng, geo.det != 0);
   } else {
-    cta_reduce_store<A, MM1, KC>(acc, FIXED ? MM1 : m1, FIXED ? MN : n, part, g, tile, geo.n_tiles);
+    cta_reduce_store<A, MM1, KC>(acc, FIXED ? MM1 : m1, FIXED ? MN : n, part, g, tile, geo.n_tiles, geo.ng, geo.det != 0);
   }
 }
 
@@ -368,13 +369,15 @@ rp.template grad_n<W / 2, kGuard<T>>(vx[j], vu[j], o, acc2);
 template <typename A>
 __global__ void __launch_bounds__(256)
     k_bwd_reduce(const A* __restrict__ part, int64_t n_tiles, int m1, int n, A* __restrict__ da,
-                 A* __restrict__ db, DevStatus* __restrict__ st) {
+                 A* __restrict__ db, DevStatus* __restrict__ st, int64_t slot_stride) {
   pdl_wait();  // K2's partials are complete and visible after this
   const int kc = m1 + n;
   const int col = blockIdx.x;  // g * kc + k
-  const A* src = part + (int64_t)col * n_tiles;
+  // column-major part[col * n_tiles + t] (slot_stride 1), or the deterministic
+  // mode's slot-major part[t * ng * kc + col] (slot_stride ng * kc)
+  const A* src = part + (slot_stride == 1 ? (int64_t)col * n_tiles : (int64_t)col);
   double s = 0.0;
-  for (int64_t t = threadIdx.x; t < n_tiles; t += blockDim.x) s += static_cast<double>(src[t]);
+  for (int64_t t = threadIdx.x; t < n_tiles; t += blockDim.x) s += static_cast<double>(src[t * slot_stride]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   __shared__ double red[8];

@@ -88,6 +88,10 @@ cudaError_t launch_fwd_t(const LaunchArgs& L) {
   });
 }
 
+template <typename A>
+cudaError_t launch_reduce_t(const A* part, int64_t n_tiles, int64_t slot_stride, int ng, int m1, int n, A* da,
+                            A* db, DevStatus* st, cudaStream_t stream);
+
 template <typename T>
 cudaError_t launch_bwd_t(const LaunchArgs& L) {
   using A = typename VecIO<T, 1>::A;
@@ -95,14 +99,17 @@ cudaError_t launch_bwd_t(const LaunchArgs& L) {
   cudaError_t e0;
   if (p.staged) {
     e0 = dispatch_staged<T>(L, [&](auto e, auto ck) -> cudaError_t {
-      constexpr auto kern = k_bwd_staged<T, decltype(e)::value, decltype(ck)::value>;
-      cudaError_t ae = allow_smem<kern>(p.smem);
-      if (ae != cudaSuccess) return ae;
-      kern<<<static_cast<unsigned>(p.ctas), kStagedThreads, p.smem, L.stream>>>(
-          static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out),
-          static_cast<const A*>(L.a), static_cast<const A*>(L.b), static_cast<A*>(L.part), p.geo,
-          p.stages, L.st);
-      return cudaGetLastError();
+      auto go = [&](auto det) -> cudaError_t {
+        constexpr auto kern = k_bwd_staged<T, decltype(e)::value, decltype(ck)::value, decltype(det)::value>;
+        cudaError_t ae = allow_smem<kern>(p.smem);
+        if (ae != cudaSuccess) return ae;
+        kern<<<static_cast<unsigned>(p.ctas), kStagedThreads, p.smem, L.stream>>>(
+            static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out),
+            static_cast<const A*>(L.a), static_cast<const A*>(L.b), static_cast<A*>(L.part), p.geo,
+            p.stages, L.st);
+        return cudaGetLastError();
+      };
+      return p.geo.det ? go(std::true_type{}) : go(std::false_type{});
     });
   } else e0 = dispatch<T>(L, is_fixed(L), [&](auto e, auto fx, auto wc, auto ck) -> cudaError_t {
     constexpr bool FX = decltype(fx)::value;
@@ -114,21 +121,29 @@ cudaError_t launch_bwd_t(const LaunchArgs& L) {
             L.m1, L.n, L.st);
     return cudaGetLastError();
   });
-  if (e0 != cudaSuccess) return e0;
+  if (e0 != cudaSuccess || L.partials_only) return e0;
+  return launch_reduce_t<A>(static_cast<const A*>(L.part), p.geo.n_tiles, p.geo.det ? (int64_t)p.geo.ng * (L.m1 + L.n) : 1,
+                            p.geo.ng, L.m1, L.n, static_cast<A*>(L.da), static_cast<A*>(L.db), L.st, L.stream);
+}
+
+// K3 alone: fixed-order fold of n_tiles partials per (group, coefficient)
+// (column-major, slot_stride 1; or slot-major, slot_stride ng * kc).
+template <typename A>
+cudaError_t launch_reduce_t(const A* part, int64_t n_tiles, int64_t slot_stride, int ng, int m1, int n, A* da,
+                            A* db, DevStatus* st, cudaStream_t stream) {
   // K3 with programmatic dependent launch: its launch overlaps K2's tail and
   // its griddepcontrol.wait orders it after all of K2's memory operations.
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(p.geo.ng * (L.m1 + L.n)));
+  cfg.gridDim = dim3(static_cast<unsigned>(ng * (m1 + n)));
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = 0;
-  cfg.stream = L.stream;
+  cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_bwd_reduce<A>, static_cast<const A*>(L.part), p.geo.n_tiles,
-                            L.m1, L.n, static_cast<A*>(L.da), static_cast<A*>(L.db), L.st);
+  return cudaLaunchKernelEx(&cfg, k_bwd_reduce<A>, part, n_tiles, m1, n, da, db, st, slot_stride);
 }
 
 template <typename T>
@@ -159,4 +174,10 @@ cudaError_t launch_atomic_t(const LaunchArgs& L) {
   cudaError_t launch_fwd_##SUF(const LaunchArgs& L) { return launch_fwd_t<T>(L); }           \
   cudaError_t launch_bwd_##SUF(const LaunchArgs& L) { return launch_bwd_t<T>(L); }           \
   cudaError_t launch_atomic_##SUF(const LaunchArgs& L) { return launch_atomic_t<T>(L); }     \
+  cudaError_t launch_reduce_##SUF(const void* part, int64_t n_tiles, int64_t slot_stride, int ng, int m1, \
+                                  int n, void* da, void* db, DevStatus* st, cudaStream_t s) {   \
+    using A = typename VecIO<T, 1>::A;                                                       \
+    return launch_reduce_t<A>(static_cast<const A*>(part), n_tiles, slot_stride, ng, m1, n,   \
+                              static_cast<A*>(da), static_cast<A*>(db), st, s);             \
+  }                                                                                          \
   }

@@ -411,7 +411,7 @@ struct RationalX2 {
   // reference's rounding in FAST mode too: measured faster for bf16 I/O, whose
   // backward is latency-bound and loses more to the guard's branches than it
   // gains from 3 fewer FMUL2 per pair (fp32: 323 -> 307 us with the guard,
-  // bf16: 260 -> 273 us at KAT-B).
+  // bf16: 260 -> 273 us at KAT-B; 283 us with a warp-uniform __any_sync branch).
   template <int NP, bool GUARD = true>
   __device__ __forceinline__ void grad_n(const float (&vx)[2 * NP], const float (&vu)[2 * NP],
                                          float (&o)[2 * NP], float2 (&acc)[KC]) const {

@@ -182,9 +182,40 @@ __device__ __forceinline__ void staged_range(const Geom& geo, int& g, int64_t& j
   j = bid / geo.ng;
   const int64_t s0 = (j * geo.nsu) / geo.pg;
   const int64_t s1 = ((j + 1) * geo.nsu) / geo.pg;
-  row0 = s0 * geo.RS;
-  const int64_t r1 = s1 * geo.RS < geo.rows ? s1 * geo.RS : geo.rows;
+  row0 = s0 * geo.RU;
+  const int64_t r1 = s1 * geo.RU < geo.rows ? s1 * geo.RU : geo.rows;
   nr = static_cast<int>(r1 - row0);
+}
+
+// Deterministic mode: the CTA's lanes have just flushed one RB-row block into
+// sacc.  Fixed butterfly per warp -> red[buf][warp], consumer-warp barrier,
+// warp 0 folds the warps in order -> part[(blk * ng + g) * KC + k]; sacc is
+// re-zeroed for the next block.  The partial depends only on the block's
+// data (the thread -> element map is fixed per stage), never on which CTA
+// processed it: bitwise identical for any row sharding aligned to RB.
+template <typename A, int KC>
+__device__ __forceinline__ void block_store(A* __restrict__ sacc, A (&red)[2][kConsumerWarps][KC], int buf,
+                                            A* __restrict__ part, int g, int64_t blk, int warp,
+                                            const Geom& geo) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < KC; ++k) {
+    A v = sacc[k * (32 * kConsumerWarps) + threadIdx.x];
+    sacc[k * (32 * kConsumerWarps) + threadIdx.x] = A(0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[buf][warp][k] = v;
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps) : "memory");
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+      A v = lane < kConsumerWarps ? red[buf][lane][k] : A(0);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) part[(blk * geo.ng + g) * KC + k] = v;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -221,7 +252,7 @@ __device__ __forceinline__ void produce(const T* const (&src)[NT], T* const (&ri
 // ---------------------------------------------------------------------------
 // K2 staged: backward main pass, degrees (5, 4).
 // ---------------------------------------------------------------------------
-template <typename T, bool EXACT, bool CHECK>
+template <typename T, bool EXACT, bool CHECK, bool DET>
 __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
     k_bwd_staged(const T* __restrict__ x, const T* __restrict__ dy, T* __restrict__ dx,
                  const typename VecIO<T, 1>::A* __restrict__ ca,
@@ -235,12 +266,14 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
   constexpr int KC = 10;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
+  __shared__ A red[DET ? 2 : 1][DET ? kConsumerWarps : 1][DET ? KC : 1];
   pdl_launch_dependents();
 
   int g;
   int64_t tile, row0;
   int nr;
   staged_range(geo, g, tile, row0, nr);
+  if (DET) tile = row0 / geo.RU;  // first RB-row block of this CTA
   const size_t ring_elems = (size_t)stages * geo.RS * geo.dg;
   T* const sx = reinterpret_cast<T*>(smem_raw);
   T* const su = sx + ring_elems;
@@ -269,7 +302,7 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
     if (lane == 0) {
       const T* const src[2] = {x, dy};
       T* const ring[2] = {sx, su};
-      produce<T, 2>(src, ring, geo, row0, nr, stages, full, empty, g);
+      if (!GRKAN_PROBE_NOMEM) produce<T, 2>(src, ring, geo, row0, nr, stages, full, empty, g);
     }
   } else {
     RationalX2<EXACT> rp;
@@ -300,7 +333,7 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
     int slot = 0, since_flush = 0;
     uint32_t phase = 0;
     for (int s = 0; s < nst; ++s) {
-      mbar_wait(&full[slot], phase);
+      if (!GRKAN_PROBE_NOMEM) mbar_wait(&full[slot], phase);
       const int rows_here = min(geo.RS, nr - s * geo.RS);
       const T* xs = sx + slot * slot_elems;
       const T* us = su + slot * slot_elems;
@@ -331,17 +364,26 @@ rp.template grad_n<W / 2, kGuard<T>>(vx, vu, o, acc2);
       if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
       // Short per-lane fp32 chains keep the da/db rounding error near the fp32
       // term-evaluation floor (see lane_flush).
-      if (++since_flush == geo.flush || s + 1 == nst) {
+      const bool block_end = DET && ((s + 1) % geo.spb == 0 || s + 1 == nst);
+      if (++since_flush == geo.flush || s + 1 == nst || block_end) {
         lane_flush<A, KC, PK>(acc, acc2, sacc);
         since_flush = 0;
+      }
+      if constexpr (DET) {
+        if (block_end) {
+          __syncwarp();
+          block_store<A, KC>(sacc, red, (s / geo.spb) & 1, part, g, tile + s / geo.spb, warp, geo);
+        }
       }
       if (++slot == stages) {
         slot = 0;
         phase ^= 1;
       }
     }
-    __syncwarp();
-    warp_store<A, KC>(sacc, part, g, tile, warp, geo);
+    if constexpr (!DET) {
+      __syncwarp();
+      warp_store<A, KC>(sacc, part, g, tile, warp, geo);
+    }
   }
   if (CHECK && chk.bad()) st->nonfinite_input = 1;
 }

@@ -21,6 +21,10 @@ struct Geom {
   int64_t nsu;      // stage units per group = ceil(rows / RS)
   float one;        // 1.0f, opaque to ptxas (see grkan_math.cuh xmad2)
   int32_t flush;    // staged backward: stages between per-lane accumulator flushes
+  int32_t RU;       // staged: rows per partition unit (RS; RB in deterministic mode)
+  int32_t det;      // deterministic (global row-block) partials: slot-major
+                    // part[(block * ng + g) * kc + k], one partial per RB-row block
+  int32_t spb;      // staged deterministic: stages per block (RB / RS)
 };
 
 struct DevStatus {
@@ -76,6 +80,9 @@ struct Plan {
 #ifndef GRKAN_FWD_STAGES
 #define GRKAN_FWD_STAGES 4         // staged forward ring depth
 #endif
+#ifndef GRKAN_PROBE_NOMEM
+#define GRKAN_PROBE_NOMEM 0       // diagnostic only: staged backward computes on unfilled shared memory
+#endif
 #ifndef GRKAN_FWD_CTAS
 #define GRKAN_FWD_CTAS 8
 #endif
@@ -103,6 +110,7 @@ struct LaunchArgs {
   DevStatus* st;
   int m1, n;
   bool exact, vec, check;
+  bool partials_only;  // backward: K2 only (deterministic multi-GPU path)
   cudaStream_t stream;
 };
 
@@ -116,5 +124,9 @@ cudaError_t launch_bwd_f64(const LaunchArgs&);
 cudaError_t launch_atomic_f32(const LaunchArgs&);
 cudaError_t launch_atomic_bf16(const LaunchArgs&);
 cudaError_t launch_atomic_f64(const LaunchArgs&);
+cudaError_t launch_reduce_f32(const void* part, int64_t n_tiles, int64_t slot_stride, int ng, int m1, int n,
+                              void* da, void* db, DevStatus* st, cudaStream_t s);
+cudaError_t launch_reduce_f64(const void* part, int64_t n_tiles, int64_t slot_stride, int ng, int m1, int n,
+                              void* da, void* db, DevStatus* st, cudaStream_t s);
 
 }  // namespace grkan

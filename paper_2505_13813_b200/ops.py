@@ -9,6 +9,9 @@ Public functions
   rational_forward(x, a, b)            -> y        (grkan_fwd)
   rational_backward(x, dy, a, b)       -> dx, da, db (grkan_bwd: K2 + K3)
   rational_backward_atomic(x, dy, a, b)-> dx, da, db (grkan_bwd_atomic, Alg. 1 comparator)
+  rational_backward(..., deterministic=True)   row-sharding-invariant da/db
+  backward_partials(x, dy, a, b)       -> dx, per-block partials (grkan_bwd_partials)
+  reduce_partials(part, ...)           -> da, db (grkan_reduce_partials)
 and the torch.library ops ``grkan_b200::rational_fwd`` / ``rational_bwd``
 (graph-capturable, torch.compile-traceable through their fake kernels).
 """
@@ -60,8 +63,9 @@ def _validate(x: torch.Tensor, a: torch.Tensor, b: torch.Tensor):
     return rows, d, ng, a.shape[1], b.shape[1]
 
 
-def _flags(exact: bool, check_finite: bool) -> int:
-    return (N.FLAG_EXACT if exact else N.FLAG_FAST) | (N.FLAG_CHECK_FINITE if check_finite else 0)
+def _flags(exact: bool, check_finite: bool, deterministic: bool = False) -> int:
+    return ((N.FLAG_EXACT if exact else N.FLAG_FAST) | (N.FLAG_CHECK_FINITE if check_finite else 0)
+            | (N.FLAG_DETERMINISTIC if deterministic else 0))
 
 
 def _raise(rc):
@@ -111,8 +115,14 @@ def workspace_bytes(rows: int, d: int, ng: int, m1: int, n: int, dtype: torch.dt
 def rational_backward(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor, b: torch.Tensor,
                       exact: bool = False, check_finite: bool = False, check_overflow: bool = False,
                       workspace: torch.Tensor | None = None, da_out: torch.Tensor | None = None,
-                      db_out: torch.Tensor | None = None, dx_out: torch.Tensor | None = None):
+                      db_out: torch.Tensor | None = None, dx_out: torch.Tensor | None = None,
+                      deterministic: bool = False):
     """(dx, da, db) with per-CTA partials and a deterministic second pass.
+
+    ``deterministic`` folds one partial per global row block
+    (det_block_rows) instead of one per CTA: da/db are then bitwise what any
+    block-aligned row sharding gives through backward_partials +
+    reduce_partials (parallel.deterministic_backward).
 
     Mirrors backward_blocked (pkg/src/grkan/backward.py:275-372).  da/db are
     in the coefficient dtype (fp32 for fp32/bf16 tensors).  ``check_overflow``
@@ -145,12 +155,74 @@ def rational_backward(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor, b: tor
     with torch.cuda.device(x.device):
         rc = N.lib().grkan_bwd(x.data_ptr(), dy.data_ptr(), a.data_ptr(), _ptr(b), dx.data_ptr(),
                                da.data_ptr(), _ptr(db), workspace.data_ptr(), workspace.numel(),
-                               rows, d, ng, m1, n, _DT[x.dtype], _flags(exact, check_finite),
+                               rows, d, ng, m1, n, _DT[x.dtype], _flags(exact, check_finite, deterministic),
                                _stream(x.device))
         _raise(rc)
         if check_finite or check_overflow:
             read_status(workspace[:8])
     return dx, da, db
+
+
+def det_block_rows(d: int, ng: int, dtype: torch.dtype) -> int:
+    """Rows per global block of the deterministic mode (shard boundaries must be multiples)."""
+    rb = N.lib().grkan_det_block_rows(d, ng, _DT[dtype])
+    if rb <= 0:
+        raise LayoutMismatchError("layout mismatch: feature_dim %d not divisible by num_groups %d" % (d, ng))
+    return rb
+
+
+def backward_partials(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor, b: torch.Tensor,
+                      exact: bool = False, check_finite: bool = False, part_out: torch.Tensor | None = None,
+                      dx_out: torch.Tensor | None = None):
+    """dx and this shard's per-block coefficient partials, [n_blocks, ng, m1 + n] (no reduction).
+
+    The shard must start on a multiple of det_block_rows() rows of the global
+    tensor; concatenating every shard's partials in row order and calling
+    reduce_partials gives bitwise the single-GPU deterministic da/db.
+    """
+    rows, d, ng, m1, n = _validate(x, a, b)
+    if dy.shape != x.shape or dy.dtype != x.dtype or dy.device != x.device:
+        from .errors import GridGeometryError
+        raise GridGeometryError("grid geometry invalid: x and upstream differ in shape, dtype or device")
+    x, dy, a, b = x.contiguous(), dy.contiguous(), a.contiguous(), b.contiguous()
+    dx = torch.empty_like(x) if dx_out is None else dx_out
+    n_blocks = -(-rows // det_block_rows(d, ng, x.dtype))
+    part = (torch.empty((n_blocks, ng, m1 + n), dtype=a.dtype, device=x.device)
+            if part_out is None else part_out)
+    if part.shape != (n_blocks, ng, m1 + n) or part.dtype != a.dtype or not part.is_contiguous():
+        raise ValueError("part_out must be a contiguous %s tensor of shape %s"
+                         % (a.dtype, (n_blocks, ng, m1 + n)))
+    status = torch.zeros(2, dtype=torch.int32, device=x.device) if check_finite else None
+    with torch.cuda.device(x.device):
+        rc = N.lib().grkan_bwd_partials(x.data_ptr(), dy.data_ptr(), a.data_ptr(), _ptr(b), dx.data_ptr(),
+                                        part.data_ptr(), part.numel() * part.element_size(), rows, d, ng,
+                                        m1, n, _DT[x.dtype], _flags(exact, check_finite), _ptr(status),
+                                        _stream(x.device))
+        _raise(rc)
+        if check_finite:
+            read_status(status)
+    return dx, part
+
+
+def reduce_partials(part: torch.Tensor, m1: int, n: int, check_overflow: bool = False,
+                    da_out: torch.Tensor | None = None, db_out: torch.Tensor | None = None):
+    """Fixed-order fp64 fold of [n_blocks, ng, m1 + n] partials -> (da, db) (combine_partials)."""
+    if part.dim() != 3 or part.shape[2] != m1 + n:
+        raise LayoutMismatchError("layout mismatch: partials must be [blocks, groups, m1 + n]")
+    if not part.is_cuda or not part.is_contiguous() or part.dtype not in (torch.float32, torch.float64):
+        raise UnsupportedError("partials must be a contiguous CUDA float32/float64 tensor")
+    nb, ng = part.shape[0], part.shape[1]
+    da = torch.empty((ng, m1), dtype=part.dtype, device=part.device) if da_out is None else da_out
+    db = torch.empty((ng, n), dtype=part.dtype, device=part.device) if db_out is None else db_out
+    status = torch.zeros(2, dtype=torch.int32, device=part.device)
+    dt = N.DT_F64 if part.dtype == torch.float64 else N.DT_F32
+    with torch.cuda.device(part.device):
+        rc = N.lib().grkan_reduce_partials(part.data_ptr(), nb, ng, m1, n, da.data_ptr(), _ptr(db), dt,
+                                           status.data_ptr(), _stream(part.device))
+        _raise(rc)
+        if check_overflow:
+            read_status(status)
+    return da, db
 
 
 def rational_backward_atomic(x, dy, a, b, exact: bool = False, check_overflow: bool = False):

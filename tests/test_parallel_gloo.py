@@ -99,3 +99,72 @@ def test_shard_rows_rejects_bad_args():
         parallel.shard_rows(10, 2, 2)
     with pytest.raises(ValueError):
         parallel.shard_rows(10, 2, 0, align=3)
+
+
+# ---------------------------------------------------------------------------
+# Deterministic (world-size-invariant) path: block-aligned shards + all-gather
+# of per-block partials in rank order (parallel.gather_blocks).  The partials
+# here are the oracle's fp64 per-block sums; on the GPU they come from
+# grkan_bwd_partials (tests/test_gpu_deterministic.py).
+# ---------------------------------------------------------------------------
+
+def _block_partials(rows, urows, num, den, start, stop, rb):
+    from oracle import grkan_oracle as orc
+    out = []
+    for r0 in range(start, stop, rb):
+        r1 = min(stop, r0 + rb)
+        _, da, db = orc.true64_grads(rows[r0:r1][None], urows[r0:r1][None], num, den)
+        out.append(np.concatenate([da, db], axis=1))
+    return np.stack(out) if out else np.zeros((0, num.shape[0], num.shape[1] + den.shape[1]))
+
+
+def _gather_worker(rank, world, port, q, total, rb):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import grkan_oracle as orc
+        x, u, num, den = orc.bench_inputs(1, total, 16, 2, seed=5)
+        rows, urows = x.reshape(-1, 16), u.reshape(-1, 16)
+        counts = parallel.block_counts(total, world, rb)
+        lo, hi = parallel.block_shard(total, world, rank, rb)
+        local = torch.from_numpy(_block_partials(rows, urows, num, den, lo, hi, rb))
+        full = parallel.gather_blocks(local, counts)
+        q.put((rank, lo, hi, full.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,total,rb", [(2, 40, 8), (3, 37, 8), (2, 5, 8)])
+def test_gather_blocks_is_rank_order_concatenation(world, total, rb):
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, q, total, rb)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from oracle import grkan_oracle as orc
+    x, u, num, den = orc.bench_inputs(1, total, 16, 2, seed=5)
+    want = _block_partials(x.reshape(-1, 16), u.reshape(-1, 16), num, den, 0, total, rb)
+    for _, _, _, full in res:
+        # every rank holds the same global-order block array: bitwise the unsharded one
+        assert full.shape == want.shape and full.tobytes() == want.tobytes()
+    assert res[0][1] == 0 and res[-1][2] == total
+
+
+@pytest.mark.parametrize("total", [0, 1, 127, 128, 129, 1000, 50432])
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_block_shards_cover_rows_on_block_boundaries(total, world):
+    rb = 128
+    counts = parallel.block_counts(total, world, rb)
+    spans = [parallel.block_shard(total, world, r, rb) for r in range(world)]
+    assert sum(counts) == -(-total // rb)
+    assert spans[0][0] == 0 and spans[-1][1] == total
+    for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+        assert a1 == b0
+    for (s0, s1), c in zip(spans, counts):
+        assert (s0 % rb == 0 or s1 == s0) and -(-(s1 - s0) // rb) == c
