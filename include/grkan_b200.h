@@ -136,6 +136,20 @@ GRKAN_API int grkan_reduce_partials(const void* part, int64_t n_blocks, int32_t 
                                     int32_t n, void* da, void* db, int32_t dtype, grkan_device_status* status,
                                     void* stream);
 
+/* Fused GR-KAN layer backward through its linear map (the
+ * reference's layer_backward, pkg/src/grkan/layer.py:318-379, step by step):
+ *   dF = dY . W  on the tcgen05 tensor cores (bf16 x bf16 -> fp32 in TMEM),
+ *   dX = R'(X, dF) and the per-tile da / db partials in the epilogue,
+ * then the fixed-order fold (as grkan_bwd) -- dF never touches HBM.
+ * dY [M, K], W [K, N] (torch Linear weight [out, in]), X / dX [M, N]: bf16,
+ * row-major, 16-byte aligned; a [n_groups, 6], b [n_groups, 4], da, db: fp32
+ * (degrees (5, 4)); FAST policy.  Needs K % 64 == 0 and a group width
+ * N / n_groups that is a multiple of 32.  Status words at the start of `ws`. */
+GRKAN_API size_t grkan_linear_bwd_workspace_bytes(int64_t M, int32_t N, int32_t K, int32_t n_groups);
+GRKAN_API int grkan_linear_bwd(const void* dy, const void* w, const void* x, const void* a, const void* b,
+                               void* dx, void* da, void* db, void* ws, size_t ws_bytes, int64_t M, int32_t N,
+                               int32_t K, int32_t n_groups, uint32_t flags, void* stream);
+
 /* Synchronise `stream` and copy the device status to the host; maps it to a
  * status code (NONFINITE_INPUT first, then ACCUM_OVERFLOW, else OK). */
 GRKAN_API int grkan_read_status(const grkan_device_status* status, void* stream,

@@ -40,7 +40,7 @@ EXPORTS = (
     "grkan_version", "grkan_status_string", "grkan_last_error", "grkan_fwd",
     "grkan_bwd_workspace_bytes", "grkan_bwd", "grkan_bwd_atomic", "grkan_read_status",
     "grkan_plan", "grkan_det_block_rows", "grkan_det_partials_bytes", "grkan_bwd_partials",
-    "grkan_reduce_partials",
+    "grkan_reduce_partials", "grkan_linear_bwd_workspace_bytes", "grkan_linear_bwd",
 )
 
 
@@ -85,6 +85,10 @@ def _declare(L):
     L.grkan_bwd_partials.restype = ctypes.c_int
     L.grkan_reduce_partials.argtypes = [p, i64, i32, i32, i32, p, p, i32, p, p]
     L.grkan_reduce_partials.restype = ctypes.c_int
+    L.grkan_linear_bwd_workspace_bytes.argtypes = [i64, i32, i32, i32]
+    L.grkan_linear_bwd_workspace_bytes.restype = sz
+    L.grkan_linear_bwd.argtypes = [p, p, p, p, p, p, p, p, p, sz, i64, i32, i32, i32, u32, p]
+    L.grkan_linear_bwd.restype = ctypes.c_int
 
 
 def lib():

@@ -239,6 +239,11 @@ size_t ws_bytes_for(const Plan& p, int32_t m1, int32_t n, int32_t dtype) {
 
 }  // namespace
 
+namespace grkan {
+// Error reporting for the other C-ABI translation units (grkan_fused.cu).
+int set_error(int code, const char* msg) { return fail(code, "%s", msg); }
+}  // namespace grkan
+
 extern "C" {
 
 const char* grkan_version(void) { return GRKAN_VERSION_STRING; }

@@ -12,6 +12,8 @@ Public functions
   rational_backward(..., deterministic=True)   row-sharding-invariant da/db
   backward_partials(x, dy, a, b)       -> dx, per-block partials (grkan_bwd_partials)
   reduce_partials(part, ...)           -> da, db (grkan_reduce_partials)
+  linear_backward_fused(dy, w, x, a, b)-> dx, da, db (grkan_linear_bwd: tcgen05 dY.W + rational
+                                        backward epilogue, dF never in HBM)
 and the torch.library ops ``grkan_b200::rational_fwd`` / ``rational_bwd``
 (graph-capturable, torch.compile-traceable through their fake kernels).
 """
@@ -268,3 +270,46 @@ def rational_bwd_op(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor, b: torch
 @rational_bwd_op.register_fake
 def _(x, dy, a, b, exact):
     return torch.empty_like(x), a.new_empty(a.shape), b.new_empty(b.shape)
+
+
+def linear_backward_fused(dy: torch.Tensor, w: torch.Tensor, x: torch.Tensor, a: torch.Tensor, b: torch.Tensor,
+                          check_overflow: bool = False):
+    """Backward of  Y = R(X) W^T  through W and R in one kernel.
+
+    dy [..., K], w [K, F] (torch Linear weight [out, in]), x [..., F]: bf16 CUDA
+    tensors; a [ng, 6], b [ng, 4] fp32.  Returns (dx like x, da, db) where
+    dx = R'(x, dy @ w) and da/db the coefficient gradients -- what
+    rational_backward(x, dy @ w, a, b) gives, without materialising dy @ w.
+    (dW = dy^T R(x) is a plain GEMM and stays with the caller.)
+    """
+    if x.dtype != torch.bfloat16 or dy.dtype != torch.bfloat16 or w.dtype != torch.bfloat16:
+        raise UnsupportedError("fused linear backward takes bf16 dy, w and x")
+    if not (x.is_cuda and dy.is_cuda and w.is_cuda):
+        raise UnsupportedError("fused linear backward needs CUDA tensors; there is no CPU path")
+    feat = x.shape[-1]
+    k = dy.shape[-1]
+    if w.dim() != 2 or tuple(w.shape) != (k, feat):
+        raise LayoutMismatchError("layout mismatch: w must be [K=%d, F=%d], got %s" % (k, feat, tuple(w.shape)))
+    rows = x.numel() // feat if feat else 0
+    if dy.numel() // k != rows:
+        from .errors import GridGeometryError
+        raise GridGeometryError("grid geometry invalid: dy and x disagree on the row count")
+    if a.dtype != torch.float32 or b.dtype != torch.float32 or a.shape[1] != 6 or b.shape[1] != 4:
+        raise UnsupportedError("fused linear backward: fp32 coefficients of degrees (5, 4)")
+    ng = a.shape[0]
+    x, dy, w, a, b = x.contiguous(), dy.contiguous(), w.contiguous(), a.contiguous(), b.contiguous()
+    dx = torch.empty_like(x)
+    da = torch.empty((ng, 6), dtype=torch.float32, device=x.device)
+    db = torch.empty((ng, 4), dtype=torch.float32, device=x.device)
+    nbytes = N.lib().grkan_linear_bwd_workspace_bytes(rows, feat, k, ng)
+    if nbytes == 0:
+        raise UnsupportedError("fused linear backward: unsupported shape (F=%d, groups=%d, K=%d)" % (feat, ng, k))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+    with torch.cuda.device(x.device):
+        rc = N.lib().grkan_linear_bwd(dy.data_ptr(), w.data_ptr(), x.data_ptr(), a.data_ptr(), b.data_ptr(),
+                                      dx.data_ptr(), da.data_ptr(), db.data_ptr(), ws.data_ptr(), ws.numel(),
+                                      rows, feat, k, ng, N.FLAG_FAST, _stream(x.device))
+        _raise(rc)
+        if check_overflow:
+            read_status(ws[:8])
+    return dx, da, db

@@ -1,0 +1,74 @@
+"""Fused GR-KAN layer backward (tcgen05 GEMM + rational-backward epilogue), SURVEY.md 8f #3.
+
+Reference: the unfused chain the reference's layer_backward performs
+(pkg/src/grkan/layer.py:318-379): dF = dY . W, then backward_blocked(X, dF).
+Here dF comes from an fp32 torch matmul of the same bf16 operands (TF32 off)
+and the rational backward from this package's own parity-tested kernel, and,
+at small sizes, from the fp64 oracle.  Tolerances: dx (bf16 output)
+max-scaled <= 1e-2 (north_star's bf16 bar); da/db max-scaled <= 1e-4 vs the
+fp32 chain (dF summation order differs) and <= 1e-5 vs fp64.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import grkan_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda", 0) if torch.cuda.is_available() else None
+
+SHAPES = [
+    # M, F (features of X), K (out features of W), groups
+    (256, 256, 128, 2),       # dg 128 -> BN 128, 128B-swizzle B atoms
+    (200, 256, 64, 4),        # M tail (TMA zero fill, masked rows); dg 64
+    (384, 768, 192, 8),       # dg 96 -> BN 96, 64B-swizzle B atoms
+    (1024, 3072, 768, 8),     # KAT-B second rational -> fc2 (dg 384 -> BN 192)
+    (512, 768, 3072, 8),      # KAT-B first rational -> fc1 (K = 3072)
+]
+
+
+def _inputs(M, F, K, ng, seed):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    x = torch.randn(M, F, generator=g).to(torch.bfloat16)
+    dy = torch.randn(M, K, generator=g).to(torch.bfloat16)
+    w = (torch.randn(K, F, generator=g) / K ** 0.5).to(torch.bfloat16)
+    a = torch.randn(ng, 6, generator=g)
+    b = torch.randn(ng, 4, generator=g)
+    return [t.to(DEV) for t in (x, dy, w, a, b)]
+
+
+@pytest.mark.parametrize("M,F,K,ng", SHAPES)
+def test_fused_matches_unfused_chain(M, F, K, ng):
+    from paper_2505_13813_b200 import ops
+    torch.backends.cuda.matmul.allow_tf32 = False
+    x, dy, w, a, b = _inputs(M, F, K, ng, seed=M + F + K)
+    dx, da, db = ops.linear_backward_fused(dy, w, x, a, b, check_overflow=True)
+    dF = dy.float() @ w.float()
+    dx_ref, da_ref, db_ref = ops.rational_backward(x.float(), dF, a, b)
+    assert orc.matrix_rel(dx.float().cpu().numpy(), dx_ref.cpu().numpy()) <= 1e-2
+    assert orc.matrix_rel(da.cpu().numpy(), da_ref.cpu().numpy()) <= 1e-4
+    assert orc.matrix_rel(db.cpu().numpy(), db_ref.cpu().numpy()) <= 1e-4
+    if M * F <= 300_000:  # fp64 oracle at small sizes
+        dF64 = dy.double().cpu().numpy() @ w.double().cpu().numpy()
+        xs = x.double().cpu().numpy()[None]
+        dx64, da64, db64 = orc.true64_grads(xs, dF64[None], a.double().cpu().numpy(), b.double().cpu().numpy())
+        assert orc.matrix_rel(da.double().cpu().numpy(), da64) <= 1e-5
+        assert orc.matrix_rel(db.double().cpu().numpy(), db64) <= 1e-5
+        assert orc.matrix_rel(dx.double().cpu().numpy(), dx64[0]) <= 1e-2
+
+
+def test_fused_is_deterministic_and_rejects_bad_shapes():
+    from paper_2505_13813_b200 import ops
+    from paper_2505_13813_b200.errors import GrkanError
+    x, dy, w, a, b = _inputs(256, 256, 128, 2, seed=3)
+    r1 = ops.linear_backward_fused(dy, w, x, a, b)
+    r2 = ops.linear_backward_fused(dy, w, x, a, b)
+    for t1, t2 in zip(r1, r2):
+        assert torch.equal(t1, t2)
+    with pytest.raises(GrkanError):  # K not a multiple of 64
+        ops.linear_backward_fused(dy[:, :100].contiguous(), w[:100].contiguous(), x, a, b)
+    with pytest.raises(GrkanError):  # group width 40 (not a multiple of 32)
+        x2, dy2, w2, a2, b2 = _inputs(128, 80, 64, 2, seed=4)
+        ops.linear_backward_fused(dy2, w2, x2, a2, b2)

@@ -13,3 +13,6 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_b
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_fwd" -s 2 -c 1 -o gpurun_out/prof_${TAG}_fwd_fp32 $B > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_bwd_reduce" -s 2 -c 1 -o gpurun_out/prof_${TAG}_reduce_fp32 $B > /dev/null 2>&1
 ls -la gpurun_out | grep ${TAG}
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_bwd_staged" -s 2 -c 1 -o gpurun_out/prof_${TAG}_bwd_bf16 $B --dtype bf16 > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s 12 -c 15 --csv --log-file gpurun_out/launches_${TAG}_bf16.csv $B --dtype bf16 > /dev/null 2>&1
+ls -la gpurun_out | grep ${TAG}
