@@ -10,22 +10,24 @@
 //     dF = dY [M, K] . W [K, N]          bf16 x bf16 -> fp32, accumulated in TMEM
 //     dX = R'(X, dF),  da / db partials  in the epilogue, straight from TMEM
 //
-// so dF never exists in HBM.  Per CTA: one 128 x BN output tile (BN divides
-// the group width, so the tile's coefficients are CTA-uniform) and the whole
-// K loop.  Warp roles (192 threads):
+// so dF never exists in HBM.  Tiles are 128 x BN (BN divides the group width,
+// so a tile's coefficients are uniform) with the whole K loop; a persistent
+// CTA per SM walks its tiles with two TMEM accumulator buffers.  Warp roles:
 //   warp 0      TMA producer: dY tile [128 x 64] (K-major, 128B swizzle) and
 //               W tile [64 x BN] (N-major, 128B/64B swizzle atoms) per stage
 //   warp 1      TMEM allocator + MMA issuer (one elected lane issues
 //               tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16 x 4 per stage;
 //               tcgen05.commit frees the stage / signals the epilogue)
-//   warps 2-5   epilogue: tcgen05.ld 32 columns at a time (thread = tile row =
-//               TMEM lane), X from global (32-byte sectors), RationalX2 grad on
-//               element pairs (the unfused backward's math, FAST policy), dX to
-//               global, ten fp32 accumulators -> one partial per tile per
-//               coefficient (fixed butterfly + fixed warp order, no atomics)
-// then the unfused path's K3 folds the partials in fixed order.  Two CTAs per
-// SM (3-stage ring, 96 KB smem, 2 x BN TMEM columns) overlap one CTA's
-// epilogue with the other's MMA.
+//   warps 2..  4 * ES epilogue warps: tcgen05.ld 32 columns at a time (thread =
+//               tile row = TMEM lane; ES warps per lane quadrant split the
+//               columns), X from global (32-byte sectors, prefetched one chunk
+//               ahead), RationalX2 grad on element pairs (the unfused
+//               backward's math, FAST policy), dX to global, ten fp32
+//               accumulators -> one partial per (tile, warp) per coefficient
+//               (fixed butterfly, no atomics)
+// then the unfused path's K3 folds the partials in fixed order.  The epilogue
+// releases a TMEM buffer as soon as its last tcgen05.ld lands, so the next
+// tile's MMA overlaps the rational math.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -46,8 +48,7 @@ namespace fused {
 
 constexpr int kBM = 128;          // tile rows (UMMA M, TMEM lanes)
 constexpr int kBK = 64;           // K per stage (one 128-byte swizzle row of bf16)
-constexpr int kStages = 3;
-constexpr int kThreads = 192;     // producer, MMA, 4 epilogue warps
+constexpr int kSmemBudget = 200 * 1024;  // operand ring (the rest: alignment + barriers)
 constexpr int kKC = 10;           // coefficient terms (degrees (5, 4))
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
@@ -109,18 +110,41 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 lanes x 16 columns.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int CH>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[CH]) {
+  if constexpr (CH == 32) tmem_ld32(taddr, v); else tmem_ld16(taddr, v);
+}
+
 struct FusedGeom {
   int64_t M;
   int32_t N, K, ng, dg;
   int32_t n_tiles_n;   // N / BN
-  int32_t tiles_pg;    // partials per group = m_tiles * (dg / BN)
+  int32_t ppg;         // partials per group = m_tiles * (dg / CW) * 4 (one per warp sub-tile)
   float one;
 };
 
-// B tile (W rows k0..k0+63, columns n0..n0+BN-1) is loaded as BN / ATOM boxes
-// of ATOM columns x 64 rows; ATOM = 64 (128B swizzle) or 32 (64B swizzle).
-template <int BN, int ATOM>
-__global__ void __launch_bounds__(kThreads, 2)
+// Persistent, warp-specialised: grid = min(tiles, SMs), CTA c takes tiles
+// c, c + grid, ...; two TMEM accumulator buffers so the MMA of tile i + 1 runs
+// while the epilogue drains tile i.  B tile (W rows k0..k0+63, columns
+// n0..n0+BN-1) is loaded as BN / ATOM boxes of ATOM columns x 64 rows; ATOM =
+// 64 (128B swizzle) or 32 (64B swizzle).  ES epilogue warps per TMEM lane
+// quadrant split the tile's columns (4 * ES epilogue warps in all).
+template <int BN, int ATOM, int ES, int CH, int kStages>
+__global__ void __launch_bounds__(64 + 128 * ES, 1)
     k_linear_bwd_fused(const __grid_constant__ CUtensorMap map_dy, const __grid_constant__ CUtensorMap map_w,
                        const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ dx,
                        const float* __restrict__ ca, const float* __restrict__ cb, float* __restrict__ part,
@@ -131,20 +155,19 @@ __global__ void __launch_bounds__(kThreads, 2)
   constexpr int ATOM_BYTES = ATOM * 2 * kBK;        // one swizzle-atom column block
   constexpr uint32_t B_LAYOUT = ATOM == 64 ? 2u : 4u;      // SWIZZLE_128B / SWIZZLE_64B
   constexpr uint32_t B_SBO = ATOM * 2 * 8;                 // 8 K-rows of one atom
-  constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  constexpr int NE = 4 * ES;                        // epilogue warps
+  constexpr int CW = BN / ES;                       // columns per epilogue warp
+  static_assert(CW % CH == 0, "epilogue columns come in CH-column TMEM loads");
+  constexpr int NV = CH / 8;                        // 16-byte X / dX vectors per chunk
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 1024-byte alignment for the swizzle atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[kStages], empty[kStages], tmem_full;
+  __shared__ uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
-  __shared__ float red[4][kKC];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tile = blockIdx.x % geo.n_tiles_n;
-  const int64_t m_tile = blockIdx.x / geo.n_tiles_n;
-  const int n0 = n_tile * BN;
-  const int64_t m0 = m_tile * kBM;
+  const int64_t n_tiles = ((geo.M + kBM - 1) / kBM) * geo.n_tiles_n;
   const int kblocks = geo.K / kBK;
 
   if (threadIdx.x == 0) {
@@ -152,7 +175,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(&tmem_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], NE);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {  // TMEM allocation (whole warp), base address to smem
@@ -172,17 +198,22 @@ __global__ void __launch_bounds__(kThreads, 2)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_w)) : "memory");
       int slot = 0;
       uint32_t phase = 0;
-      for (int kb = 0; kb < kblocks; ++kb) {
-        if (kb >= kStages) mbar_wait(&empty[slot], phase ^ 1);
-        unsigned char* sa = smem + slot * STAGE;
-        unsigned char* sb = sa + A_BYTES;
-        mbar_arrive_expect_tx(&full[slot], STAGE);
-        tma_load_2d(sa, &map_dy, kb * kBK, static_cast<int>(m0), &full[slot]);
+      int64_t it = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int n0 = static_cast<int>(tile % geo.n_tiles_n) * BN;
+        const int m0 = static_cast<int>((tile / geo.n_tiles_n) * kBM);
+        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          if (it >= kStages) mbar_wait(&empty[slot], phase ^ 1);
+          unsigned char* sa = smem + slot * STAGE;
+          unsigned char* sb = sa + A_BYTES;
+          mbar_arrive_expect_tx(&full[slot], STAGE);
+          tma_load_2d(sa, &map_dy, kb * kBK, m0, &full[slot]);
 #pragma unroll
-        for (int a = 0; a < BN / ATOM; ++a) tma_load_2d(sb + a * ATOM_BYTES, &map_w, n0 + a * ATOM, kb * kBK, &full[slot]);
-        if (++slot == kStages) {
-          slot = 0;
-          phase ^= 1;
+          for (int a = 0; a < BN / ATOM; ++a) tma_load_2d(sb + a * ATOM_BYTES, &map_w, n0 + a * ATOM, kb * kBK, &full[slot]);
+          if (++slot == kStages) {
+            slot = 0;
+            phase ^= 1;
+          }
         }
       }
     }
@@ -191,80 +222,106 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint32_t idesc = instr_desc<BN>();
       int slot = 0;
       uint32_t phase = 0;
-      for (int kb = 0; kb < kblocks; ++kb) {
-        mbar_wait(&full[slot], phase);
+      int i = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++i) {
+        const int acc = i & 1;
+        mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);  // epilogue has drained this buffer
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t sa = smem_u32(smem + slot * STAGE);
-        const uint32_t sb = sa + A_BYTES;
+        const uint32_t dcol = tmem_d + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[slot], phase);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(smem + slot * STAGE);
+          const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-        for (int k = 0; k < kBK / 16; ++k) {
-          // A: K-major SW128, +32 B per 16-element K step inside the swizzle row
-          const uint64_t ad = smem_desc(sa + k * 32, 16, 1024, 2);
-          // B: MN-major, K step = two 8-row groups
-          const uint64_t bd = smem_desc(sb + k * 2 * B_SBO, ATOM_BYTES, B_SBO, B_LAYOUT);
-          umma_bf16(tmem_d, ad, bd, idesc, (kb | k) != 0);
+          for (int k = 0; k < kBK / 16; ++k) {
+            // A: K-major SW128, +32 B per 16-element K step inside the swizzle row
+            const uint64_t ad = smem_desc(sa + k * 32, 16, 1024, 2);
+            // B: MN-major, K step = two 8-row groups
+            const uint64_t bd = smem_desc(sb + k * 2 * B_SBO, ATOM_BYTES, B_SBO, B_LAYOUT);
+            umma_bf16(dcol, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[slot]);  // frees the stage when these MMAs complete
+          if (++slot == kStages) {
+            slot = 0;
+            phase ^= 1;
+          }
         }
-        umma_commit(&empty[slot]);  // frees the stage when these MMAs complete
-        if (kb == kblocks - 1) umma_commit(&tmem_full);
-        if (++slot == kStages) {
-          slot = 0;
-          phase ^= 1;
-        }
+        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
       }
     }
   } else {
-    // ---- epilogue: warps 2..5; TMEM lanes 32 * (warp % 4) ..
+    // ---- epilogue warps: lanes 32 * (warp % 4) .. of TMEM, columns cs*CW ..
+    const int e = warp - 2;
     const int q = warp & 3;
+    const int cs = e >> 2;
     const int row = q * 32 + lane;
-    const int64_t grow = m0 + row;
-    const bool live = grow < geo.M;
-    const int g = n0 / geo.dg;
-    RationalX2<false> rp;
-    rp.load(ca, cb, g, geo.one);
-    float2 acc2[kKC];
-#pragma unroll
-    for (int k = 0; k < kKC; ++k) acc2[k] = make_float2(0.f, 0.f);
-    mbar_wait(&tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t taddr = tmem_d + (static_cast<uint32_t>(q * 32) << 16);
-    const __nv_bfloat16* xrow = x + grow * geo.N + n0;
-    __nv_bfloat16* dxrow = dx + grow * geo.N + n0;
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      float u[32];
-      tmem_ld32(taddr + c, u);  // warp-collective: every lane participates
-      if (live) {
-        uint4 xr[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) xr[i] = __ldcs(reinterpret_cast<const uint4*>(xrow + c) + i);
-        uint4 o4[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          float xv[8], o[8];
-          Raw16<__nv_bfloat16>::unpack(xr[i], xv);
-          float uv[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) uv[e] = u[i * 8 + e];
-          rp.template grad_n<4, false>(xv, uv, o, acc2);
-          o4[i] = Raw16<__nv_bfloat16>::pack(o);
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) __stcs(reinterpret_cast<uint4*>(dxrow + c) + i, o4[i]);
+    int i = 0;
+    int g_loaded = -1;
+    RationalX2<false> rp;  // the warp's column block lies in one group (CW | dg)
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++i) {
+      const int acc = i & 1;
+      const int n0 = static_cast<int>(tile % geo.n_tiles_n) * BN;
+      const int64_t m_tile = tile / geo.n_tiles_n;
+      const int64_t grow = m_tile * kBM + row;
+      const bool live = grow < geo.M;
+      const int c0 = n0 + cs * CW;
+      const int g = c0 / geo.dg;
+      if (g != g_loaded) {
+        rp.load(ca, cb, g, geo.one);
+        g_loaded = g;
       }
-    }
-    // one partial per tile per coefficient: fixed butterfly, fixed warp order
+      const __nv_bfloat16* xrow = x + grow * geo.N + c0;
+      __nv_bfloat16* dxrow = dx + grow * geo.N + c0;
+      // X for the first 32 columns is independent of the MMA: fetch it first
+      uint4 xr[2][NV];
+      if (live) {
 #pragma unroll
-    for (int k = 0; k < kKC; ++k) {
-      float v = acc2[k].x + acc2[k].y;
+        for (int v = 0; v < NV; ++v) xr[0][v] = __ldcs(reinterpret_cast<const uint4*>(xrow) + v);
+      }
+      float2 acc2[kKC];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) red[q][k] = v;
-    }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    if (warp == 2 && lane < kKC) {
-      const float v = ((red[0][lane] + red[1][lane]) + red[2][lane]) + red[3][lane];
-      const int64_t t = m_tile * (geo.dg / BN) + (n0 % geo.dg) / BN;
-      part[(static_cast<int64_t>(g) * kKC + lane) * geo.tiles_pg + t] = v;
+      for (int k = 0; k < kKC; ++k) acc2[k] = make_float2(0.f, 0.f);
+      mbar_wait(&tfull[acc], (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t taddr = tmem_d + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + cs * CW);
+#pragma unroll
+      for (int c = 0; c < CW / CH; ++c) {
+        if (live && c + 1 < CW / CH) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) xr[(c + 1) & 1][v] = __ldcs(reinterpret_cast<const uint4*>(xrow + (c + 1) * CH) + v);
+        }
+        float u[CH];
+        tmem_ld<CH>(taddr + c * CH, u);  // warp-collective: every lane participates
+        if (c + 1 == CW / CH) {          // this warp is done with the accumulator buffer
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        if (live) {
+          uint4 o4[NV];
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            float xv[8], o[8], uv[8];
+            Raw16<__nv_bfloat16>::unpack(xr[c & 1][v], xv);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) uv[k] = u[v * 8 + k];
+            rp.template grad_n<4, false>(xv, uv, o, acc2);
+            o4[v] = Raw16<__nv_bfloat16>::pack(o);
+          }
+#pragma unroll
+          for (int v = 0; v < NV; ++v) __stcs(reinterpret_cast<uint4*>(dxrow + c * CH) + v, o4[v]);
+        }
+      }
+      // one partial per (128-row x CW-column warp block) per coefficient: fixed butterfly
+      const int64_t t = (m_tile * (geo.dg / CW) + (c0 % geo.dg) / CW) * 4 + q;
+#pragma unroll
+      for (int k = 0; k < kKC; ++k) {
+        float v = acc2[k].x + acc2[k].y;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) part[(static_cast<int64_t>(g) * kKC + k) * geo.ppg + t] = v;
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -301,33 +358,47 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, 
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Widest BN in {256, 192, 128, 64} dividing the group width, else a multiple
-// of 32 (64B-swizzle B atoms): {224, 160, 96, 32}.
-int pick_bn(int dg, int* atom) {
-  const int c128[] = {256, 192, 128, 64};
-  for (int bn : c128)
-    if (dg % bn == 0) {
-      *atom = 64;
-      return bn;
+// Tile shapes, best first: (BN, B swizzle atom, epilogue warps per lane
+// quadrant ES).  A shape fits when BN divides N and each epilogue warp's
+// column block CW = BN / ES lies inside one group (CW divides the group width).
+// ES = 4 (16 epilogue warps, 576 threads) uses 16-column TMEM loads to fit
+// the 112-register budget; ES <= 2 loads 32 columns at a time.
+struct TileShape {
+  int bn, atom, es, ch;
+};
+constexpr TileShape kShapes[] = {{256, 64, 4, 16}, {192, 64, 4, 16}, {256, 64, 2, 32}, {192, 64, 2, 32},
+                                 {128, 64, 4, 16}, {128, 64, 2, 32}, {96, 32, 1, 32}, {64, 64, 2, 32},
+                                 {64, 64, 1, 32},  {32, 32, 1, 32}};
+
+bool pick_shape(int N, int dg, TileShape* out) {
+  for (const TileShape& t : kShapes) {
+    const int cw = t.bn / t.es;
+    if (N % t.bn == 0 && cw % t.ch == 0 && cw % 16 == 0 && dg % cw == 0) {
+      *out = t;
+      return true;
     }
-  const int c64[] = {224, 160, 96, 32};
-  for (int bn : c64)
-    if (dg % bn == 0) {
-      *atom = 32;
-      return bn;
-    }
-  return 0;
+  }
+  return false;
 }
 
-template <int BN, int ATOM>
+int sms_of_device() {
+  int dev = 0, v = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  return v > 0 ? v : 148;
+}
+
+template <int BN, int ATOM, int ES, int CH>
 cudaError_t launch_t(const CUtensorMap& mdy, const CUtensorMap& mw, const void* x, void* dx, const float* a,
-                     const float* b, float* part, const FusedGeom& geo, int64_t ctas, cudaStream_t s) {
-  constexpr size_t smem = static_cast<size_t>(kStages) * (kBM * kBK * 2 + kBK * BN * 2) + 1024;
-  auto kern = k_linear_bwd_fused<BN, ATOM>;
+                     const float* b, float* part, const FusedGeom& geo, int64_t tiles, cudaStream_t s) {
+  constexpr int kStageBytes = kBM * kBK * 2 + kBK * BN * 2;
+  constexpr int kSt = kSmemBudget / kStageBytes > 8 ? 8 : kSmemBudget / kStageBytes;
+  constexpr size_t smem = static_cast<size_t>(kSt) * kStageBytes + 1024;
+  auto kern = k_linear_bwd_fused<BN, ATOM, ES, CH, kSt>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  kern<<<static_cast<unsigned>(ctas), kThreads, smem, s>>>(mdy, mw, static_cast<const __nv_bfloat16*>(x),
-                                                            static_cast<__nv_bfloat16*>(dx), a, b, part, geo);
+  const int64_t grid = tiles < sms_of_device() ? tiles : sms_of_device();
+  kern<<<static_cast<unsigned>(grid), 64 + 128 * ES, smem, s>>>(mdy, mw, static_cast<const __nv_bfloat16*>(x),
+                                                                 static_cast<__nv_bfloat16*>(dx), a, b, part, geo);
   return cudaGetLastError();
 }
 
@@ -338,11 +409,10 @@ extern "C" {
 
 size_t grkan_linear_bwd_workspace_bytes(int64_t M, int32_t N, int32_t K, int32_t n_groups) {
   if (M < 0 || N < 1 || K < 1 || n_groups < 1 || N % n_groups) return 0;
-  int atom = 0;
-  const int bn = grkan::fused::pick_bn(N / n_groups, &atom);
-  if (!bn) return 0;
-  const int64_t tiles_pg = ((M + grkan::fused::kBM - 1) / grkan::fused::kBM) * ((N / n_groups) / bn);
-  const size_t part = static_cast<size_t>(n_groups) * grkan::fused::kKC * tiles_pg * sizeof(float);
+  grkan::fused::TileShape t;
+  if (!grkan::fused::pick_shape(N, N / n_groups, &t)) return 0;
+  const int64_t ppg = ((M + grkan::fused::kBM - 1) / grkan::fused::kBM) * ((N / n_groups) / (t.bn / t.es)) * 4;
+  const size_t part = static_cast<size_t>(n_groups) * grkan::fused::kKC * ppg * sizeof(float);
   return 256 + ((part + 255) / 256) * 256;
 }
 
@@ -359,9 +429,8 @@ int grkan_linear_bwd(const void* dy, const void* w, const void* x, const void* a
   if (flags & ~GRKAN_FLAG_FAST)
     return grkan::set_error(GRKAN_ERR_UNSUPPORTED, "fused linear backward: FAST policy only");
   const int dg = N / n_groups;
-  int atom = 0;
-  const int bn = pick_bn(dg, &atom);
-  if (!bn || K % kBK) {
+  TileShape ts;
+  if (!pick_shape(N, dg, &ts) || K % kBK) {
     snprintf(msg, sizeof msg, "fused linear backward needs group width %% 32 == 0 and K %% 64 == 0 (dg=%d, K=%d)", dg, K);
     return grkan::set_error(GRKAN_ERR_UNSUPPORTED, msg);
   }
@@ -382,8 +451,8 @@ int grkan_linear_bwd(const void* dy, const void* w, const void* x, const void* a
   }
   CUtensorMap mdy, mw;
   if (!make_map(&mdy, dy, static_cast<uint64_t>(K), static_cast<uint64_t>(M), kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_map(&mw, w, static_cast<uint64_t>(N), static_cast<uint64_t>(K), atom, kBK,
-                atom == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B))
+      !make_map(&mw, w, static_cast<uint64_t>(N), static_cast<uint64_t>(K), ts.atom, kBK,
+                ts.atom == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B))
     return grkan::set_error(GRKAN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   FusedGeom geo;
   geo.M = M;
@@ -391,26 +460,31 @@ int grkan_linear_bwd(const void* dy, const void* w, const void* x, const void* a
   geo.K = K;
   geo.ng = n_groups;
   geo.dg = dg;
-  geo.n_tiles_n = N / bn;
+  geo.n_tiles_n = N / ts.bn;
   const int64_t m_tiles = (M + kBM - 1) / kBM;
-  geo.tiles_pg = static_cast<int32_t>(m_tiles * (dg / bn));
+  geo.ppg = static_cast<int32_t>(m_tiles * (dg / (ts.bn / ts.es)) * 4);
   geo.one = 1.0f;
-  const int64_t ctas = m_tiles * geo.n_tiles_n;
+  const int64_t tiles = m_tiles * geo.n_tiles_n;
   float* part = reinterpret_cast<float*>(static_cast<char*>(ws) + 256);
   const float* fa = static_cast<const float*>(a);
   const float* fb = static_cast<const float*>(b);
-  switch (bn) {
-    case 256: e = launch_t<256, 64>(mdy, mw, x, dx, fa, fb, part, geo, ctas, s); break;
-    case 192: e = launch_t<192, 64>(mdy, mw, x, dx, fa, fb, part, geo, ctas, s); break;
-    case 128: e = launch_t<128, 64>(mdy, mw, x, dx, fa, fb, part, geo, ctas, s); break;
-    case 64: e = launch_t<64, 64>(mdy, mw, x, dx, fa, fb, part, geo, ctas, s); break;
-    case 224: e = launch_t<224, 32>(mdy, mw, x, dx, fa, fb, part, geo, ctas, s); break;
-    case 160: e = launch_t<160, 32>(mdy, mw, x, dx, fa, fb, part, geo, ctas, s); break;
-    case 96: e = launch_t<96, 32>(mdy, mw, x, dx, fa, fb, part, geo, ctas, s); break;
-    default: e = launch_t<32, 32>(mdy, mw, x, dx, fa, fb, part, geo, ctas, s); break;
-  }
+#define GRKAN_FUSED_CASE(BN_, AT_, ES_, CH_)                                                  \
+  if (ts.bn == BN_ && ts.atom == AT_ && ts.es == ES_ && ts.ch == CH_)                          \
+    e = launch_t<BN_, AT_, ES_, CH_>(mdy, mw, x, dx, fa, fb, part, geo, tiles, s);            \
+  else
+  GRKAN_FUSED_CASE(256, 64, 4, 16)
+  GRKAN_FUSED_CASE(192, 64, 4, 16)
+  GRKAN_FUSED_CASE(256, 64, 2, 32)
+  GRKAN_FUSED_CASE(192, 64, 2, 32)
+  GRKAN_FUSED_CASE(128, 64, 4, 16)
+  GRKAN_FUSED_CASE(128, 64, 2, 32)
+  GRKAN_FUSED_CASE(96, 32, 1, 32)
+  GRKAN_FUSED_CASE(64, 64, 2, 32)
+  GRKAN_FUSED_CASE(64, 64, 1, 32)
+  e = launch_t<32, 32, 1, 32>(mdy, mw, x, dx, fa, fb, part, geo, tiles, s);
+#undef GRKAN_FUSED_CASE
   if (e != cudaSuccess) return grkan::set_error(GRKAN_ERR_CUDA, cudaGetErrorString(e));
-  e = grkan::launch_reduce_f32(part, geo.tiles_pg, 1, n_groups, 6, 4, da, db, st, s);
+  e = grkan::launch_reduce_f32(part, geo.ppg, 1, n_groups, 6, 4, da, db, st, s);
   if (e != cudaSuccess) return grkan::set_error(GRKAN_ERR_CUDA, cudaGetErrorString(e));
   return GRKAN_OK;
 }
