@@ -50,6 +50,7 @@ constexpr int kBM = 128;          // tile rows (UMMA M, TMEM lanes)
 constexpr int kBK = 64;           // K per stage (one 128-byte swizzle row of bf16)
 constexpr int kSmemBudget = 200 * 1024;  // operand ring (the rest: alignment + barriers)
 constexpr int kKC = 10;           // coefficient terms (degrees (5, 4))
+constexpr int kMaxGroups = 64;    // coefficient table in shared memory
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(
@@ -143,10 +144,13 @@ struct FusedGeom {
 // n0..n0+BN-1) is loaded as BN / ATOM boxes of ATOM columns x 64 rows; ATOM =
 // 64 (128B swizzle) or 32 (64B swizzle).  ES epilogue warps per TMEM lane
 // quadrant split the tile's columns (4 * ES epilogue warps in all).
-template <int BN, int ATOM, int ES, int CH, int kStages>
+// XS: the producer also TMA-streams each tile's X block [128 x BN] (64-column
+// 128B-swizzled boxes) into a double-buffered smem tile, so the epilogue reads
+// X with conflict-free LDS.128 instead of waiting on global loads.
+template <int BN, int ATOM, int ES, int CH, bool XS, int kStages>
 __global__ void __launch_bounds__(64 + 128 * ES, 1)
     k_linear_bwd_fused(const __grid_constant__ CUtensorMap map_dy, const __grid_constant__ CUtensorMap map_w,
-                       const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ dx,
+                       const __grid_constant__ CUtensorMap map_x, const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ dx,
                        const float* __restrict__ ca, const float* __restrict__ cb, float* __restrict__ part,
                        FusedGeom geo) {
   constexpr int A_BYTES = kBM * kBK * 2;            // 16 KB
@@ -160,11 +164,16 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
   constexpr int CW = BN / ES;                       // columns per epilogue warp
   static_assert(CW % CH == 0, "epilogue columns come in CH-column TMEM loads");
   constexpr int NV = CH / 8;                        // 16-byte X / dX vectors per chunk
+  constexpr int XBOX = kBM * 64 * 2;                // one 64-column X box (16 KB)
+  constexpr int XBYTES = XS ? BN * kBM * 2 : 0;     // one X tile buffer
+  static_assert(!XS || BN % 64 == 0, "X staging uses 64-column boxes");
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
+  __shared__ uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], xfull[2], xempty[2];
   __shared__ uint32_t tmem_base;
+  __shared__ float scoef[kMaxGroups * kKC];  // every group's a (6) || b (4)
+  unsigned char* const xs = smem + kStages * STAGE;  // X tile buffers (XS)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_tiles = ((geo.M + kBM - 1) / kBM) * geo.n_tiles_n;
@@ -178,6 +187,8 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], NE);
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], NE);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -186,6 +197,10 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
                  "n"(TMEM_COLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  for (int t = threadIdx.x; t < geo.ng * kKC; t += blockDim.x) {
+    const int g = t / kKC, k = t - g * kKC;
+    scoef[t] = k < 6 ? ca[g * 6 + k] : cb[g * 4 + (k - 6)];
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -199,9 +214,17 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
       int slot = 0;
       uint32_t phase = 0;
       int64_t it = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      int i = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++i) {
         const int n0 = static_cast<int>(tile % geo.n_tiles_n) * BN;
         const int m0 = static_cast<int>((tile / geo.n_tiles_n) * kBM);
+        if constexpr (XS) {  // the tile's X block, into buffer i & 1
+          const int xb = i & 1;
+          mbar_wait(&xempty[xb], ((i >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&xfull[xb], XBYTES);
+#pragma unroll
+          for (int a = 0; a < BN / 64; ++a) tma_load_2d(xs + xb * XBYTES + a * XBOX, &map_x, n0 + a * 64, m0, &xfull[xb]);
+        }
         for (int kb = 0; kb < kblocks; ++kb, ++it) {
           if (it >= kStages) mbar_wait(&empty[slot], phase ^ 1);
           unsigned char* sa = smem + slot * STAGE;
@@ -268,28 +291,42 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
       const int c0 = n0 + cs * CW;
       const int g = c0 / geo.dg;
       if (g != g_loaded) {
-        rp.load(ca, cb, g, geo.one);
+        rp.load_row(scoef + g * kKC, geo.one);
         g_loaded = g;
       }
       const __nv_bfloat16* xrow = x + grow * geo.N + c0;
       __nv_bfloat16* dxrow = dx + grow * geo.N + c0;
       // X for the first 32 columns is independent of the MMA: fetch it first
       uint4 xr[2][NV];
-      if (live) {
+      if (!XS && live) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) xr[0][v] = __ldcs(reinterpret_cast<const uint4*>(xrow) + v);
       }
-      float2 acc2[kKC];
+      const unsigned char* xtile = xs + acc * XBYTES;
+      if constexpr (XS) mbar_wait(&xfull[acc], (i >> 1) & 1);
+      float sacc[kKC];  // scalar accumulators: register budget of 16 epilogue warps
 #pragma unroll
-      for (int k = 0; k < kKC; ++k) acc2[k] = make_float2(0.f, 0.f);
+      for (int k = 0; k < kKC; ++k) sacc[k] = 0.f;
       mbar_wait(&tfull[acc], (i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t taddr = tmem_d + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + cs * CW);
 #pragma unroll
       for (int c = 0; c < CW / CH; ++c) {
-        if (live && c + 1 < CW / CH) {
+        if (!XS && live && c + 1 < CW / CH) {
 #pragma unroll
           for (int v = 0; v < NV; ++v) xr[(c + 1) & 1][v] = __ldcs(reinterpret_cast<const uint4*>(xrow + (c + 1) * CH) + v);
+        }
+        if constexpr (XS) {  // 128B-swizzled box: 16-byte chunk j of row r sits at (j ^ (r & 7))
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const int col = cs * CW + c * CH + v * 8;
+            const int j = (col & 63) >> 3;
+            xr[c & 1][v] = *reinterpret_cast<const uint4*>(xtile + (col >> 6) * XBOX + row * 128 + ((j ^ (row & 7)) << 4));
+          }
+          if (c + 1 == CW / CH) {  // done with this X buffer
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&xempty[acc]);
+          }
         }
         float u[CH];
         tmem_ld<CH>(taddr + c * CH, u);  // warp-collective: every lane participates
@@ -306,7 +343,7 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
             Raw16<__nv_bfloat16>::unpack(xr[c & 1][v], xv);
 #pragma unroll
             for (int k = 0; k < 8; ++k) uv[k] = u[v * 8 + k];
-            rp.template grad_n<4, false>(xv, uv, o, acc2);
+            rp.template grad_n<4, false, float>(xv, uv, o, sacc);
             o4[v] = Raw16<__nv_bfloat16>::pack(o);
           }
 #pragma unroll
@@ -317,7 +354,7 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
       const int64_t t = (m_tile * (geo.dg / CW) + (c0 % geo.dg) / CW) * 4 + q;
 #pragma unroll
       for (int k = 0; k < kKC; ++k) {
-        float v = acc2[k].x + acc2[k].y;
+        float v = sacc[k];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0) part[(static_cast<int64_t>(g) * kKC + k) * geo.ppg + t] = v;
@@ -363,15 +400,25 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, 
 // column block CW = BN / ES lies inside one group (CW divides the group width).
 // ES = 4 (16 epilogue warps, 576 threads) uses 16-column TMEM loads to fit
 // the 112-register budget; ES <= 2 loads 32 columns at a time.
+// xs: X staged through shared memory (chosen when the epilogue dominates,
+// i.e. small K: it costs ring stages the MMA needs at large K).
 struct TileShape {
   int bn, atom, es, ch;
+  bool xs;
 };
-constexpr TileShape kShapes[] = {{256, 64, 4, 16}, {192, 64, 4, 16}, {256, 64, 2, 32}, {192, 64, 2, 32},
-                                 {128, 64, 4, 16}, {128, 64, 2, 32}, {96, 32, 1, 32}, {64, 64, 2, 32},
-                                 {64, 64, 1, 32},  {32, 32, 1, 32}};
+constexpr TileShape kShapesLongK[] = {{256, 64, 4, 16, false}, {192, 64, 4, 16, false}, {256, 64, 2, 32, false},
+                                      {192, 64, 2, 32, false}, {128, 64, 4, 16, false}, {128, 64, 2, 32, false},
+                                      {96, 32, 1, 32, false},  {64, 64, 2, 32, false},  {64, 64, 1, 32, false},
+                                      {32, 32, 1, 32, false}};
+constexpr TileShape kShapesShortK[] = {{128, 64, 4, 16, true}, {64, 64, 2, 32, true}, {96, 32, 1, 32, false},
+                                       {32, 32, 1, 32, false}};
 
-bool pick_shape(int N, int dg, TileShape* out) {
-  for (const TileShape& t : kShapes) {
+bool pick_shape(int N, int dg, int K, TileShape* out) {
+  const bool short_k = K <= 1024;
+  const TileShape* list = short_k ? kShapesShortK : kShapesLongK;
+  const int n = short_k ? 4 : 10;
+  for (int i = 0; i < n; ++i) {
+    const TileShape& t = list[i];
     const int cw = t.bn / t.es;
     if (N % t.bn == 0 && cw % t.ch == 0 && cw % 16 == 0 && dg % cw == 0) {
       *out = t;
@@ -387,17 +434,21 @@ int sms_of_device() {
   return v > 0 ? v : 148;
 }
 
-template <int BN, int ATOM, int ES, int CH>
-cudaError_t launch_t(const CUtensorMap& mdy, const CUtensorMap& mw, const void* x, void* dx, const float* a,
-                     const float* b, float* part, const FusedGeom& geo, int64_t tiles, cudaStream_t s) {
+template <int BN, int ATOM, int ES, int CH, bool XS>
+cudaError_t launch_t(const CUtensorMap& mdy, const CUtensorMap& mw, const CUtensorMap& mx, const void* x, void* dx,
+                     const float* a, const float* b, float* part, const FusedGeom& geo, int64_t tiles,
+                     cudaStream_t s) {
   constexpr int kStageBytes = kBM * kBK * 2 + kBK * BN * 2;
-  constexpr int kSt = kSmemBudget / kStageBytes > 8 ? 8 : kSmemBudget / kStageBytes;
-  constexpr size_t smem = static_cast<size_t>(kSt) * kStageBytes + 1024;
-  auto kern = k_linear_bwd_fused<BN, ATOM, ES, CH, kSt>;
+  constexpr int kXBytes = XS ? 2 * BN * kBM * 2 : 0;
+  constexpr int kRing = kSmemBudget - kXBytes;
+  constexpr int kSt = kRing / kStageBytes > 8 ? 8 : kRing / kStageBytes;
+  static_assert(kSt >= 2, "operand ring needs two stages");
+  constexpr size_t smem = static_cast<size_t>(kSt) * kStageBytes + kXBytes + 1024;
+  auto kern = k_linear_bwd_fused<BN, ATOM, ES, CH, XS, kSt>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int64_t grid = tiles < sms_of_device() ? tiles : sms_of_device();
-  kern<<<static_cast<unsigned>(grid), 64 + 128 * ES, smem, s>>>(mdy, mw, static_cast<const __nv_bfloat16*>(x),
+  kern<<<static_cast<unsigned>(grid), 64 + 128 * ES, smem, s>>>(mdy, mw, mx, static_cast<const __nv_bfloat16*>(x),
                                                                  static_cast<__nv_bfloat16*>(dx), a, b, part, geo);
   return cudaGetLastError();
 }
@@ -410,7 +461,7 @@ extern "C" {
 size_t grkan_linear_bwd_workspace_bytes(int64_t M, int32_t N, int32_t K, int32_t n_groups) {
   if (M < 0 || N < 1 || K < 1 || n_groups < 1 || N % n_groups) return 0;
   grkan::fused::TileShape t;
-  if (!grkan::fused::pick_shape(N, N / n_groups, &t)) return 0;
+  if (!grkan::fused::pick_shape(N, N / n_groups, K, &t)) return 0;
   const int64_t ppg = ((M + grkan::fused::kBM - 1) / grkan::fused::kBM) * ((N / n_groups) / (t.bn / t.es)) * 4;
   const size_t part = static_cast<size_t>(n_groups) * grkan::fused::kKC * ppg * sizeof(float);
   return 256 + ((part + 255) / 256) * 256;
@@ -430,8 +481,10 @@ int grkan_linear_bwd(const void* dy, const void* w, const void* x, const void* a
     return grkan::set_error(GRKAN_ERR_UNSUPPORTED, "fused linear backward: FAST policy only");
   const int dg = N / n_groups;
   TileShape ts;
-  if (!pick_shape(N, dg, &ts) || K % kBK) {
-    snprintf(msg, sizeof msg, "fused linear backward needs group width %% 32 == 0 and K %% 64 == 0 (dg=%d, K=%d)", dg, K);
+  if (!pick_shape(N, dg, K, &ts) || K % kBK || n_groups > kMaxGroups) {
+    snprintf(msg, sizeof msg,
+             "fused linear backward needs group width %% 32 == 0, K %% 64 == 0, groups <= %d (dg=%d, K=%d, groups=%d)",
+             kMaxGroups, dg, K, n_groups);
     return grkan::set_error(GRKAN_ERR_UNSUPPORTED, msg);
   }
   if (!ws || !da || !db || !dx || !dy || !w || !x || !a || !b)
@@ -449,10 +502,11 @@ int grkan_linear_bwd(const void* dy, const void* w, const void* x, const void* a
     if (e == cudaSuccess) e = cudaMemsetAsync(db, 0, static_cast<size_t>(n_groups) * 4 * 4, s);
     return e == cudaSuccess ? GRKAN_OK : grkan::set_error(GRKAN_ERR_CUDA, cudaGetErrorString(e));
   }
-  CUtensorMap mdy, mw;
+  CUtensorMap mdy, mw, mx;
   if (!make_map(&mdy, dy, static_cast<uint64_t>(K), static_cast<uint64_t>(M), kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&mw, w, static_cast<uint64_t>(N), static_cast<uint64_t>(K), ts.atom, kBK,
-                ts.atom == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B))
+                ts.atom == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B) ||
+      !make_map(&mx, x, static_cast<uint64_t>(N), static_cast<uint64_t>(M), 64, kBM, CU_TENSOR_MAP_SWIZZLE_128B))
     return grkan::set_error(GRKAN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   FusedGeom geo;
   geo.M = M;
@@ -468,20 +522,22 @@ int grkan_linear_bwd(const void* dy, const void* w, const void* x, const void* a
   float* part = reinterpret_cast<float*>(static_cast<char*>(ws) + 256);
   const float* fa = static_cast<const float*>(a);
   const float* fb = static_cast<const float*>(b);
-#define GRKAN_FUSED_CASE(BN_, AT_, ES_, CH_)                                                  \
-  if (ts.bn == BN_ && ts.atom == AT_ && ts.es == ES_ && ts.ch == CH_)                          \
-    e = launch_t<BN_, AT_, ES_, CH_>(mdy, mw, x, dx, fa, fb, part, geo, tiles, s);            \
+#define GRKAN_FUSED_CASE(BN_, AT_, ES_, CH_, XS_)                                             \
+  if (ts.bn == BN_ && ts.atom == AT_ && ts.es == ES_ && ts.ch == CH_ && ts.xs == XS_)           \
+    e = launch_t<BN_, AT_, ES_, CH_, XS_>(mdy, mw, mx, x, dx, fa, fb, part, geo, tiles, s);    \
   else
-  GRKAN_FUSED_CASE(256, 64, 4, 16)
-  GRKAN_FUSED_CASE(192, 64, 4, 16)
-  GRKAN_FUSED_CASE(256, 64, 2, 32)
-  GRKAN_FUSED_CASE(192, 64, 2, 32)
-  GRKAN_FUSED_CASE(128, 64, 4, 16)
-  GRKAN_FUSED_CASE(128, 64, 2, 32)
-  GRKAN_FUSED_CASE(96, 32, 1, 32)
-  GRKAN_FUSED_CASE(64, 64, 2, 32)
-  GRKAN_FUSED_CASE(64, 64, 1, 32)
-  e = launch_t<32, 32, 1, 32>(mdy, mw, x, dx, fa, fb, part, geo, tiles, s);
+  GRKAN_FUSED_CASE(256, 64, 4, 16, false)
+  GRKAN_FUSED_CASE(192, 64, 4, 16, false)
+  GRKAN_FUSED_CASE(256, 64, 2, 32, false)
+  GRKAN_FUSED_CASE(192, 64, 2, 32, false)
+  GRKAN_FUSED_CASE(128, 64, 4, 16, false)
+  GRKAN_FUSED_CASE(128, 64, 2, 32, false)
+  GRKAN_FUSED_CASE(96, 32, 1, 32, false)
+  GRKAN_FUSED_CASE(64, 64, 2, 32, false)
+  GRKAN_FUSED_CASE(64, 64, 1, 32, false)
+  GRKAN_FUSED_CASE(128, 64, 4, 16, true)
+  GRKAN_FUSED_CASE(64, 64, 2, 32, true)
+  e = launch_t<32, 32, 1, 32, false>(mdy, mw, mx, x, dx, fa, fb, part, geo, tiles, s);
 #undef GRKAN_FUSED_CASE
   if (e != cudaSuccess) return grkan::set_error(GRKAN_ERR_CUDA, cudaGetErrorString(e));
   e = grkan::launch_reduce_f32(part, geo.ppg, 1, n_groups, 6, 4, da, db, st, s);

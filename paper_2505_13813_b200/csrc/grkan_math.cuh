@@ -259,10 +259,25 @@ struct RationalX2 {
 
   __device__ __forceinline__ void load(const float* __restrict__ ga, const float* __restrict__ gb, int g,
                                        float one_param) {
+    float ab[10];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) a[k] = __ldg(ga + g * 6 + k);
+    for (int k = 0; k < 6; ++k) ab[k] = __ldg(ga + g * 6 + k);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) b[k] = __ldg(gb + g * 4 + k);
+    for (int k = 0; k < 4; ++k) ab[6 + k] = __ldg(gb + g * 4 + k);
+    set(ab, one_param);
+  }
+  // From one row a_0..a_5 || b_1..b_4 in any memory space (shared-memory tables).
+  __device__ __forceinline__ void load_row(const float* ab_row, float one_param) {
+    float ab[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) ab[k] = ab_row[k];
+    set(ab, one_param);
+  }
+  __device__ __forceinline__ void set(const float (&ab)[10], float one_param) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) a[k] = ab[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) b[k] = ab[6 + k];
     da[0] = a[1];  // 1 * a_1 is exact
 #pragma unroll
     for (int k = 2; k < 6; ++k) da[k - 1] = __fmul_rn(a[k], float(k));  // fp32 k*a_k, as rational.py:207
@@ -350,8 +365,17 @@ struct RationalX2 {
   __device__ __forceinline__ float2 series_ref(float2 x) const { return mul2(horner2<true, 4>(b, x), x); }
 
   // dx and the ten coefficient terms of one pair, given A(x) = s.
+  // Accumulators: float2 per coefficient (packed FFMA2, the streaming kernels)
+  // or one float per coefficient (two scalar FFMAs per pair: the same FMA-pipe
+  // cycles, half the registers -- the fused GEMM epilogue).
+  static __device__ __forceinline__ void acc_add(float2& a, float2 t) { a = add2(a, t); }
+  static __device__ __forceinline__ void acc_add(float& a, float2 t) { a = (a + t.x) + t.y; }
+  static __device__ __forceinline__ void acc_fma(float2& a, float2 t, float2 p) { a = fma2(t, p, a); }
+  static __device__ __forceinline__ void acc_fma(float& a, float2 t, float2 p) { a = fmaf(t.y, p.y, fmaf(t.x, p.x, a)); }
+
+  template <typename ACC>
   __device__ __forceinline__ float2 grad_given(float2 x, float2 u, float2 s, float2 x2, float2 x3,
-                                               float2 (&acc)[KC]) const {
+                                               ACC (&acc)[KC]) const {
     const float2 p = horner2<EXACT, 6>(a, x);
     const float2 iq = make_float2(rcp(__fadd_rn(1.0f, fabsf(s.x))), rcp(__fadd_rn(1.0f, fabsf(s.y))));
     const float2 dp = horner2<EXACT, 5>(da, x);
@@ -367,18 +391,18 @@ struct RationalX2 {
       const float2 t2 = mul2(mul2(mul2(sg, ds), pq), iq);
       dx = mul2(u, xsub2(t1, t2, one));
       float2 t = mul2(u, iq);
-      acc[0] = add2(acc[0], t);
+      acc_add(acc[0], t);
 #pragma unroll
       for (int i = 1; i < 6; ++i) {
         t = mul2(t, x);
-        acc[i] = add2(acc[i], t);
+        acc_add(acc[i], t);
       }
       float2 v = mul2(mul2(mul2(neg2(mul2(sg, u)), pq), iq), x);
-      acc[6] = add2(acc[6], v);
+      acc_add(acc[6], v);
 #pragma unroll
       for (int j = 1; j < 4; ++j) {
         v = mul2(v, x);
-        acc[6 + j] = add2(acc[6 + j], v);
+        acc_add(acc[6 + j], v);
       }
     } else {
       const float2 t0 = mul2(u, iq);
@@ -388,16 +412,16 @@ struct RationalX2 {
       const float2 w = mul2(t0, z);                 // -(sign(A) u/q) P/q
       const float2 x4 = mul2(x2, x2);
       const float2 x5 = mul2(x4, x);
-      acc[0] = add2(acc[0], t0);
-      acc[1] = fma2(t0, x, acc[1]);
-      acc[2] = fma2(t0, x2, acc[2]);
-      acc[3] = fma2(t0, x3, acc[3]);
-      acc[4] = fma2(t0, x4, acc[4]);
-      acc[5] = fma2(t0, x5, acc[5]);
-      acc[6] = fma2(w, x, acc[6]);
-      acc[7] = fma2(w, x2, acc[7]);
-      acc[8] = fma2(w, x3, acc[8]);
-      acc[9] = fma2(w, x4, acc[9]);
+      acc_add(acc[0], t0);
+      acc_fma(acc[1], t0, x);
+      acc_fma(acc[2], t0, x2);
+      acc_fma(acc[3], t0, x3);
+      acc_fma(acc[4], t0, x4);
+      acc_fma(acc[5], t0, x5);
+      acc_fma(acc[6], w, x);
+      acc_fma(acc[7], w, x2);
+      acc_fma(acc[8], w, x3);
+      acc_fma(acc[9], w, x4);
     }
     return dx;
   }
@@ -412,9 +436,9 @@ struct RationalX2 {
   // backward is latency-bound and loses more to the guard's branches than it
   // gains from 3 fewer FMUL2 per pair (fp32: 323 -> 307 us with the guard,
   // bf16: 260 -> 273 us at KAT-B; 283 us with a warp-uniform __any_sync branch).
-  template <int NP, bool GUARD = true>
+  template <int NP, bool GUARD = true, typename ACC = float2>
   __device__ __forceinline__ void grad_n(const float (&vx)[2 * NP], const float (&vu)[2 * NP],
-                                         float (&o)[2 * NP], float2 (&acc)[KC]) const {
+                                         float (&o)[2 * NP], ACC (&acc)[KC]) const {
     constexpr int G = GRKAN_GUARD_NP < NP ? GRKAN_GUARD_NP : NP;
     static_assert(NP % G == 0, "guard group must divide the pair count");
 #pragma unroll
