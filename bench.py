@@ -67,6 +67,8 @@ def parse_args(argv=None):
     p.add_argument("--cpu-sample-batch", type=int, default=16)
     p.add_argument("--cpu-passes", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--fused-mlp", action="store_true",
+                   help="*-train configs: GR-KAN rational->Linear pairs with the fused tcgen05 backward")
     p.add_argument("--dist-backend", default="nccl",
                    help="torch.distributed backend for N > 1 (gloo only to exercise the multi-rank "
                         "code path when several ranks share one GPU)")
@@ -461,7 +463,7 @@ def run_train(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     torch.manual_seed(1234 + rank)
-    model = getattr(kat, TRAIN_CONFIGS[args.config])().to(dev)
+    model = getattr(kat, TRAIN_CONFIGS[args.config])(fused_mlp=args.fused_mlp).to(dev)
     if world > 1:
         model = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local_rank])
     opt = torch.optim.AdamW(model.parameters(), lr=1e-4, weight_decay=0.05, fused=True)
@@ -506,7 +508,8 @@ def run_train(args, rank, world, local_rank):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic images N(0,1), random labels",
             "config": {"workload": args.config, "model": TRAIN_CONFIGS[args.config], "params": n_params,
-                       "batch_per_gpu": B, "global_batch": B * world, "parallelism": "ddp%d" % world},
+                       "batch_per_gpu": B, "global_batch": B * world, "parallelism": "ddp%d" % world,
+                       "fused_mlp": bool(args.fused_mlp)},
             "final_loss": float(loss.item()), "clocks": sampler.summary(),
             "paper_h200_images_s": {"kat_b": 1801.75, "kat_s": 3741.91, "kat_t": 6317.90}[TRAIN_CONFIGS[args.config]],
         }), flush=True)

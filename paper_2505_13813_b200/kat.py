@@ -20,24 +20,36 @@ import torch
 import torch.nn.functional as F
 from torch import nn
 
-from .module import GroupRational
+from .module import GroupRational, GroupRationalLinearFn, fused_layer_supported
 
 
 class GRKAN(nn.Module):
-    """GR-KAN MLP: rational(identity) -> Linear -> rational(swish) -> Linear."""
+    """GR-KAN MLP: rational(identity) -> Linear -> rational(swish) -> Linear.
 
-    def __init__(self, dim: int, hidden: int, groups: int = 8, drop: float = 0.0):
+    ``fused=True`` runs each rational -> Linear pair through
+    GroupRationalLinearFn (fused tcgen05 backward) whenever the
+    activations qualify (bf16 under autocast, supported shape); otherwise the
+    two modules run one after the other.
+    """
+
+    def __init__(self, dim: int, hidden: int, groups: int = 8, drop: float = 0.0, fused: bool = False):
         super().__init__()
         self.act1 = GroupRational(groups, init="identity")
         self.fc1 = nn.Linear(dim, hidden)
         self.act2 = GroupRational(groups, init="swish")
         self.fc2 = nn.Linear(hidden, dim)
         self.drop = nn.Dropout(drop)
+        self.fused = fused
+
+    def _layer(self, x, act, fc):
+        if self.fused and (self.drop.p == 0.0 or not self.training):
+            xd = x.to(torch.bfloat16) if torch.is_autocast_enabled() and x.is_cuda else x
+            if fused_layer_supported(xd, act, fc):
+                return GroupRationalLinearFn.apply(xd, act.a, act.b, fc.weight, fc.bias)
+        return fc(self.drop(act(x)))
 
     def forward(self, x):
-        x = self.fc1(self.drop(self.act1(x)))
-        x = self.fc2(self.drop(self.act2(x)))
-        return x
+        return self._layer(self._layer(x, self.act1, self.fc1), self.act2, self.fc2)
 
 
 class Attention(nn.Module):
@@ -55,12 +67,12 @@ class Attention(nn.Module):
 
 
 class Block(nn.Module):
-    def __init__(self, dim: int, heads: int, mlp_ratio: float = 4.0, groups: int = 8):
+    def __init__(self, dim: int, heads: int, mlp_ratio: float = 4.0, groups: int = 8, fused: bool = False):
         super().__init__()
         self.norm1 = nn.LayerNorm(dim, eps=1e-6)
         self.attn = Attention(dim, heads)
         self.norm2 = nn.LayerNorm(dim, eps=1e-6)
-        self.mlp = GRKAN(dim, int(dim * mlp_ratio), groups)
+        self.mlp = GRKAN(dim, int(dim * mlp_ratio), groups, fused=fused)
 
     def forward(self, x):
         x = x + self.attn(self.norm1(x))
@@ -69,13 +81,13 @@ class Block(nn.Module):
 
 class KAT(nn.Module):
     def __init__(self, img: int = 224, patch: int = 16, dim: int = 768, depth: int = 12, heads: int = 12,
-                 classes: int = 1000, groups: int = 8):
+                 classes: int = 1000, groups: int = 8, fused_mlp: bool = False):
         super().__init__()
         self.patch = nn.Conv2d(3, dim, patch, patch)
         n = (img // patch) ** 2
         self.cls = nn.Parameter(torch.zeros(1, 1, dim))
         self.pos = nn.Parameter(torch.randn(1, n + 1, dim) * 0.02)
-        self.blocks = nn.ModuleList([Block(dim, heads, 4.0, groups) for _ in range(depth)])
+        self.blocks = nn.ModuleList([Block(dim, heads, 4.0, groups, fused=fused_mlp) for _ in range(depth)])
         self.norm = nn.LayerNorm(dim, eps=1e-6)
         self.head = nn.Linear(dim, classes)
         init_variance_preserving(self)

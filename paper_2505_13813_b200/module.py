@@ -70,3 +70,45 @@ class GroupRational(nn.Module):
     def extra_repr(self) -> str:
         return "num_groups=%d, init=%s, degrees=%s, exact=%s" % (
             self.num_groups, self.init, self.degrees, self.exact)
+
+
+class GroupRationalLinearFn(torch.autograd.Function):
+    """y = R(x) W^T + bias -- a GR-KAN layer -- with the fused tcgen05 backward.
+
+    Forward runs the rational kernel and cuBLAS; backward computes
+    (dx, da, db) in ONE kernel (ops.linear_backward_fused: dy.W on the tensor
+    cores, the rational backward in its epilogue, dF never stored) and
+    dW = dy^T R(x), dbias = sum(dy) with cuBLAS.  bf16 activations (autocast)
+    with fp32 coefficients, degrees (5, 4); see ops.linear_backward_fused for
+    the supported shapes.  Reference: layer_forward / layer_backward
+    (pkg/src/grkan/layer.py:318-379).
+    """
+
+    @staticmethod
+    def forward(ctx, x, a, b, weight, bias):
+        w = weight.to(x.dtype)
+        f = torch.ops.grkan_b200.rational_fwd(x, a, b, False)
+        y = torch.nn.functional.linear(f, w, None if bias is None else bias.to(x.dtype))
+        ctx.save_for_backward(x, a, b, w, f)
+        ctx.has_bias = bias is not None
+        ctx.weight_dtype = weight.dtype
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, a, b, w, f = ctx.saved_tensors
+        dy = dy.contiguous()
+        dx, da, db = ops.linear_backward_fused(dy, w, x, a, b)
+        dy2 = dy.reshape(-1, dy.shape[-1])
+        dw = (dy2.t() @ f.reshape(-1, f.shape[-1])).to(ctx.weight_dtype)
+        dbias = dy2.sum(0).to(ctx.weight_dtype) if ctx.has_bias else None
+        return dx, da, db, dw, dbias
+
+
+def fused_layer_supported(x: torch.Tensor, act: "GroupRational", fc: nn.Linear) -> bool:
+    """The fused backward's contract: bf16 CUDA activations, degrees (5, 4), fp32 coefficients,
+    K % 64 == 0, group width a multiple of 32, at most 64 groups."""
+    n, k = fc.in_features, fc.out_features
+    return (x.is_cuda and x.dtype == torch.bfloat16 and act.degrees == (5, 4) and act.a.dtype == torch.float32
+            and k % 64 == 0 and n % act.num_groups == 0 and (n // act.num_groups) % 32 == 0
+            and act.num_groups <= 64)

@@ -72,3 +72,46 @@ def test_fused_is_deterministic_and_rejects_bad_shapes():
     with pytest.raises(GrkanError):  # group width 40 (not a multiple of 32)
         x2, dy2, w2, a2, b2 = _inputs(128, 80, 64, 2, seed=4)
         ops.linear_backward_fused(dy2, w2, x2, a2, b2)
+
+
+def test_fused_grkan_layer_matches_unfused_in_a_kat_block():
+    """GroupRationalLinearFn (fused backward) vs the module-by-module GR-KAN MLP, bf16 autocast."""
+    from paper_2505_13813_b200 import kat
+    torch.manual_seed(5)
+    ref = kat.GRKAN(256, 1024, 8).to(DEV)
+    fus = kat.GRKAN(256, 1024, 8, fused=True).to(DEV)
+    fus.load_state_dict(ref.state_dict())
+    with torch.no_grad():  # non-trivial coefficients for both rationals
+        for m in (ref, fus):
+            m.act1.b.copy_(torch.linspace(-0.3, 0.3, 32, device=DEV).reshape(8, 4))
+    x = torch.randn(4, 50, 256, device=DEV).to(torch.bfloat16)  # both paths see the same bf16 input
+    outs = []
+    for m in (ref, fus):
+        xi = x.clone().requires_grad_(True)
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            y = m(xi)
+        y.float().square().mean().backward()
+        outs.append((y.float(), xi.grad.float(), [p.grad.float() for p in m.parameters()]))
+    (y0, g0, p0), (y1, g1, p1) = outs
+    assert orc.matrix_rel(y1.detach().cpu().numpy(), y0.detach().cpu().numpy()) <= 2e-2
+    assert orc.matrix_rel(g1.cpu().numpy(), g0.cpu().numpy()) <= 3e-2
+    for a, b in zip(p1, p0):
+        assert orc.matrix_rel(a.cpu().numpy(), b.cpu().numpy()) <= 3e-2
+
+
+def test_kat_training_with_fused_mlp():
+    from paper_2505_13813_b200 import kat
+    torch.manual_seed(7)
+    model = kat.KAT(img=32, patch=8, dim=256, depth=2, heads=4, classes=10, fused_mlp=True).to(DEV)
+    imgs = torch.randn(16, 3, 32, 32, device=DEV)
+    labels = torch.randint(0, 10, (16,), device=DEV)
+    opt = torch.optim.AdamW(model.parameters(), lr=1e-3)
+    losses = []
+    for _ in range(40):
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = torch.nn.functional.cross_entropy(model(imgs), labels)
+        loss.backward()
+        opt.step()
+        opt.zero_grad(set_to_none=True)
+        losses.append(loss.item())
+    assert losses[-1] < 0.2 * losses[0]
