@@ -113,3 +113,36 @@ def test_kat_b_plan_is_persistent_and_balanced():
     assert p["vector_width"] == 4 and p["staged"] and p["threads"] == 288
     assert p["rows_per_unit"] == 8  # 8 rows x 96 float4 = 768 vectors per stage
     assert p["ctas"] == 8 * (2 * 148 // 8)  # one persistent CTA per resident slot
+
+
+def test_deterministic_and_fused_entry_points_validate_on_the_host():
+    L = N.lib()
+    # global row block: a whole number of 768-vector stages, >= 128 rows
+    assert L.grkan_det_block_rows(3072, 8, N.DT_F32) == 128   # V = 96 -> 8-row stages
+    assert L.grkan_det_block_rows(3072, 8, N.DT_BF16) == 128  # V = 48 -> 16-row stages
+    assert L.grkan_det_block_rows(192, 8, N.DT_F32) == 128    # V = 6 -> 128-row stages
+    assert L.grkan_det_block_rows(3072, 1, N.DT_F32) == 128   # V = 768 -> 1-row stages
+    assert L.grkan_det_block_rows(10, 4, N.DT_F32) == 0       # layout mismatch
+    assert L.grkan_det_partials_bytes(50432, 3072, 8, 6, 4, N.DT_F32) == 394 * 8 * 10 * 4
+    assert L.grkan_det_partials_bytes(129, 3072, 8, 6, 4, N.DT_F64) == 2 * 8 * 10 * 8
+    # partials: short buffer and null pointers are host errors
+    rc = L.grkan_bwd_partials(None, None, None, None, None, None, 0, 4, 8, 2, 6, 4, N.DT_F32, 0, None, None)
+    assert rc == N.ERR_INVALID and "too small" in N.last_error()
+    rc = L.grkan_reduce_partials(None, -1, 2, 6, 4, None, None, N.DT_F32, None, None)
+    assert rc == N.ERR_GRID
+    rc = L.grkan_reduce_partials(None, 3, 2, 6, 4, None, None, N.DT_F32, None, None)
+    assert rc == N.ERR_INVALID
+    # fused layer backward: shape contract checked before any CUDA call
+    assert L.grkan_linear_bwd_workspace_bytes(50432, 3072, 768, 8) > 256
+    assert L.grkan_linear_bwd_workspace_bytes(100, 80, 64, 2) == 0    # group width 40
+    rc = L.grkan_linear_bwd(None, None, None, None, None, None, None, None, None, 0, 128, 80, 64, 2, 0, None)
+    assert rc == N.ERR_UNSUPPORTED and "group width" in N.last_error()
+    rc = L.grkan_linear_bwd(None, None, None, None, None, None, None, None, None, 0, 128, 256, 100, 2, 0, None)
+    assert rc == N.ERR_UNSUPPORTED  # K % 64
+    rc = L.grkan_linear_bwd(None, None, None, None, None, None, None, None, None, 0, 128, 255, 64, 2, 0, None)
+    assert rc == N.ERR_LAYOUT
+    rc = L.grkan_linear_bwd(None, None, None, None, None, None, None, None, None, 0, 128, 256, 64, 2,
+                            N.FLAG_EXACT, None)
+    assert rc == N.ERR_UNSUPPORTED  # FAST policy only
+    rc = L.grkan_linear_bwd(None, None, None, None, None, None, None, None, None, 0, 128, 256, 64, 2, 0, None)
+    assert rc == N.ERR_INVALID  # null pointers

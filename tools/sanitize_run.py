@@ -2,7 +2,8 @@
 
     compute-sanitizer --tool racecheck python tools/sanitize_run.py
 Exercises every kernel family on small shapes: staged (fp32/bf16/fp64, fast/exact, checked),
-register-direct (unaligned), generic degrees, the reduce and the atomic comparator.
+register-direct (unaligned), generic degrees, the reduce, the atomic comparator, the
+deterministic block partials and the fused tcgen05 layer backward.
 """
 import os
 import sys
@@ -29,5 +30,20 @@ for dtype in (torch.float32, torch.bfloat16, torch.float64):
         xs = torch.randn(x.numel() + 1, device=dev).to(dtype)[1:].view(shape)  # unaligned
         ops.rational_forward(xs, a, b)
         ops.rational_backward(xs, u, a, b)
+        # deterministic mode: whole-tensor call and a two-shard partials + reduce
+        if shape[0] * shape[1] > 1:
+            ops.rational_backward(x, u, a, b, deterministic=True, check_overflow=True)
+            rows = shape[0] * shape[1]
+            x2, u2 = x.reshape(rows, -1), u.reshape(rows, -1)
+            _, p0 = ops.backward_partials(x2, u2, a, b)
+            ops.reduce_partials(p0, m1, n, check_overflow=True)
+# fused tcgen05 layer backward: both B-atom swizzles, X staged and direct, M tail
+for M, F, K, g in [(200, 256, 128, 2), (130, 768, 192, 8), (256, 256, 1536, 2)]:
+    x = torch.randn(M, F, device=dev).to(torch.bfloat16)
+    dy = torch.randn(M, K, device=dev).to(torch.bfloat16)
+    w = torch.randn(K, F, device=dev).to(torch.bfloat16)
+    a = torch.randn(g, 6, device=dev)
+    b = torch.randn(g, 4, device=dev)
+    ops.linear_backward_fused(dy, w, x, a, b, check_overflow=True)
 torch.cuda.synchronize()
 print("sanitize run ok")
