@@ -1,0 +1,54 @@
+"""PCIe roofline for the e2e line: pinned host <-> device copy bandwidth, one way and both ways at once.
+
+    python tools/pcie_bw.py  -> one JSON line (GB/s)
+"""
+import json
+
+import torch
+
+
+def main():
+    dev = torch.device("cuda", 0)
+    n = 256 << 20  # 1 GiB of fp32
+    h_in = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    h_out = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    d_in = torch.empty(n, dtype=torch.float32, device=dev)
+    d_out = torch.empty(n, dtype=torch.float32, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    nbytes = n * 4
+
+    def timed(fn, reps=5):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps / 1e3
+
+    def h2d():
+        d_in.copy_(h_in, non_blocking=True)
+
+    def d2h():
+        h_out.copy_(d_out, non_blocking=True)
+
+    def both():
+        cur = torch.cuda.current_stream(dev)
+        s1.wait_stream(cur)
+        s2.wait_stream(cur)
+        with torch.cuda.stream(s1):
+            d_in.copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_out.copy_(d_out, non_blocking=True)
+        cur.wait_stream(s1)
+        cur.wait_stream(s2)
+
+    t1, t2, t3 = timed(h2d), timed(d2h), timed(both)
+    print(json.dumps({"h2d_gbs": nbytes / t1 / 1e9, "d2h_gbs": nbytes / t2 / 1e9,
+                      "bidirectional_gbs_each_way": nbytes / t3 / 1e9, "bytes": nbytes}))
+
+
+if __name__ == "__main__":
+    main()
