@@ -40,7 +40,7 @@ EXPORTS = (
     "grkan_version", "grkan_status_string", "grkan_last_error", "grkan_fwd",
     "grkan_bwd_workspace_bytes", "grkan_bwd", "grkan_bwd_atomic", "grkan_read_status",
     "grkan_plan", "grkan_det_block_rows", "grkan_det_partials_bytes", "grkan_bwd_partials",
-    "grkan_reduce_partials", "grkan_linear_bwd_workspace_bytes", "grkan_linear_bwd",
+    "grkan_reduce_partials", "grkan_linear_bwd_workspace_bytes", "grkan_linear_bwd", "grkan_linear_fwd",
 )
 
 
@@ -89,6 +89,8 @@ def _declare(L):
     L.grkan_linear_bwd_workspace_bytes.restype = sz
     L.grkan_linear_bwd.argtypes = [p, p, p, p, p, p, p, p, p, sz, i64, i32, i32, i32, u32, p]
     L.grkan_linear_bwd.restype = ctypes.c_int
+    L.grkan_linear_fwd.argtypes = [p, p, p, p, p, p, i64, i32, i32, i32, u32, p]
+    L.grkan_linear_fwd.restype = ctypes.c_int
 
 
 def lib():
