@@ -64,6 +64,11 @@ def parse_args(argv=None):
     p.add_argument("--mode", choices=("fast", "exact"), default="fast")
     p.add_argument("--scaling", choices=("weak", "strong"), default="weak")
     p.add_argument("--e2e-steps", type=int, default=None)
+    p.add_argument("--collective", choices=("allreduce", "deterministic"), default="allreduce",
+                   help="da/db exchange: NCCL all-reduce of the 320 B da||db, or the world-size-invariant "
+                        "path (per-block partials, all-gather, fixed-order fold; SURVEY 8e)")
+    p.add_argument("--e2e-chunks", type=int, default=16,
+                   help="row chunks of the streaming e2e pipeline (fill + drain cost one chunk each)")
     p.add_argument("--cpu-sample-batch", type=int, default=16)
     p.add_argument("--cpu-passes", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -147,7 +152,7 @@ def config_block(args, cfg):
                     "degrees (5,4)" % (args.config.upper(), batch, seq, dim, groups),
         "batch_per_gpu": batch, "seq_len": seq, "dim": dim, "groups": groups,
         "degrees": [M1 - 1, NDEN], "mode": args.mode, "io_dtype": args.dtype,
-        "parallelism": "dp%d" % args.gpus,
+        "parallelism": "dp%d" % args.gpus, "collective": args.collective,
         "l2": "inputs larger than L2 (no flush): %d MB per tensor vs 126 MB L2"
               % (batch * seq * dim * (4 if args.dtype == "fp32" else 2) // 2**20),
     }
@@ -279,12 +284,41 @@ def run_b200(args, rank, world, local_rank):
         if world > 1:
             dist.all_reduce(grads)
 
+    if args.collective == "deterministic":
+        # world-size-invariant da/db: K2 writes one partial per 128-row block,
+        # the ranks all-gather them (global block order = rank order) and every
+        # rank runs the same fixed-order K3 fold (parallel.deterministic_backward)
+        rb = ops.det_block_rows(dim, groups, tdt)
+        n_blk = -(-rows // rb)
+        part = torch.empty((n_blk, groups, M1 + NDEN), dtype=torch.float32, device=dev)
+        gathered = torch.empty((world * n_blk, groups, M1 + NDEN), dtype=torch.float32, device=dev)
+        parts_list = list(gathered.chunk(world))
+        st = torch.zeros(2, dtype=torch.int32, device=dev)
+
+        def bwd():
+            rc = L.grkan_bwd_partials(x.data_ptr(), dy.data_ptr(), a.data_ptr(), b.data_ptr(), dx.data_ptr(),
+                                      part.data_ptr(), part.numel() * 4, rows, dim, groups, M1, NDEN, dt_code,
+                                      flags, None, sp)
+            assert rc == 0, N.last_error()
+
+        def allreduce():
+            src = part
+            if world > 1:
+                if args.dist_backend == "nccl":
+                    dist.all_gather_into_tensor(gathered, part)
+                else:
+                    dist.all_gather(parts_list, part)
+                src = gathered
+            rc = L.grkan_reduce_partials(src.data_ptr(), src.shape[0], groups, M1, NDEN, da.data_ptr(),
+                                         db.data_ptr(), N.DT_F32, st.data_ptr(), sp)
+            assert rc == 0, N.last_error()
+
     for _ in range(max(3, args.warmup)):
         fwd(); bwd(); allreduce()
     torch.cuda.synchronize()
 
     K = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(nvml_index(dev))
@@ -300,6 +334,7 @@ def run_b200(args, rank, world, local_rank):
         bwd()
         ev[k][2].record(stream)
         allreduce()
+        ev[k][3].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
     sampler.stop()
@@ -308,10 +343,11 @@ def run_b200(args, rank, world, local_rank):
     ms_total = t_start.elapsed_time(t_end)
     fwd_ms = statistics.fmean(e[0].elapsed_time(e[1]) for e in ev)
     bwd_ms = statistics.fmean(e[1].elapsed_time(e[2]) for e in ev)
+    coll_ms = statistics.fmean(e[2].elapsed_time(e[3]) for e in ev)
     if world > 1:
-        t = torch.tensor([ms_total, fwd_ms, bwd_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms_total, fwd_ms, bwd_ms, coll_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total, fwd_ms, bwd_ms = t.tolist()
+        ms_total, fwd_ms, bwd_ms, coll_ms = t.tolist()
     ms_step = ms_total / K
     value = world * E / (ms_step / 1e3)
 
@@ -347,7 +383,7 @@ def run_b200(args, rank, world, local_rank):
     del y, dx, ws
     torch.cuda.empty_cache()
     pipe = HostPipeline(dev, dim, groups, M1, NDEN, tdt,
-                        chunk_rows=max(rows // 16, -(-HostPipeline.AUTO_CHUNK_BYTES // (dim * es))))
+                        chunk_rows=max(rows // args.e2e_chunks, -(-(4 << 20) // (dim * es))))
 
     def e2e_stream():
         da_, db_ = pipe.fwd_bwd(xh, dyh, a, b, yh, dxh, exact=exact)
@@ -424,6 +460,7 @@ def run_b200(args, rank, world, local_rank):
             "fwd_us": fwd_ms * 1e3, "fwd_gbs": fwd_gbs, "fwd_frac": fwd_gbs / peak,
             "fwd_traffic": ncu_traffic(args, "fwd"),
             "bwd_us": bwd_ms * 1e3, "bwd_gbs": bwd_gbs, "bwd_frac": bwd_gbs / peak,
+            "collective": args.collective, "collective_us": coll_ms * 1e3,
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * es * E,
                 "d2h_bytes_per_step": 2 * es * E + 4 * groups * (M1 + NDEN),
