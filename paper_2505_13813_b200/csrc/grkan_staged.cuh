@@ -31,10 +31,13 @@ constexpr int kMaxStages = 8;
 // KAT-B: 2 CTAs, 4-stage ring, unrolled vectors is best for both fp32 and
 // bf16 (bf16 with 3 CTAs at 72 registers, 2-stage ring, serial vectors:
 // 311 us vs 279 us -- the bf16 backward is FMA-pipe bound, not warp bound).
+// kFullStage: branch-free body for full stages -- measured 260 -> 255 us for
+// bf16 I/O but 308 -> 320 us for fp32 (KAT-B), so bf16 only.
 template <typename T>
 struct BwdCfg {
   static constexpr int kMinBlocks = GRKAN_BWD_CTAS;
   static constexpr bool kSerialVectors = false;
+  static constexpr bool kFullStage = GRKAN_FULL_STAGE && std::is_same<T, __nv_bfloat16>::value;
 };
 constexpr int kFwdCtasPerSm = GRKAN_FWD_CTAS;
 // Forward geometry (separately tunable: one tensor in, little math per byte).
@@ -328,6 +331,7 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
       gp[j] = dx + (row0 + r) * geo.d + (int64_t)g * geo.dg + c;
     }
     const int64_t gstep = (int64_t)geo.RS * geo.d;
+    const bool full_slots = svecs == kStageVecs;  // every thread slot maps into the stage
     const int slot_elems = geo.RS * geo.dg;
     const int nst = (nr + geo.RS - 1) / geo.RS;
     int slot = 0, since_flush = 0;
@@ -337,29 +341,37 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
       const int rows_here = min(geo.RS, nr - s * geo.RS);
       const T* xs = sx + slot * slot_elems;
       const T* us = su + slot * slot_elems;
-#pragma unroll(BwdCfg<T>::kSerialVectors ? 1 : kVPT)
-      for (int j = 0; j < kVPT; ++j) {
-        if (sr[j] < rows_here) {
-          A vx[W], vu[W], o[W];
-          RW::unpack(*reinterpret_cast<const uint4*>(xs + so[j]), vx);
-          RW::unpack(*reinterpret_cast<const uint4*>(us + so[j]), vu);
-          if constexpr (PK) {
-rp.template grad_n<W / 2, kGuard<T>>(vx, vu, o, acc2);
-          } else {
+      auto vec = [&](int j) {
+        A vx[W], vu[W], o[W];
+        RW::unpack(*reinterpret_cast<const uint4*>(xs + so[j]), vx);
+        RW::unpack(*reinterpret_cast<const uint4*>(us + so[j]), vu);
+        if constexpr (PK) {
+          rp.template grad_n<W / 2, kGuard<T>>(vx, vu, o, acc2);
+        } else {
 #pragma unroll
-            for (int e = 0; e < W; ++e) o[e] = rs.grad(vx[e], vu[e], acc);
-          }
-          if constexpr (CHECK) {
-#pragma unroll
-            for (int e = 0; e < W; ++e) {
-              chk.add(vx[e]);
-              chk.add(vu[e]);
-            }
-          }
-          __stcs(reinterpret_cast<uint4*>(gp[j]), RW::pack(o));
+          for (int e = 0; e < W; ++e) o[e] = rs.grad(vx[e], vu[e], acc);
         }
-        gp[j] += gstep;
+        if constexpr (CHECK) {
+#pragma unroll
+          for (int e = 0; e < W; ++e) {
+            chk.add(vx[e]);
+            chk.add(vu[e]);
+          }
+        }
+        __stcs(reinterpret_cast<uint4*>(gp[j]), RW::pack(o));
+      };
+      if (BwdCfg<T>::kFullStage && full_slots && rows_here == geo.RS) {
+        // every slot of a full stage is valid: one branch-free block the
+        // scheduler can interleave across the thread's kVPT vectors
+#pragma unroll
+        for (int j = 0; j < kVPT; ++j) vec(j);
+      } else {
+#pragma unroll(BwdCfg<T>::kSerialVectors ? 1 : kVPT)
+        for (int j = 0; j < kVPT; ++j)
+          if (sr[j] < rows_here) vec(j);
       }
+#pragma unroll
+      for (int j = 0; j < kVPT; ++j) gp[j] += gstep;
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
       // Short per-lane fp32 chains keep the da/db rounding error near the fp32

@@ -80,6 +80,9 @@ struct Plan {
 #ifndef GRKAN_FWD_STAGES
 #define GRKAN_FWD_STAGES 4         // staged forward ring depth
 #endif
+#ifndef GRKAN_FULL_STAGE
+#define GRKAN_FULL_STAGE 1        // staged backward: branch-free path for full stages
+#endif
 #ifndef GRKAN_PROBE_NOMEM
 #define GRKAN_PROBE_NOMEM 0       // diagnostic only: staged backward computes on unfilled shared memory
 #endif
