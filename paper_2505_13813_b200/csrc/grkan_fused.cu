@@ -35,6 +35,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <type_traits>
 
 #include "../../include/grkan_b200.h"
 #include "grkan_staged.cuh"
@@ -48,9 +49,18 @@ namespace fused {
 
 constexpr int kBM = 128;          // tile rows (UMMA M, TMEM lanes)
 constexpr int kBK = 64;           // K per stage (one 128-byte swizzle row of bf16)
-constexpr int kSmemBudget = 200 * 1024;  // operand ring (the rest: alignment + barriers)
+#ifndef GRKAN_FUSED_SMEM_KB
+#define GRKAN_FUSED_SMEM_KB 200
+#endif
+constexpr int kSmemBudget = GRKAN_FUSED_SMEM_KB * 1024;  // operand ring + X tiles (the rest: alignment, barriers)
 constexpr int kKC = 10;           // coefficient terms (degrees (5, 4))
 constexpr int kMaxGroups = 64;    // coefficient table in shared memory
+#ifndef GRKAN_FUSED_SK_BN
+#define GRKAN_FUSED_SK_BN 192     // short-K (X staged) tile width ...
+#endif
+#ifndef GRKAN_FUSED_SK_ES
+#define GRKAN_FUSED_SK_ES 3       // ... and epilogue warps per TMEM lane quadrant
+#endif
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(
@@ -304,9 +314,12 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
       }
       const unsigned char* xtile = xs + acc * XBYTES;
       if constexpr (XS) mbar_wait(&xfull[acc], (i >> 1) & 1);
-      float sacc[kKC];  // scalar accumulators: register budget of 16 epilogue warps
+      // accumulators: float2 (packed FFMA2) when the register budget allows
+      // (ES <= 3: <= 14 warps, 128 registers), else one float per coefficient
+      using AccT = std::conditional_t<(ES <= 3), float2, float>;
+      AccT sacc[kKC];
 #pragma unroll
-      for (int k = 0; k < kKC; ++k) sacc[k] = 0.f;
+      for (int k = 0; k < kKC; ++k) sacc[k] = AccT{};
       mbar_wait(&tfull[acc], (i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t taddr = tmem_d + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + cs * CW);
@@ -343,7 +356,7 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
             Raw16<__nv_bfloat16>::unpack(xr[c & 1][v], xv);
 #pragma unroll
             for (int k = 0; k < 8; ++k) uv[k] = u[v * 8 + k];
-            rp.template grad_n<4, false, float>(xv, uv, o, sacc);
+            rp.template grad_n<4, false, AccT>(xv, uv, o, sacc);
             o4[v] = Raw16<__nv_bfloat16>::pack(o);
           }
 #pragma unroll
@@ -354,7 +367,8 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
       const int64_t t = (m_tile * (geo.dg / CW) + (c0 % geo.dg) / CW) * 4 + q;
 #pragma unroll
       for (int k = 0; k < kKC; ++k) {
-        float v = sacc[k];
+        float v;
+        if constexpr (ES <= 3) v = sacc[k].x + sacc[k].y; else v = sacc[k];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0) part[(static_cast<int64_t>(g) * kKC + k) * geo.ppg + t] = v;
@@ -613,13 +627,14 @@ constexpr TileShape kShapesLongK[] = {{256, 64, 4, 16, false}, {192, 64, 4, 16, 
                                       {192, 64, 2, 32, false}, {128, 64, 4, 16, false}, {128, 64, 2, 32, false},
                                       {96, 32, 1, 32, false},  {64, 64, 2, 32, false},  {64, 64, 1, 32, false},
                                       {32, 32, 1, 32, false}};
-constexpr TileShape kShapesShortK[] = {{128, 64, 4, 16, true}, {64, 64, 2, 32, true}, {96, 32, 1, 32, false},
+constexpr TileShape kShapesShortK[] = {{GRKAN_FUSED_SK_BN, 64, GRKAN_FUSED_SK_ES, 16, true}, {128, 64, 4, 16, true},
+                                       {64, 64, 2, 32, true}, {96, 32, 1, 32, false},
                                        {32, 32, 1, 32, false}};
 
 bool pick_shape(int N, int dg, int K, TileShape* out) {
   const bool short_k = K <= 1024;
   const TileShape* list = short_k ? kShapesShortK : kShapesLongK;
-  const int n = short_k ? 4 : 10;
+  const int n = short_k ? 5 : 10;
   for (int i = 0; i < n; ++i) {
     const TileShape& t = list[i];
     const int cw = t.bn / t.es;
@@ -759,6 +774,9 @@ int grkan_linear_bwd(const void* dy, const void* w, const void* x, const void* a
   GRKAN_FUSED_CASE(64, 64, 2, 32, false)
   GRKAN_FUSED_CASE(64, 64, 1, 32, false)
   GRKAN_FUSED_CASE(128, 64, 4, 16, true)
+#if GRKAN_FUSED_SK_BN != 128 || GRKAN_FUSED_SK_ES != 4
+  GRKAN_FUSED_CASE(GRKAN_FUSED_SK_BN, 64, GRKAN_FUSED_SK_ES, 16, true)
+#endif
   GRKAN_FUSED_CASE(64, 64, 2, 32, true)
   e = launch_t<32, 32, 1, 32, false>(mdy, mw, mx, x, dx, fa, fb, part, geo, tiles, s);
 #undef GRKAN_FUSED_CASE
