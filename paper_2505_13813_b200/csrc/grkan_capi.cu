@@ -93,7 +93,7 @@ int64_t det_rows(int32_t d, int32_t ng, size_t es) {
   const int W = static_cast<int>(16 / es);
   const int V = dg % W == 0 ? dg / W : 0;
   const int RS = (V >= 1 && V <= grkan::kStageVecsHost) ? grkan::kStageVecsHost / V : 1;
-  return static_cast<int64_t>(RS) * ((128 + RS - 1) / RS);
+  return static_cast<int64_t>(RS) * ((GRKAN_DET_ROWS + RS - 1) / RS);
 }
 
 // nt = tensors streamed in (1 forward, 2 backward).  det: one partial per

@@ -83,6 +83,9 @@ struct Plan {
 #ifndef GRKAN_FULL_STAGE
 #define GRKAN_FULL_STAGE 1        // staged backward: branch-free path for full stages
 #endif
+#ifndef GRKAN_DET_ROWS
+#define GRKAN_DET_ROWS 128        // deterministic mode: minimum rows per global block
+#endif
 #ifndef GRKAN_PROBE_NOMEM
 #define GRKAN_PROBE_NOMEM 0       // diagnostic only: staged backward computes on unfilled shared memory
 #endif
