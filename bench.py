@@ -64,9 +64,10 @@ def parse_args(argv=None):
     p.add_argument("--mode", choices=("fast", "exact"), default="fast")
     p.add_argument("--scaling", choices=("weak", "strong"), default="weak")
     p.add_argument("--e2e-steps", type=int, default=None)
-    p.add_argument("--collective", choices=("allreduce", "deterministic"), default="allreduce",
-                   help="da/db exchange: NCCL all-reduce of the 320 B da||db, or the world-size-invariant "
-                        "path (per-block partials, all-gather, fixed-order fold; SURVEY 8e)")
+    p.add_argument("--collective", choices=("allreduce", "deterministic", "p2p"), default="allreduce",
+                   help="da/db exchange: NCCL all-reduce of the 320 B da||db; the world-size-invariant "
+                        "path (per-block partials, all-gather, fixed-order fold; SURVEY 8e); or p2p: K3 "
+                        "fused with the exchange over CUDA-IPC peer memory (grkan_bwd_p2p, no NCCL)")
     p.add_argument("--e2e-chunks", type=int, default=16,
                    help="row chunks of the streaming e2e pipeline (fill + drain cost one chunk each)")
     p.add_argument("--cpu-sample-batch", type=int, default=16)
@@ -304,6 +305,22 @@ def run_b200(args, rank, world, local_rank):
     def join_comm():
         if comm is not None:
             stream.wait_stream(comm)
+
+    if args.collective == "p2p":
+        from paper_2505_13813_b200.parallel import PeerExchange
+
+        pex = PeerExchange(groups, M1, NDEN, dev)
+        ws_p2p = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+
+        def bwd():
+            pex.epoch += 1
+            rc = L.grkan_bwd_p2p(x.data_ptr(), dy.data_ptr(), a.data_ptr(), b.data_ptr(), dx.data_ptr(),
+                                 da.data_ptr(), db.data_ptr(), ws_p2p.data_ptr(), ws_bytes, rows, dim, groups,
+                                 M1, NDEN, dt_code, flags, pex.ptrs.data_ptr(), pex.rank, pex.world, pex.epoch, sp)
+            assert rc == 0, N.last_error()
+
+        def allreduce(timed=False):
+            pass  # the exchange happened inside bwd's reduce kernel
 
     if args.collective == "deterministic":
         # world-size-invariant da/db: K2 writes one partial per 128-row block,

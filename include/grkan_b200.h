@@ -162,6 +162,28 @@ GRKAN_API int grkan_linear_fwd(const void* x, const void* w, const void* bias, c
                                void* y, int64_t M, int32_t N, int32_t K, int32_t n_groups, uint32_t flags,
                                void* stream);
 
+/* K3 fused with the cross-GPU da||db sum over peer memory:
+ * grkan_bwd_p2p runs K2, then ONE kernel that folds this rank's partials,
+ * stores the fp64 column values into every rank's exchange buffer through
+ * CUDA-IPC-mapped pointers (NVLink), bumps every rank's arrival counter and,
+ * once all ranks arrived, folds the world values in rank order -- no NCCL
+ * launch, bitwise-identical da/db on every rank.  `peer_bufs` is a DEVICE
+ * array of `world` pointers: rank r's exchange buffer mapped into this
+ * process (own buffer at index `rank`); each buffer comes from
+ * grkan_p2p_alloc(grkan_p2p_buffer_bytes(...)) (zeroed); `epoch` counts calls
+ * from 1 and must advance identically on every rank. */
+#define GRKAN_IPC_HANDLE_BYTES 64
+GRKAN_API size_t grkan_p2p_buffer_bytes(int32_t world, int32_t n_groups, int32_t m1, int32_t n);
+GRKAN_API int grkan_p2p_alloc(size_t bytes, void** out);
+GRKAN_API int grkan_p2p_free(void* ptr);
+GRKAN_API int grkan_ipc_get_handle(const void* dev_ptr, void* handle_out);
+GRKAN_API int grkan_ipc_open_handle(const void* handle, void** dev_ptr_out);
+GRKAN_API int grkan_ipc_close_handle(void* dev_ptr);
+GRKAN_API int grkan_bwd_p2p(const void* x, const void* dy, const void* a, const void* b, void* dx, void* da,
+                            void* db, void* ws, size_t ws_bytes, int64_t rows, int32_t d, int32_t n_groups,
+                            int32_t m1, int32_t n, int32_t dtype, uint32_t flags, void* const* peer_bufs,
+                            int32_t rank, int32_t world, uint64_t epoch, void* stream);
+
 /* Synchronise `stream` and copy the device status to the host; maps it to a
  * status code (NONFINITE_INPUT first, then ACCUM_OVERFLOW, else OK). */
 GRKAN_API int grkan_read_status(const grkan_device_status* status, void* stream,

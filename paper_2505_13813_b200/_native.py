@@ -41,7 +41,10 @@ EXPORTS = (
     "grkan_bwd_workspace_bytes", "grkan_bwd", "grkan_bwd_atomic", "grkan_read_status",
     "grkan_plan", "grkan_det_block_rows", "grkan_det_partials_bytes", "grkan_bwd_partials",
     "grkan_reduce_partials", "grkan_linear_bwd_workspace_bytes", "grkan_linear_bwd", "grkan_linear_fwd",
+    "grkan_p2p_buffer_bytes", "grkan_p2p_alloc", "grkan_p2p_free", "grkan_ipc_get_handle",
+    "grkan_ipc_open_handle", "grkan_ipc_close_handle", "grkan_bwd_p2p",
 )
+IPC_HANDLE_BYTES = 64
 
 
 class NativeLibraryError(RuntimeError):
@@ -91,6 +94,21 @@ def _declare(L):
     L.grkan_linear_bwd.restype = ctypes.c_int
     L.grkan_linear_fwd.argtypes = [p, p, p, p, p, p, i64, i32, i32, i32, u32, p]
     L.grkan_linear_fwd.restype = ctypes.c_int
+    L.grkan_p2p_buffer_bytes.argtypes = [i32, i32, i32, i32]
+    L.grkan_p2p_buffer_bytes.restype = sz
+    L.grkan_p2p_alloc.argtypes = [sz, ctypes.POINTER(ctypes.c_void_p)]
+    L.grkan_p2p_alloc.restype = ctypes.c_int
+    L.grkan_p2p_free.argtypes = [p]
+    L.grkan_p2p_free.restype = ctypes.c_int
+    L.grkan_ipc_get_handle.argtypes = [p, p]
+    L.grkan_ipc_get_handle.restype = ctypes.c_int
+    L.grkan_ipc_open_handle.argtypes = [p, ctypes.POINTER(ctypes.c_void_p)]
+    L.grkan_ipc_open_handle.restype = ctypes.c_int
+    L.grkan_ipc_close_handle.argtypes = [p]
+    L.grkan_ipc_close_handle.restype = ctypes.c_int
+    L.grkan_bwd_p2p.argtypes = [p, p, p, p, p, p, p, p, sz, i64, i32, i32, i32, i32, i32, u32, p, i32, i32,
+                                ctypes.c_uint64, p]
+    L.grkan_bwd_p2p.restype = ctypes.c_int
 
 
 def lib():

@@ -240,6 +240,9 @@ size_t ws_bytes_for(const Plan& p, int32_t m1, int32_t n, int32_t dtype) {
 }  // namespace
 
 namespace grkan {
+cudaError_t launch_reduce_p2p(int dtype, const void* part, int64_t n_tiles, int ng, int m1, int n, void* const* bufs,
+                              int rank, int world, unsigned long long epoch, void* da, void* db, DevStatus* st,
+                              cudaStream_t stream);  // grkan_p2p.cu
 // Error reporting for the other C-ABI translation units (grkan_fused.cu).
 int set_error(int code, const char* msg) { return fail(code, "%s", msg); }
 }  // namespace grkan
@@ -380,6 +383,61 @@ int grkan_bwd(const void* x, const void* dy, const void* a, const void* b, void*
   L.stream = s;
   e = launch("bwd", dtype, L);
   if (e != cudaSuccess) return cuda_fail(e, "k_bwd launch");
+  return GRKAN_OK;
+}
+
+int grkan_bwd_p2p(const void* x, const void* dy, const void* a, const void* b, void* dx, void* da, void* db,
+                  void* ws, size_t ws_bytes, int64_t rows, int32_t d, int32_t n_groups, int32_t m1, int32_t n,
+                  int32_t dtype, uint32_t flags, void* const* peer_bufs, int32_t rank, int32_t world,
+                  uint64_t epoch, void* stream) {
+  int rc = check_layout(rows, d, n_groups, m1, n, dtype, flags);
+  if (rc) return rc;
+  if (flags & GRKAN_FLAG_DETERMINISTIC)
+    return fail(GRKAN_ERR_INVALID, "the peer-memory exchange folds per-CTA partials; no DETERMINISTIC flag");
+  if (!ws || !da || (n > 0 && !db) || !peer_bufs) return fail(GRKAN_ERR_INVALID, "null workspace / gradient / peer pointer");
+  if (world < 1 || rank < 0 || rank >= world || epoch == 0)
+    return fail(GRKAN_ERR_INVALID, "bad rank %d / world %d / epoch (must start at 1)", rank, world);
+  if (!aligned16(ws)) return fail(GRKAN_ERR_INVALID, "workspace must be 16-byte aligned");
+  if (!x || !dy || !dx || !a || (n > 0 && !b)) {
+    if (rows > 0) return fail(GRKAN_ERR_INVALID, "null tensor pointer");
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DevStatus* st = reinterpret_cast<DevStatus*>(ws);
+  cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(DevStatus), s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(status)");
+  const size_t es = elem_size(dtype);
+  const bool vec = rows > 0 && vec_ok(d, n_groups, es, {x, dy, dx});
+  const Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count());
+  if (!plan_fits(p)) return fail(GRKAN_ERR_GRID, "grid geometry invalid: %lld CTAs", (long long)p.ctas);
+  const size_t need = ws_bytes_for(p, m1, n, dtype);
+  if (ws_bytes < need) return fail(GRKAN_ERR_INVALID, "workspace too small: %zu < %zu bytes", ws_bytes, need);
+  if (rows > 0) {
+    LaunchArgs L{};
+    L.plan = &p;
+    L.x = x;
+    L.dy = dy;
+    L.out = dx;
+    L.a = a;
+    L.b = b;
+    L.part = static_cast<char*>(ws) + 256;
+    L.st = st;
+    L.m1 = m1;
+    L.n = n;
+    L.exact = (flags & GRKAN_FLAG_EXACT) != 0;
+    L.vec = vec;
+    L.check = (flags & GRKAN_FLAG_CHECK_FINITE) != 0;
+    L.partials_only = true;
+    L.stream = s;
+    e = launch("bwd", dtype, L);
+    if (e != cudaSuccess) return cuda_fail(e, "k_bwd (partials) launch");
+  } else {  // an empty shard still takes part in the exchange, with zero partials
+    e = cudaMemsetAsync(static_cast<char*>(ws) + 256, 0, need - 256, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(partials)");
+  }
+  const int64_t n_tiles = rows > 0 ? p.geo.n_tiles : 1;
+  e = grkan::launch_reduce_p2p(dtype, static_cast<char*>(ws) + 256, n_tiles, n_groups, m1, n, peer_bufs, rank, world,
+                               epoch, da, db, st, s);
+  if (e != cudaSuccess) return cuda_fail(e, "k_bwd_reduce_p2p launch");
   return GRKAN_OK;
 }
 

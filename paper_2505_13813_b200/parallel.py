@@ -171,3 +171,92 @@ def deterministic_backward(x_shard: torch.Tensor, dy_shard: torch.Tensor, a: tor
     full = gather_blocks(part, counts, group)
     da, db = ops.reduce_partials(full.contiguous(), m1, n)
     return dx, da, db
+
+
+class PeerExchange:
+    """da||db summed across ranks INSIDE the reduce kernel, over peer memory (no NCCL).
+
+    Setup (once): every rank allocates a zeroed exchange buffer
+    (grkan_p2p_alloc), the CUDA-IPC handles are all-gathered through the
+    process group (any backend: only 64 bytes per rank) and opened, and the
+    device array of the ``world`` mapped pointers is built.  Each
+    ``backward(...)`` is then K2 + one fused reduce/exchange kernel
+    (grkan_bwd_p2p) -- bitwise-identical da/db on every rank.  Ranks must call
+    ``backward`` the same number of times (the epoch counter).
+    """
+
+    def __init__(self, n_groups: int, m1: int, n: int, device, group=None):
+        import ctypes
+
+        from . import _native as N
+
+        self._N = N
+        self.device = torch.device(device)
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        L = N.lib()
+        nbytes = L.grkan_p2p_buffer_bytes(self.world, n_groups, m1, n)
+        buf = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            self._check(L.grkan_p2p_alloc(nbytes, ctypes.byref(buf)))
+        self._own = buf.value
+        handle = (ctypes.c_char * N.IPC_HANDLE_BYTES)()
+        self._check(L.grkan_ipc_get_handle(self._own, handle))
+        handles = [bytes(handle)]
+        if self.world > 1:
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(handle), group=group)
+        self._opened = []
+        ptrs = []
+        with torch.cuda.device(self.device):
+            for r, h in enumerate(handles):
+                if r == self.rank:
+                    ptrs.append(self._own)
+                    continue
+                p = ctypes.c_void_p()
+                hb = (ctypes.c_char * N.IPC_HANDLE_BYTES).from_buffer_copy(h)
+                self._check(L.grkan_ipc_open_handle(hb, ctypes.byref(p)))
+                self._opened.append(p.value)
+                ptrs.append(p.value)
+        self.ptrs = torch.tensor(ptrs, dtype=torch.int64, device=self.device)
+        self.epoch = 0
+        if self.world > 1:
+            dist.barrier(group=group)  # every buffer is zeroed before anyone writes into it
+
+    def _check(self, rc):
+        if rc != 0:
+            from .errors import raise_for_status
+            raise_for_status(rc, self._N.last_error())
+
+    def backward(self, x, dy, a, b, exact: bool = False, check_overflow: bool = False):
+        """(dx, da, db): dx for this rank's rows, da/db summed over every rank."""
+        from . import ops
+
+        rows, d, ng, m1, n = ops._validate(x, a, b)
+        x, dy, a, b = x.contiguous(), dy.contiguous(), a.contiguous(), b.contiguous()
+        dx = torch.empty_like(x)
+        da = torch.empty((ng, m1), dtype=a.dtype, device=x.device)
+        db = torch.empty((ng, n), dtype=a.dtype, device=x.device)
+        ws = torch.empty(ops.workspace_bytes(max(rows, 1), d, ng, m1, n, x.dtype), dtype=torch.uint8,
+                         device=x.device)
+        self.epoch += 1
+        N = self._N
+        with torch.cuda.device(x.device):
+            rc = N.lib().grkan_bwd_p2p(x.data_ptr(), dy.data_ptr(), a.data_ptr(), ops._ptr(b), dx.data_ptr(),
+                                       da.data_ptr(), ops._ptr(db), ws.data_ptr(), ws.numel(), rows, d, ng, m1, n,
+                                       ops._DT[x.dtype], ops._flags(exact, False), self.ptrs.data_ptr(),
+                                       self.rank, self.world, self.epoch, ops._stream(x.device))
+            self._check(rc)
+            if check_overflow:
+                ops.read_status(ws[:8])
+        return dx, da, db
+
+    def close(self):
+        L = self._N.lib()
+        torch.cuda.synchronize(self.device)
+        for p in self._opened:
+            L.grkan_ipc_close_handle(p)
+        self._opened = []
+        if self._own:
+            L.grkan_p2p_free(self._own)
+            self._own = None
