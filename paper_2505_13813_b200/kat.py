@@ -43,7 +43,7 @@ class GRKAN(nn.Module):
 
     def _layer(self, x, act, fc):
         if self.fused and (self.drop.p == 0.0 or not self.training):
-            xd = x.to(torch.bfloat16) if torch.is_autocast_enabled() and x.is_cuda else x
+            xd = x.to(torch.bfloat16) if x.is_cuda and torch.is_autocast_enabled("cuda") else x
             if fused_layer_supported(xd, act, fc):
                 return GroupRationalLinearFn.apply(xd, act.a, act.b, fc.weight, fc.bias)
         return fc(self.drop(act(x)))

@@ -16,3 +16,10 @@ ls -la gpurun_out | grep ${TAG}
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_bwd_staged" -s 2 -c 1 -o gpurun_out/prof_${TAG}_bwd_bf16 $B --dtype bf16 > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s 12 -c 15 --csv --log-file gpurun_out/launches_${TAG}_bf16.csv $B --dtype bf16 > /dev/null 2>&1
 ls -la gpurun_out | grep ${TAG}
+timeout 600 python bench.py --config kat-b-train --steps 10 --warmup 3 > gpurun_out/train_${TAG}.json 2>&1
+timeout 600 python bench.py --config kat-b-train --steps 10 --warmup 3 --fused-mlp > gpurun_out/train_${TAG}_fused.json 2>&1
+timeout 600 python tools/bench_fused.py > gpurun_out/fused_${TAG}.jsonl 2>&1
+timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --e2e-steps 2 --collective deterministic > gpurun_out/bench_${TAG}_det.json 2>&1
+timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --e2e-steps 2 --collective p2p > gpurun_out/bench_${TAG}_p2p.json 2>&1
+timeout 300 python tools/pcie_bw.py > gpurun_out/pcie_${TAG}.json 2>&1
+ls -la gpurun_out | grep ${TAG}
