@@ -11,7 +11,12 @@ per-group da/db (the path's only exchange).  Weak scaling: every rank owns a
 full KAT-B batch (B=256), so per-GPU work is fixed as N grows.
 
 ``value``  elements/s over all ranks, inputs already resident in HBM, device
-           time (CUDA events) max over ranks.
+           time (CUDA events) max over ranks.  Warm-up: >= W steps and >= 150 ms;
+           the timed K steps are enqueued behind a short device-side spin
+           (--hold-ms) so host launch jitter cannot open gaps inside them.
+           ``--collective`` picks the da/db exchange for N > 1 (NCCL
+           all-reduce on a side stream, the world-size-invariant block path,
+           or the peer-memory fused reduce); its time is ``kernels.collective_us``.
 ``e2e``    the same metric through the public streaming API
            (streaming.HostPipeline.fwd_bwd) with x, dy copied from pinned host
            memory and y, dx, da, db copied back every step; the plain
@@ -64,6 +69,8 @@ def parse_args(argv=None):
     p.add_argument("--mode", choices=("fast", "exact"), default="fast")
     p.add_argument("--scaling", choices=("weak", "strong"), default="weak")
     p.add_argument("--e2e-steps", type=int, default=None)
+    p.add_argument("--hold-ms", type=float, default=20.0,
+                   help="device-side spin before the timed region while the host enqueues it")
     p.add_argument("--collective", choices=("allreduce", "deterministic", "p2p"), default="allreduce",
                    help="da/db exchange: NCCL all-reduce of the 320 B da||db; the world-size-invariant "
                         "path (per-block partials, all-gather, fixed-order fold; SURVEY 8e); or p2p: K3 "
@@ -351,8 +358,16 @@ def run_b200(args, rank, world, local_rank):
                                          db.data_ptr(), N.DT_F32, st.data_ptr(), sp)
             assert rc == 0, N.last_error()
 
-    for _ in range(max(3, args.warmup)):
+    # warm-up: at least W steps and at least 150 ms of device work (clocks and
+    # memory settled on a fresh box), untimed
+    t_w = time.perf_counter()
+    n_w = 0
+    while n_w < max(3, args.warmup) or time.perf_counter() - t_w < 0.15:
         fwd(); bwd(); allreduce()
+        n_w += 1
+        if n_w % 20 == 0:
+            torch.cuda.synchronize()
+    join_comm()
     torch.cuda.synchronize()
 
     K = args.steps
@@ -364,6 +379,9 @@ def run_b200(args, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     sampler.start()
+    # hold the stream with a short device-side spin while the host enqueues all
+    # K steps, so host-side jitter cannot open launch gaps inside the timed region
+    torch.cuda._sleep(int(args.hold_ms * 1e-3 * 1.965e9))
     t_start.record(stream)
     for k in range(K):
         ev[k][0].record(stream)
