@@ -33,6 +33,7 @@ Inputs exceed L2 (KAT-B fp32: 620 MB per tensor vs 126 MB L2), so no flush.
 from __future__ import annotations
 
 import argparse
+import math
 import json
 import os
 import statistics
@@ -80,6 +81,8 @@ def parse_args(argv=None):
     p.add_argument("--cpu-sample-batch", type=int, default=16)
     p.add_argument("--cpu-passes", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--single-thread-baseline", action=argparse.BooleanOptionalAction, default=True,
+                   help="--impl reference: also time the CPU path with one worker (SURVEY 8d)")
     p.add_argument("--fused-mlp", action="store_true",
                    help="*-train configs: GR-KAN rational->Linear pairs with the fused tcgen05 backward")
     p.add_argument("--dist-backend", default="nccl",
@@ -112,13 +115,13 @@ def peaks():
 # CPU path: the oracle port of the reference (forward_tensor + backward_blocked)
 # ---------------------------------------------------------------------------
 
-def cpu_reference_rate(cfg, batch, passes, warmup=1):
+def cpu_reference_rate(cfg, batch, passes, warmup=1, workers=None):
     """elements/s of the NumPy restatement of the reference path on this host."""
     from oracle import grkan_oracle as orc
 
     _, seq, dim, groups = cfg
     x, u, num, den = orc.bench_inputs(batch, seq, dim, groups, M1, NDEN, seed=0)
-    workers = os.cpu_count() or 1
+    workers = workers or os.cpu_count() or 1
     for _ in range(warmup):
         orc.cpu_step(x, u, num, den, workers=workers)
     times = []
@@ -150,6 +153,11 @@ def run_reference(args, rank):
                          "sample": sample},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if args.single_thread_baseline:  # also time workers=1 (one pass, B=4 rows sample)
+        r1, _, t1 = cpu_reference_rate(cfg, min(4, batch), 1, warmup=0, workers=1)
+        line["cpu_baseline"]["single_thread"] = {
+            "value": r1, "unit": UNIT, "cores": 1,
+            "sample": "%s rows B=%d, workers=1, one pass (%.2f s)" % (args.config, min(4, batch), t1[0])}
     print(json.dumps(line), flush=True)
 
 
@@ -410,6 +418,10 @@ def run_b200(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total, fwd_ms, bwd_ms, coll_ms = t.tolist()
     ms_step = ms_total / K
+    # per-step device times (fwd start -> after the step's exchange): mean +- CI95
+    # with the normal approximation, as the reference reports (verification.py:344-349)
+    step_ms = [e[0].elapsed_time(e[3]) for e in ev]
+    ci95_ms = 1.96 * statistics.stdev(step_ms) / math.sqrt(len(step_ms)) if len(step_ms) > 1 else None
     value = world * E / (ms_step / 1e3)
 
     # ---- the paper's Alg. 1 comparator (per-element atomicAdd), same inputs ----------------
@@ -504,7 +516,7 @@ def run_b200(args, rank, world, local_rank):
     fwd_gbs = fwd_bytes / (fwd_ms / 1e3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_ci95": ci95_ms, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f32" if args.dtype == "fp32" else "bf16-io/f32-math",
         "data": "synthetic: x, dy ~ N(0,1) (torch seeded per rank), coefficients ~ N(0,1) "
