@@ -184,6 +184,15 @@ GRKAN_API int grkan_bwd_p2p(const void* x, const void* dy, const void* a, const 
                             int32_t m1, int32_t n, int32_t dtype, uint32_t flags, void* const* peer_bufs,
                             int32_t rank, int32_t world, uint64_t epoch, void* stream);
 
+/* Per-element gradient terms (the reference's gradient_terms,
+ * pkg/src/grkan/rational.py:227-278): dx plus the m1 + n per-element
+ * contributions, unreduced, into terms[(k) * rows * d + i] (coefficient dtype).
+ * Introspection / parity only (10x the output of grkan_bwd); EXACT gives the
+ * reference's terms bit for bit. */
+GRKAN_API int grkan_bwd_terms(const void* x, const void* dy, const void* a, const void* b, void* dx, void* terms,
+                              int64_t rows, int32_t d, int32_t n_groups, int32_t m1, int32_t n, int32_t dtype,
+                              uint32_t flags, void* stream);
+
 /* Synchronise `stream` and copy the device status to the host; maps it to a
  * status code (NONFINITE_INPUT first, then ACCUM_OVERFLOW, else OK). */
 GRKAN_API int grkan_read_status(const grkan_device_status* status, void* stream,

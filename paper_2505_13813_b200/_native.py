@@ -42,7 +42,7 @@ EXPORTS = (
     "grkan_plan", "grkan_det_block_rows", "grkan_det_partials_bytes", "grkan_bwd_partials",
     "grkan_reduce_partials", "grkan_linear_bwd_workspace_bytes", "grkan_linear_bwd", "grkan_linear_fwd",
     "grkan_p2p_buffer_bytes", "grkan_p2p_alloc", "grkan_p2p_free", "grkan_ipc_get_handle",
-    "grkan_ipc_open_handle", "grkan_ipc_close_handle", "grkan_bwd_p2p",
+    "grkan_ipc_open_handle", "grkan_ipc_close_handle", "grkan_bwd_p2p", "grkan_bwd_terms",
 )
 IPC_HANDLE_BYTES = 64
 
@@ -109,6 +109,8 @@ def _declare(L):
     L.grkan_bwd_p2p.argtypes = [p, p, p, p, p, p, p, p, sz, i64, i32, i32, i32, i32, i32, u32, p, i32, i32,
                                 ctypes.c_uint64, p]
     L.grkan_bwd_p2p.restype = ctypes.c_int
+    L.grkan_bwd_terms.argtypes = [p, p, p, p, p, p, i64, i32, i32, i32, i32, i32, u32, p]
+    L.grkan_bwd_terms.restype = ctypes.c_int
 
 
 def lib():

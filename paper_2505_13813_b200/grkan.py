@@ -397,6 +397,61 @@ def elementwise_grads(x: float, upstream: float, numerator, denominator,
 
 
 # ---------------------------------------------------------------------------
+# Array-level helpers for one coefficient row (rational.py:218-278)
+# ---------------------------------------------------------------------------
+
+def _row_arrays(x, numerator, denominator):
+    x = np.asarray(x)
+    if x.dtype not in (np.float32, np.float64):
+        x = x.astype(np.float64)
+    dev = _device()
+    flat = torch.from_numpy(np.ascontiguousarray(x).reshape(1, -1)).to(dev)
+    cd = ops.coeff_dtype(flat.dtype)
+    a = torch.as_tensor(np.asarray(numerator, dtype=x.dtype).reshape(1, -1), dtype=cd, device=dev)
+    b = torch.as_tensor(np.asarray(denominator, dtype=x.dtype).reshape(1, -1), dtype=cd, device=dev)
+    return x, flat, a, b
+
+
+def rational_values(x: np.ndarray, numerator, denominator, exact: bool | None = None) -> np.ndarray:
+    """P(x) / Q(x) for one coefficient row, in x.dtype (rational.py:218-224)."""
+    x, flat, a, b = _row_arrays(x, numerator, denominator)
+    if flat.numel() == 0:
+        return np.empty_like(x)
+    y = ops.rational_forward(flat, a, b, exact=_exact(exact))
+    return y.cpu().numpy().reshape(x.shape)
+
+
+def gradient_terms(x: np.ndarray, upstream: np.ndarray, numerator, denominator, exact: bool | None = None):
+    """(d_x, da_terms, db_terms) per element for one coefficient row (rational.py:227-278).
+
+    Unreduced: da_terms[i] = u x^i / Q, db_terms[j] = -u sign(A) x^(j+1) P / Q^2,
+    in x.dtype.  EXACT (the shim's default) gives the reference's terms bit for
+    bit (grkan_bwd_terms).
+    """
+    x, flat, a, b = _row_arrays(x, numerator, denominator)
+    up = np.asarray(upstream, dtype=x.dtype)
+    if up.shape != x.shape:
+        raise GridGeometryError("grid geometry invalid: x and upstream shapes differ")
+    m1, n = a.shape[1], b.shape[1]
+    if flat.numel() == 0:
+        return np.empty_like(x), [np.empty_like(x) for _ in range(m1)], [np.empty_like(x) for _ in range(n)]
+    u = torch.from_numpy(np.ascontiguousarray(up).reshape(1, -1)).to(flat.device)
+    dx = torch.empty_like(flat)
+    terms = torch.empty((m1 + n, flat.numel()), dtype=a.dtype, device=flat.device)
+    from . import _native as N
+    with torch.cuda.device(flat.device):
+        rc = N.lib().grkan_bwd_terms(flat.data_ptr(), u.data_ptr(), a.data_ptr(), b.data_ptr(), dx.data_ptr(),
+                                     terms.data_ptr(), 1, flat.numel(), 1, m1, n, ops._DT[flat.dtype],
+                                     N.FLAG_EXACT if _exact(exact) else N.FLAG_FAST,
+                                     ops._stream(flat.device))
+        ops._raise(rc)
+    t = terms.cpu().numpy().astype(x.dtype, copy=False)
+    shape = x.shape
+    return (dx.cpu().numpy().reshape(shape), [t[i].reshape(shape) for i in range(m1)],
+            [t[m1 + j].reshape(shape) for j in range(n)])
+
+
+# ---------------------------------------------------------------------------
 # GRKB dumps (cli.py:104-129)
 # ---------------------------------------------------------------------------
 

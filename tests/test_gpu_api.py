@@ -8,6 +8,7 @@ import pytest
 import torch
 
 from grkan_testutil import sha
+from oracle import grkan_oracle as orc
 
 pytestmark = pytest.mark.gpu
 DEV = torch.device("cuda", 0) if torch.cuda.is_available() else None
@@ -418,3 +419,26 @@ def test_grkb_dump_of_gpu_dx_is_byte_identical(golden, tmp_path):
     ref = os.path.join(os.path.dirname(__file__), "golden", "dx_f32_2x4x16.grkb")
     assert out.read_bytes() == open(ref, "rb").read()
     assert np.array_equal(grkb.load(str(out)), b.d_x.data)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("degrees", [(5, 4), (3, 2), (5, 0)])
+def test_gradient_terms_bitwise_vs_reference_restatement(dtype, degrees):
+    """shim.gradient_terms (grkan_bwd_terms, EXACT) == the reference's per-element terms, bit for bit."""
+    from paper_2505_13813_b200 import grkan as shim
+    m, n = degrees
+    rng = np.random.default_rng(9 + m + n)
+    x = rng.standard_normal((3, 7, 11)).astype(dtype)
+    u = rng.standard_normal((3, 7, 11)).astype(dtype)
+    x.reshape(-1)[:3] = [0.0, -0.0, 2.0]
+    u.reshape(-1)[3] = -0.0
+    num = rng.standard_normal(m + 1)
+    den = rng.standard_normal(n)
+    dx, ta, tb = shim.gradient_terms(x, u, num, den)
+    rdx, rta, rtb = orc.element_terms(x, u, num, den)
+    assert dx.tobytes() == rdx.tobytes()
+    assert len(ta) == m + 1 and len(tb) == n
+    for got, ref in zip(ta + tb, rta + rtb):
+        assert got.dtype == ref.dtype and got.tobytes() == ref.tobytes()
+    y = shim.rational_values(x, num, den)
+    assert y.tobytes() == orc.rational(x, num, den).tobytes()
