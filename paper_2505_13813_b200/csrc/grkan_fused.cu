@@ -34,6 +34,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 
@@ -55,6 +56,9 @@ constexpr int kBK = 64;           // K per stage (one 128-byte swizzle row of bf
 constexpr int kSmemBudget = GRKAN_FUSED_SMEM_KB * 1024;  // operand ring + X tiles (the rest: alignment, barriers)
 constexpr int kKC = 10;           // coefficient terms (degrees (5, 4))
 constexpr int kMaxGroups = 64;    // coefficient table in shared memory
+#ifndef GRKAN_FUSED_PROBE_NOEPI
+#define GRKAN_FUSED_PROBE_NOEPI 0  // diagnostic only: backward epilogue skips the rational math
+#endif
 #ifndef GRKAN_FUSED_SK_BN
 #define GRKAN_FUSED_SK_BN 192     // short-K (X staged) tile width ...
 #endif
@@ -140,6 +144,52 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[CH]) {
   if constexpr (CH == 32) tmem_ld32(taddr, v); else tmem_ld16(taddr, v);
 }
 
+// ---- CTA-pair (cta_group::2) helpers --------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Both CTAs of the pair load into their own shared memory; the transaction
+// bytes land on the leader's (CTA 0's) barrier: clear the peer bit.
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// commit to the barrier at this offset in BOTH CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .b16 m;\n"
+      "mov.b16 m, 3;\n"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+// arrive on the leader CTA's copy of a barrier
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
 struct FusedGeom {
   int64_t M;
   int32_t N, K, ng, dg;
@@ -157,16 +207,24 @@ struct FusedGeom {
 // XS: the producer also TMA-streams each tile's X block [128 x BN] (64-column
 // 128B-swizzled boxes) into a double-buffered smem tile, so the epilogue reads
 // X with conflict-free LDS.128 instead of waiting on global loads.
-template <int BN, int ATOM, int ES, int CH, bool XS, int kStages>
+// PAIR: CTA pairs (cluster of 2) run tcgen05.mma.cta_group::2 on 256-row
+// tiles -- each CTA loads its 128 rows of dY and HALF of the W tile, the
+// leader issues the MMA over both shared memories, each CTA's TMEM receives
+// its 128 rows, and each CTA's epilogue drains its own.  Halves the W traffic
+// into each SM's shared memory (the long-K shape's limiter).
+template <int BN, int ATOM, int ES, int CH, bool XS, int kStages, bool PAIR = false>
 __global__ void __launch_bounds__(64 + 128 * ES, 1)
     k_linear_bwd_fused(const __grid_constant__ CUtensorMap map_dy, const __grid_constant__ CUtensorMap map_w,
                        const __grid_constant__ CUtensorMap map_x, const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ dx,
                        const float* __restrict__ ca, const float* __restrict__ cb, float* __restrict__ part,
                        FusedGeom geo) {
+  static_assert(!(PAIR && XS), "CTA pairs serve the long-K (unstaged X) shapes");
   constexpr int A_BYTES = kBM * kBK * 2;            // 16 KB
-  constexpr int B_BYTES = kBK * BN * 2;             // BN * 128 B
+  constexpr int B_BYTES = kBK * BN * 2 / (PAIR ? 2 : 1);  // BN * 128 B (half of it per CTA of a pair)
   constexpr int STAGE = A_BYTES + B_BYTES;
   constexpr int ATOM_BYTES = ATOM * 2 * kBK;        // one swizzle-atom column block
+  constexpr int B_BOXES = (PAIR ? BN / 2 : BN) / ATOM;
+  static_assert(!PAIR || (BN / 2) % ATOM == 0, "each CTA of a pair loads whole B atoms");
   constexpr uint32_t B_LAYOUT = ATOM == 64 ? 2u : 4u;      // SWIZZLE_128B / SWIZZLE_64B
   constexpr uint32_t B_SBO = ATOM * 2 * 8;                 // 8 K-rows of one atom
   constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
@@ -186,7 +244,12 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
   unsigned char* const xs = smem + kStages * STAGE;  // X tile buffers (XS)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t n_tiles = ((geo.M + kBM - 1) / kBM) * geo.n_tiles_n;
+  // PAIR: units are 256-row pair tiles walked by clusters; else 128-row tiles by CTAs
+  const uint32_t crank = PAIR ? cluster_ctarank() : 0;
+  const bool leader = crank == 0;
+  const int64_t unit0 = PAIR ? (blockIdx.x >> 1) : blockIdx.x;
+  const int64_t ustep = PAIR ? (gridDim.x >> 1) : gridDim.x;
+  const int64_t n_tiles = ((geo.M + (PAIR ? 2 : 1) * kBM - 1) / ((PAIR ? 2 : 1) * kBM)) * geo.n_tiles_n;
   const int kblocks = geo.K / kBK;
 
   if (threadIdx.x == 0) {
@@ -196,24 +259,31 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], NE);
+      mbar_init(&tempty[s], PAIR ? 2 * NE : NE);  // PAIR: both CTAs' epilogues drain into the leader's
       mbar_init(&xfull[s], 1);
       mbar_init(&xempty[s], NE);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {  // TMEM allocation (whole warp), base address to smem
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
-                 "n"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                   "n"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                   "n"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   for (int t = threadIdx.x; t < geo.ng * kKC; t += blockDim.x) {
     const int g = t / kKC, k = t - g * kKC;
     scoef[t] = k < 6 ? ca[g * 6 + k] : cb[g * 4 + (k - 6)];
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync_all(); else __syncthreads();  // barriers visible to the peer
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_d = tmem_base;
 
@@ -225,9 +295,9 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
       uint32_t phase = 0;
       int64_t it = 0;
       int i = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++i) {
+      for (int64_t tile = unit0; tile < n_tiles; tile += ustep, ++i) {
         const int n0 = static_cast<int>(tile % geo.n_tiles_n) * BN;
-        const int m0 = static_cast<int>((tile / geo.n_tiles_n) * kBM);
+        const int m0 = static_cast<int>((tile / geo.n_tiles_n) * (PAIR ? 2 : 1) * kBM + crank * kBM);
         if constexpr (XS) {  // the tile's X block, into buffer i & 1
           const int xb = i & 1;
           mbar_wait(&xempty[xb], ((i >> 1) & 1) ^ 1);
@@ -239,10 +309,18 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
           if (it >= kStages) mbar_wait(&empty[slot], phase ^ 1);
           unsigned char* sa = smem + slot * STAGE;
           unsigned char* sb = sa + A_BYTES;
-          mbar_arrive_expect_tx(&full[slot], STAGE);
-          tma_load_2d(sa, &map_dy, kb * kBK, m0, &full[slot]);
+          if constexpr (PAIR) {
+            if (leader) mbar_arrive_expect_tx(&full[slot], 2 * STAGE);  // both CTAs' bytes
+            tma_load_2d_pair(sa, &map_dy, kb * kBK, m0, &full[slot]);
 #pragma unroll
-          for (int a = 0; a < BN / ATOM; ++a) tma_load_2d(sb + a * ATOM_BYTES, &map_w, n0 + a * ATOM, kb * kBK, &full[slot]);
+            for (int a = 0; a < B_BOXES; ++a)
+              tma_load_2d_pair(sb + a * ATOM_BYTES, &map_w, n0 + crank * (BN / 2) + a * ATOM, kb * kBK, &full[slot]);
+          } else {
+            mbar_arrive_expect_tx(&full[slot], STAGE);
+            tma_load_2d(sa, &map_dy, kb * kBK, m0, &full[slot]);
+#pragma unroll
+            for (int a = 0; a < B_BOXES; ++a) tma_load_2d(sb + a * ATOM_BYTES, &map_w, n0 + a * ATOM, kb * kBK, &full[slot]);
+          }
           if (++slot == kStages) {
             slot = 0;
             phase ^= 1;
@@ -251,12 +329,13 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer
-      const uint32_t idesc = instr_desc<BN>();
+    if (lane == 0 && leader) {  // ---- MMA issuer (the pair's leader issues for both CTAs)
+      const uint32_t idesc = PAIR ? (instr_desc<BN>() & ~(31u << 24)) | (static_cast<uint32_t>(2 * kBM >> 4) << 24)
+                                  : instr_desc<BN>();
       int slot = 0;
       uint32_t phase = 0;
       int i = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++i) {
+      for (int64_t tile = unit0; tile < n_tiles; tile += ustep, ++i) {
         const int acc = i & 1;
         mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);  // epilogue has drained this buffer
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -272,15 +351,24 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
             const uint64_t ad = smem_desc(sa + k * 32, 16, 1024, 2);
             // B: MN-major, K step = two 8-row groups
             const uint64_t bd = smem_desc(sb + k * 2 * B_SBO, ATOM_BYTES, B_SBO, B_LAYOUT);
-            umma_bf16(dcol, ad, bd, idesc, (kb | k) != 0);
+            if constexpr (PAIR)
+              umma_bf16_pair(dcol, ad, bd, idesc, (kb | k) != 0);
+            else
+              umma_bf16(dcol, ad, bd, idesc, (kb | k) != 0);
           }
-          umma_commit(&empty[slot]);  // frees the stage when these MMAs complete
+          if constexpr (PAIR)
+            umma_commit_pair(&empty[slot]);  // frees the stage in both CTAs
+          else
+            umma_commit(&empty[slot]);  // frees the stage when these MMAs complete
           if (++slot == kStages) {
             slot = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if constexpr (PAIR)
+          umma_commit_pair(&tfull[acc]);
+        else
+          umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
       }
     }
   } else {
@@ -292,10 +380,10 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
     int i = 0;
     int g_loaded = -1;
     RationalX2<false> rp;  // the warp's column block lies in one group (CW | dg)
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++i) {
+    for (int64_t tile = unit0; tile < n_tiles; tile += ustep, ++i) {
       const int acc = i & 1;
       const int n0 = static_cast<int>(tile % geo.n_tiles_n) * BN;
-      const int64_t m_tile = tile / geo.n_tiles_n;
+      const int64_t m_tile = (tile / geo.n_tiles_n) * (PAIR ? 2 : 1) + crank;  // 128-row tile index
       const int64_t grow = m_tile * kBM + row;
       const bool live = grow < geo.M;
       const int c0 = n0 + cs * CW;
@@ -346,9 +434,14 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
         if (c + 1 == CW / CH) {          // this warp is done with the accumulator buffer
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) {
+            if constexpr (PAIR)
+              mbar_arrive_leader(&tempty[acc]);
+            else
+              mbar_arrive(&tempty[acc]);
+          }
         }
-        if (live) {
+        if (live && !GRKAN_FUSED_PROBE_NOEPI) {
           uint4 o4[NV];
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
@@ -376,10 +469,14 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync_all(); else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "n"(TMEM_COLS) : "memory");
+  if (warp == 1) {
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "n"(TMEM_COLS) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "n"(TMEM_COLS) : "memory");
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -671,6 +768,40 @@ cudaError_t launch_t(const CUtensorMap& mdy, const CUtensorMap& mw, const CUtens
   return cudaGetLastError();
 }
 
+// CTA-pair launch (cluster of 2, cta_group::2 MMA on 256-row tiles).
+template <int BN, int ATOM, int ES, int CH>
+cudaError_t launch_pair_t(const CUtensorMap& mdy, const CUtensorMap& mw, const CUtensorMap& mx, const void* x,
+                          void* dx, const float* a, const float* b, float* part, const FusedGeom& geo,
+                          cudaStream_t s) {
+  constexpr int kStageBytes = kBM * kBK * 2 + kBK * BN;  // A + half of B
+  constexpr int kSt = kSmemBudget / kStageBytes > 8 ? 8 : kSmemBudget / kStageBytes;
+  constexpr size_t smem = static_cast<size_t>(kSt) * kStageBytes + 1024;
+  auto kern = k_linear_bwd_fused<BN, ATOM, ES, CH, false, kSt, true>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const int64_t pair_tiles = ((geo.M + 2 * kBM - 1) / (2 * kBM)) * geo.n_tiles_n;
+  const int64_t pairs = pair_tiles < sms_of_device() / 2 ? pair_tiles : sms_of_device() / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+  cfg.blockDim = dim3(64 + 128 * ES);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, mdy, mw, mx, static_cast<const __nv_bfloat16*>(x),
+                            static_cast<__nv_bfloat16*>(dx), a, b, part, geo);
+}
+
+bool pair_enabled() {
+  const char* v = getenv("GRKAN_FUSED_PAIR");
+  return v && v[0] == '1';
+}
+
 #ifndef GRKAN_FUSED_FWD_NT
 #define GRKAN_FUSED_FWD_NT 16
 #endif
@@ -764,6 +895,13 @@ int grkan_linear_bwd(const void* dy, const void* w, const void* x, const void* a
   if (ts.bn == BN_ && ts.atom == AT_ && ts.es == ES_ && ts.ch == CH_ && ts.xs == XS_)           \
     e = launch_t<BN_, AT_, ES_, CH_, XS_>(mdy, mw, mx, x, dx, fa, fb, part, geo, tiles, s);    \
   else
+  if (!ts.xs && ts.bn == 192 && ts.es == 4 && ts.ch == 16 && pair_enabled()) {
+    // each CTA of the pair loads 96 of the 192 W columns: 64B-swizzle, 32-column atoms
+    CUtensorMap mw32;
+    if (!make_map(&mw32, w, static_cast<uint64_t>(N), static_cast<uint64_t>(K), 32, kBK, CU_TENSOR_MAP_SWIZZLE_64B))
+      return grkan::set_error(GRKAN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    e = launch_pair_t<192, 32, 4, 16>(mdy, mw32, mx, x, dx, fa, fb, part, geo, s);
+  } else
   GRKAN_FUSED_CASE(256, 64, 4, 16, false)
   GRKAN_FUSED_CASE(192, 64, 4, 16, false)
   GRKAN_FUSED_CASE(256, 64, 2, 32, false)

@@ -147,3 +147,18 @@ def test_fused_forward_matches_unfused_chain(M, K, N, ng, with_bias):
         f64 = orc.forward(xs, a.double().cpu().numpy(), b.double().cpu().numpy())[0]
         y64 = f64 @ w.double().cpu().numpy().T + (bias.double().cpu().numpy() if with_bias else 0.0)
         assert orc.matrix_rel(y.double().cpu().numpy(), y64) <= 2e-2
+
+
+def test_cta_pair_path_matches(monkeypatch):
+    """GRKAN_FUSED_PAIR=1: the long-K shape on CTA pairs (cluster of 2, tcgen05.mma.cta_group::2,
+    each CTA loading half of the W tile) gives the single-CTA kernel's results."""
+    from paper_2505_13813_b200 import ops
+    x, dy, w, a, b = _inputs(512, 768, 3072, 8, seed=21)
+    monkeypatch.delenv("GRKAN_FUSED_PAIR", raising=False)
+    dx1, da1, db1 = ops.linear_backward_fused(dy, w, x, a, b)
+    monkeypatch.setenv("GRKAN_FUSED_PAIR", "1")
+    dx2, da2, db2 = ops.linear_backward_fused(dy, w, x, a, b, check_overflow=True)
+    # same dF up to fp32 summation order inside the tensor core -> bf16 dx within one ulp-ish
+    assert orc.matrix_rel(dx2.float().cpu().numpy(), dx1.float().cpu().numpy()) <= 1e-2
+    assert orc.matrix_rel(da2.cpu().numpy(), da1.cpu().numpy()) <= 1e-4
+    assert orc.matrix_rel(db2.cpu().numpy(), db1.cpu().numpy()) <= 1e-4
