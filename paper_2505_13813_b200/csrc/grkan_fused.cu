@@ -62,6 +62,9 @@ constexpr int kMaxGroups = 64;    // coefficient table in shared memory
 #ifndef GRKAN_FUSED_SK_BN
 #define GRKAN_FUSED_SK_BN 192     // short-K (X staged) tile width ...
 #endif
+#ifndef GRKAN_FUSED_SK_CH
+#define GRKAN_FUSED_SK_CH 16      // ... and TMEM columns per epilogue load
+#endif
 #ifndef GRKAN_FUSED_SK_ES
 #define GRKAN_FUSED_SK_ES 3       // ... and epilogue warps per TMEM lane quadrant
 #endif
@@ -139,9 +142,22 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 lanes x 8 columns.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 template <int CH>
 __device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[CH]) {
-  if constexpr (CH == 32) tmem_ld32(taddr, v); else tmem_ld16(taddr, v);
+  if constexpr (CH == 32) tmem_ld32(taddr, v);
+  else if constexpr (CH == 16) tmem_ld16(taddr, v);
+  else tmem_ld8(taddr, v);
 }
 
 // ---- CTA-pair (cta_group::2) helpers --------------------------------------
@@ -404,7 +420,7 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
       if constexpr (XS) mbar_wait(&xfull[acc], (i >> 1) & 1);
       // accumulators: float2 (packed FFMA2) when the register budget allows
       // (ES <= 3: <= 14 warps, 128 registers), else one float per coefficient
-      using AccT = std::conditional_t<(ES <= 3), float2, float>;
+      using AccT = std::conditional_t<(ES <= 3 || CH <= 8), float2, float>;
       AccT sacc[kKC];
 #pragma unroll
       for (int k = 0; k < kKC; ++k) sacc[k] = AccT{};
@@ -461,7 +477,7 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
 #pragma unroll
       for (int k = 0; k < kKC; ++k) {
         float v;
-        if constexpr (ES <= 3) v = sacc[k].x + sacc[k].y; else v = sacc[k];
+        if constexpr (ES <= 3 || CH <= 8) v = sacc[k].x + sacc[k].y; else v = sacc[k];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0) part[(static_cast<int64_t>(g) * kKC + k) * geo.ppg + t] = v;
@@ -724,7 +740,8 @@ constexpr TileShape kShapesLongK[] = {{256, 64, 4, 16, false}, {192, 64, 4, 16, 
                                       {192, 64, 2, 32, false}, {128, 64, 4, 16, false}, {128, 64, 2, 32, false},
                                       {96, 32, 1, 32, false},  {64, 64, 2, 32, false},  {64, 64, 1, 32, false},
                                       {32, 32, 1, 32, false}};
-constexpr TileShape kShapesShortK[] = {{GRKAN_FUSED_SK_BN, 64, GRKAN_FUSED_SK_ES, 16, true}, {128, 64, 4, 16, true},
+constexpr TileShape kShapesShortK[] = {{GRKAN_FUSED_SK_BN, 64, GRKAN_FUSED_SK_ES, GRKAN_FUSED_SK_CH, true},
+                                       {128, 64, 4, 16, true},
                                        {64, 64, 2, 32, true}, {96, 32, 1, 32, false},
                                        {32, 32, 1, 32, false}};
 
@@ -735,7 +752,7 @@ bool pick_shape(int N, int dg, int K, TileShape* out) {
   for (int i = 0; i < n; ++i) {
     const TileShape& t = list[i];
     const int cw = t.bn / t.es;
-    if (N % t.bn == 0 && cw % t.ch == 0 && cw % 16 == 0 && dg % cw == 0) {
+    if (N % t.bn == 0 && cw % t.ch == 0 && cw % 8 == 0 && dg % cw == 0) {
       *out = t;
       return true;
     }
@@ -912,8 +929,8 @@ int grkan_linear_bwd(const void* dy, const void* w, const void* x, const void* a
   GRKAN_FUSED_CASE(64, 64, 2, 32, false)
   GRKAN_FUSED_CASE(64, 64, 1, 32, false)
   GRKAN_FUSED_CASE(128, 64, 4, 16, true)
-#if GRKAN_FUSED_SK_BN != 128 || GRKAN_FUSED_SK_ES != 4
-  GRKAN_FUSED_CASE(GRKAN_FUSED_SK_BN, 64, GRKAN_FUSED_SK_ES, 16, true)
+#if GRKAN_FUSED_SK_BN != 128 || GRKAN_FUSED_SK_ES != 4 || GRKAN_FUSED_SK_CH != 16
+  GRKAN_FUSED_CASE(GRKAN_FUSED_SK_BN, 64, GRKAN_FUSED_SK_ES, GRKAN_FUSED_SK_CH, true)
 #endif
   GRKAN_FUSED_CASE(64, 64, 2, 32, true)
   e = launch_t<32, 32, 1, 32, false>(mdy, mw, mx, x, dx, fa, fb, part, geo, tiles, s);
