@@ -1,6 +1,8 @@
 """Host-side logic that needs no GPU: the reference-API shim's types and checks,
 presets, error mapping, and that the product path refuses to run without CUDA."""
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -158,3 +160,31 @@ def test_grkb_reads_and_writes_reference_dumps(golden, tmp_path):
         grkb.dumps(np.zeros((2, 2), np.float32))
     with pytest.raises(ValueError):
         grkb.dumps(np.zeros((1, 1, 2), np.int32))
+
+
+def test_missing_library_fails_loudly():
+    """No CUDA extension -> NativeLibraryError at the first call; nothing falls back to a CPU path."""
+    import subprocess
+    import sys
+    code = ("import torch\n"
+            "from paper_2505_13813_b200 import _native as N, ops\n"
+            "try:\n"
+            "    N.lib()\n"
+            "except N.NativeLibraryError as e:\n"
+            "    print('raised', e)\n")
+    env = dict(os.environ, GRKAN_LIB="/nonexistent/libgrkan_b200.so")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=300)
+    assert out.returncode == 0, out.stderr
+    assert "raised" in out.stdout and "not built" in out.stdout
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_fused_and_parallel_paths_have_no_cpu_fallback():
+    from paper_2505_13813_b200 import ops
+    x = torch.randn(4, 256).to(torch.bfloat16)
+    with pytest.raises(errors.UnsupportedError):
+        ops.linear_backward_fused(torch.randn(4, 64).to(torch.bfloat16), torch.randn(64, 256).to(torch.bfloat16),
+                                  x, torch.randn(2, 6), torch.randn(2, 4))
+    with pytest.raises(errors.UnsupportedError):
+        ops.linear_forward_fused(x, torch.randn(64, 256).to(torch.bfloat16), torch.randn(2, 6), torch.randn(2, 4))
