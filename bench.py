@@ -13,7 +13,9 @@ full KAT-B batch (B=256), so per-GPU work is fixed as N grows.
 ``value``  elements/s over all ranks, inputs already resident in HBM, device
            time (CUDA events) max over ranks.  Warm-up: >= W steps and >= 150 ms;
            the timed K steps are enqueued behind a short device-side spin
-           (--hold-ms) so host launch jitter cannot open gaps inside them.
+           (--hold-ms) so host launch jitter cannot open gaps inside them;
+           NVML clocks are then sampled by the (idle) host thread from the
+           first timed step to the last.
            ``--collective`` picks the da/db exchange for N > 1 (NCCL
            all-reduce on a side stream, the world-size-invariant block path,
            or the peer-memory fused reduce); its time is ``kernels.collective_us``.
@@ -70,7 +72,7 @@ def parse_args(argv=None):
     p.add_argument("--mode", choices=("fast", "exact"), default="fast")
     p.add_argument("--scaling", choices=("weak", "strong"), default="weak")
     p.add_argument("--e2e-steps", type=int, default=None)
-    p.add_argument("--hold-ms", type=float, default=20.0,
+    p.add_argument("--hold-ms", type=float, default=8.0,
                    help="device-side spin before the timed region while the host enqueues it")
     p.add_argument("--collective", choices=("allreduce", "deterministic", "p2p"), default="allreduce",
                    help="da/db exchange: NCCL all-reduce of the 320 B da||db; the world-size-invariant "
@@ -196,6 +198,7 @@ class ClockSampler:
 
     def __init__(self, index):
         self.samples = []
+        self.power_mw = []
         self.reasons = 0
         self.max_mhz = None
         self._stop = threading.Event()
@@ -212,12 +215,30 @@ class ClockSampler:
     def _run(self):
         nv = self._nv
         while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
-                self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
-            except Exception:
-                pass
+            self._sample()
             time.sleep(0.002)
+
+    def _sample(self):
+        nv = self._nv
+        try:
+            self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+            self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
+            self.power_mw.append(nv.nvmlDeviceGetPowerUsage(self._h))
+        except Exception:
+            pass
+
+    def poll_until(self, begin, end, period_s=0.0005):
+        """Sample in the calling thread from when the device reaches event `begin`
+        until it completes event `end` (host otherwise idle)."""
+        if self._nv is None:
+            return
+        while not begin.query():
+            time.sleep(period_s / 4)
+        while not end.query():
+            self._sample()
+            time.sleep(period_s)
+        if not self.samples:
+            self._sample()
 
     def start(self):
         if self._nv is not None:
@@ -233,8 +254,14 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
         reasons = [name for bit, name in self.REASONS.items() if self.reasons & bit and bit != 0x1]
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": reasons, "samples": len(self.samples)}
+        out = {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+               "reasons": reasons, "reasons_mask": hex(self.reasons), "samples": len(self.samples)}
+        try:  # power draw vs the enforced limit: a power-capped run shows median power at the limit
+            out["power_w_median"] = statistics.median(self.power_mw) / 1e3 if self.power_mw else None
+            out["power_limit_w"] = self._nv.nvmlDeviceGetEnforcedPowerLimit(self._h) / 1e3
+        except Exception:
+            pass
+        return out
 
 
 # ---------------------------------------------------------------------------
@@ -377,6 +404,14 @@ def run_b200(args, rank, world, local_rank):
             torch.cuda.synchronize()
     join_comm()
     torch.cuda.synchronize()
+    # host cost of enqueueing one step (events included), to size the hold below
+    t_h = time.perf_counter()
+    for _ in range(4):
+        e_tmp = torch.cuda.Event(enable_timing=True)
+        e_tmp.record(stream)
+        fwd(); bwd(); allreduce()
+    host_step_ms = (time.perf_counter() - t_h) / 4 * 1e3
+    torch.cuda.synchronize()
 
     K = args.steps
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
@@ -386,10 +421,11 @@ def run_b200(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler.start()
     # hold the stream with a short device-side spin while the host enqueues all
     # K steps, so host-side jitter cannot open launch gaps inside the timed region
-    torch.cuda._sleep(int(args.hold_ms * 1e-3 * 1.965e9))
+    hold_ms = max(args.hold_ms, 2.0 * K * host_step_ms + 2.0)
+    torch.cuda._sleep(int(hold_ms * 1e-3 * 1.965e9))
+    t_enq = time.perf_counter()
     t_start.record(stream)
     for k in range(K):
         ev[k][0].record(stream)
@@ -402,8 +438,11 @@ def run_b200(args, rank, world, local_rank):
     if args.collective == "allreduce":
         join_comm()
     t_end.record(stream)
+    host_enqueue_ms = (time.perf_counter() - t_enq) * 1e3
+    # the host is idle now: sample the clocks from this thread until the timed
+    # region has drained (only while the device is past the hold)
+    sampler.poll_until(t_start, t_end)
     torch.cuda.synchronize()
-    sampler.stop()
     if world > 1:
         dist.barrier()
     ms_total = t_start.elapsed_time(t_end)
@@ -516,7 +555,10 @@ def run_b200(args, rank, world, local_rank):
     fwd_gbs = fwd_bytes / (fwd_ms / 1e3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-        "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_ci95": ci95_ms, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_ci95": ci95_ms,
+        "timing": {"hold_ms": hold_ms, "host_enqueue_ms": host_enqueue_ms,
+                   "note": "timed steps enqueued behind a device-side hold longer than the host enqueue"},
+        "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f32" if args.dtype == "fp32" else "bf16-io/f32-math",
         "data": "synthetic: x, dy ~ N(0,1) (torch seeded per rank), coefficients ~ N(0,1) "
