@@ -63,7 +63,7 @@ FALLBACK_HBM_GBS = 6650.0
 def parse_args(argv=None):
     p = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--steps", type=int, default=100)  # repeats 100, as the paper and run_bench (cli.py:73-74)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=("b200", "reference"), default="b200")
     p.add_argument("--dtype", choices=("fp32", "bf16"), default="fp32")
