@@ -848,7 +848,10 @@ size_t grkan_linear_bwd_workspace_bytes(int64_t M, int32_t N, int32_t K, int32_t
   if (M < 0 || N < 1 || K < 1 || n_groups < 1 || N % n_groups) return 0;
   grkan::fused::TileShape t;
   if (!grkan::fused::pick_shape(N, N / n_groups, K, &t)) return 0;
-  const int64_t ppg = ((M + grkan::fused::kBM - 1) / grkan::fused::kBM) * ((N / n_groups) / (t.bn / t.es)) * 4;
+  // 128-row tiles, rounded up to an even count: CTA pairs cover 256 rows and the
+  // second CTA of a ragged last pair writes (zero) partials for its tile too
+  const int64_t m_tiles = 2 * ((M + 2 * grkan::fused::kBM - 1) / (2 * grkan::fused::kBM));
+  const int64_t ppg = m_tiles * ((N / n_groups) / (t.bn / t.es)) * 4;
   const size_t part = static_cast<size_t>(n_groups) * grkan::fused::kKC * ppg * sizeof(float);
   return 256 + ((part + 255) / 256) * 256;
 }
@@ -902,7 +905,11 @@ int grkan_linear_bwd(const void* dy, const void* w, const void* x, const void* a
   geo.dg = dg;
   geo.n_tiles_n = N / ts.bn;
   const int64_t m_tiles = (M + kBM - 1) / kBM;
-  geo.ppg = static_cast<int32_t>(m_tiles * (dg / (ts.bn / ts.es)) * 4);
+  // CTA pairs write partials for an even number of 128-row tiles (the second
+  // CTA of a ragged last pair contributes zeros); the workspace covers both
+  const bool pair = !ts.xs && ts.bn == 192 && ts.es == 4 && ts.ch == 16 && pair_enabled();
+  const int64_t m_slots = pair ? 2 * ((M + 2 * kBM - 1) / (2 * kBM)) : m_tiles;
+  geo.ppg = static_cast<int32_t>(m_slots * (dg / (ts.bn / ts.es)) * 4);
   geo.one = 1.0f;
   const int64_t tiles = m_tiles * geo.n_tiles_n;
   float* part = reinterpret_cast<float*>(static_cast<char*>(ws) + 256);
@@ -912,7 +919,7 @@ int grkan_linear_bwd(const void* dy, const void* w, const void* x, const void* a
   if (ts.bn == BN_ && ts.atom == AT_ && ts.es == ES_ && ts.ch == CH_ && ts.xs == XS_)           \
     e = launch_t<BN_, AT_, ES_, CH_, XS_>(mdy, mw, mx, x, dx, fa, fb, part, geo, tiles, s);    \
   else
-  if (!ts.xs && ts.bn == 192 && ts.es == 4 && ts.ch == 16 && pair_enabled()) {
+  if (pair) {
     // each CTA of the pair loads 96 of the 192 W columns: 64B-swizzle, 32-column atoms
     CUtensorMap mw32;
     if (!make_map(&mw32, w, static_cast<uint64_t>(N), static_cast<uint64_t>(K), 32, kBK, CU_TENSOR_MAP_SWIZZLE_64B))

@@ -149,11 +149,12 @@ def test_fused_forward_matches_unfused_chain(M, K, N, ng, with_bias):
         assert orc.matrix_rel(y.double().cpu().numpy(), y64) <= 2e-2
 
 
-def test_cta_pair_path_matches(monkeypatch):
+@pytest.mark.parametrize("M", [512, 300, 130])
+def test_cta_pair_path_matches(monkeypatch, M):
     """GRKAN_FUSED_PAIR=1: the long-K shape on CTA pairs (cluster of 2, tcgen05.mma.cta_group::2,
     each CTA loading half of the W tile) gives the single-CTA kernel's results."""
     from paper_2505_13813_b200 import ops
-    x, dy, w, a, b = _inputs(512, 768, 3072, 8, seed=21)
+    x, dy, w, a, b = _inputs(M, 768, 3072, 8, seed=21)  # ragged last pair tile at M = 300, 130
     monkeypatch.delenv("GRKAN_FUSED_PAIR", raising=False)
     dx1, da1, db1 = ops.linear_backward_fused(dy, w, x, a, b)
     monkeypatch.setenv("GRKAN_FUSED_PAIR", "1")
