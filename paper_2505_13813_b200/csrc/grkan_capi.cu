@@ -430,11 +430,9 @@ int grkan_bwd_p2p(const void* x, const void* dy, const void* a, const void* b, v
     L.stream = s;
     e = launch("bwd", dtype, L);
     if (e != cudaSuccess) return cuda_fail(e, "k_bwd (partials) launch");
-  } else {  // an empty shard still takes part in the exchange, with zero partials
-    e = cudaMemsetAsync(static_cast<char*>(ws) + 256, 0, need - 256, s);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(partials)");
   }
-  const int64_t n_tiles = rows > 0 ? p.geo.n_tiles : 1;
+  // an empty shard still takes part in the exchange: no partials, a zero fold
+  const int64_t n_tiles = rows > 0 ? p.geo.n_tiles : 0;
   e = grkan::launch_reduce_p2p(dtype, static_cast<char*>(ws) + 256, n_tiles, n_groups, m1, n, peer_bufs, rank, world,
                                epoch, da, db, st, s);
   if (e != cudaSuccess) return cuda_fail(e, "k_bwd_reduce_p2p launch");

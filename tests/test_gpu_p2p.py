@@ -98,3 +98,20 @@ def test_peer_exchange_single_rank_matches_k3():
             assert torch.equal(da, da0) and torch.equal(db, db0)
     finally:
         ex.close()
+
+
+def test_peer_exchange_empty_shard():
+    """A rank with no rows still joins the exchange and contributes zeros."""
+    from paper_2505_13813_b200 import parallel
+    dev = torch.device("cuda", 0)
+    ex = parallel.PeerExchange(8, 6, 4, dev)
+    try:
+        x = torch.empty((0, 384), device=dev)
+        a = torch.randn(8, 6, device=dev)
+        b = torch.randn(8, 4, device=dev)
+        for _ in range(2):
+            dx, da, db = ex.backward(x, x, a, b, check_overflow=True)
+            assert dx.shape == (0, 384)
+            assert float(da.abs().sum()) == 0.0 and float(db.abs().sum()) == 0.0
+    finally:
+        ex.close()
