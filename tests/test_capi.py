@@ -3,7 +3,6 @@
 CPU-only: nothing here launches a kernel.
 """
 
-import ctypes
 import glob
 import os
 import re

@@ -9,7 +9,6 @@ max-scaled <= 1e-2 (north_star's bf16 bar); da/db max-scaled <= 1e-4 vs the
 fp32 chain (dF summation order differs) and <= 1e-5 vs fp64.
 """
 
-import numpy as np
 import pytest
 import torch
 
