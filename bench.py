@@ -327,13 +327,17 @@ def run_b200(args, rank, world, local_rank):
     # da||db all-reduce on a side stream: it overlaps the next step's forward
     # (the next K3 waits for it before overwriting the buffer); the timed
     # region ends only after the last one completes.
-    comm = torch.cuda.Stream(dev) if world > 1 else None
+    # (NCCL only: gloo -- several ranks sharing one GPU in tests -- stages CUDA
+    # tensors through the host and runs in stream order on the main stream)
+    comm = torch.cuda.Stream(dev) if world > 1 and args.dist_backend == "nccl" else None
     bwd_done = torch.cuda.Event()
 
     comm_ev = []  # (start, end) on the comm stream, timed steps only
 
     def allreduce(timed=False):
-        if world > 1:
+        if world > 1 and comm is None:
+            dist.all_reduce(grads)
+        elif world > 1:
             bwd_done.record(stream)
             comm.wait_event(bwd_done)
             with torch.cuda.stream(comm):
@@ -457,6 +461,17 @@ def run_b200(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total, fwd_ms, bwd_ms, coll_ms = t.tolist()
     ms_step = ms_total / K
+    # after the timed region: every rank must hold the same da||db (the
+    # deterministic and peer-memory paths bitwise by construction)
+    coll_check = None
+    if world > 1:
+        torch.cuda.synchronize()
+        mine = grads.detach().cpu()
+        allg = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather_object(allg, mine)
+        same = all(torch.equal(g, allg[0]) for g in allg)
+        coll_check = {"ranks": world, "bitwise_identical": same,
+                      "max_abs_diff": max(float((g - allg[0]).abs().max()) for g in allg)}
     # per-step device times (fwd start -> after the step's exchange): mean +- CI95
     # with the normal approximation, as the reference reports (verification.py:344-349)
     step_ms = [e[0].elapsed_time(e[3]) for e in ev]
@@ -576,6 +591,7 @@ def run_b200(args, rank, world, local_rank):
             "fwd_traffic": ncu_traffic(args, "fwd"),
             "bwd_us": bwd_ms * 1e3, "bwd_gbs": bwd_gbs, "bwd_frac": bwd_gbs / peak,
             "collective": args.collective, "collective_us": coll_ms * 1e3,
+            "collective_check": coll_check,
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * es * E,
                 "d2h_bytes_per_step": 2 * es * E + 4 * groups * (M1 + NDEN),
