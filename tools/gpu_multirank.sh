@@ -8,3 +8,8 @@ for c in ${COLLECTIVES:-allreduce deterministic p2p}; do
     --collective $c --no-cpu-baseline --e2e-steps 1 > gpurun_out/multirank_$c.json 2> gpurun_out/multirank_$c.err
   echo "$c rc=$?"; tail -c 600 gpurun_out/multirank_$c.json; grep -i "error\|Traceback" gpurun_out/multirank_$c.err | head -5
 done
+# the DDP training step (config 4 path) with two ranks, KAT-T
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+  --master-port $((29500 + RANDOM % 1000)) bench.py --config kat-t-train --gpus 2 --steps 5 --warmup 3 \
+  --dist-backend gloo > gpurun_out/multirank_train.json 2> gpurun_out/multirank_train.err
+echo "train rc=$?"
