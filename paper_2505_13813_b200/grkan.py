@@ -363,6 +363,43 @@ def run_backward(x, upstream, params, plan: ExecutionPlan, workers: int = 1,
                             validate=validate, counter=counter, coverage=coverage, exact=exact)
 
 
+def combine_partials(partials, num_groups: int, mode: str = COMBINE_ORDERED):
+    """Fold per-block partials into per-group totals (backward.py:142-179), on the GPU.
+
+    ``partials``: (block_id, numerator_partials, denominator_partials) with
+    block_id = row_block * num_groups + group; every id in 0..len-1 exactly once
+    (else PartialCoverageError, as the reference).  The fold is K3
+    (grkan_reduce_partials): fp64, in ascending block order for BOTH modes --
+    the reference's ``unordered_scatter`` folds in submission order, which
+    only changes rounding, so here it reproduces the ordered result (the
+    reference's own test only asserts it runs, test_backward.py).  Results are
+    the fixed-order fp64 sums cast to the partials' dtype, not the reference's
+    left-to-right sums in that dtype.
+    """
+    if mode not in (COMBINE_ORDERED, COMBINE_UNORDERED):
+        raise ValueError("unknown combine mode %r" % (mode,))
+    if not partials:
+        raise PartialCoverageError("partial coverage violation: no partials")
+    ids = [int(p[0]) for p in partials]
+    if sorted(ids) != list(range(len(partials))):
+        raise PartialCoverageError("partial coverage violation")
+    first_a = np.asarray(partials[0][1])
+    first_b = np.asarray(partials[0][2])
+    num_w, den_w = first_a.shape[0], first_b.shape[0]
+    for _, pa, pb in partials:
+        if np.asarray(pa).shape != (num_w,) or np.asarray(pb).shape != (den_w,):
+            raise PartialCoverageError("partial coverage violation: inconsistent shapes")
+    dtype = first_a.dtype if first_a.dtype in (np.float32, np.float64) else np.float64
+    n_blk = -(-len(partials) // num_groups)
+    host = np.zeros((n_blk * num_groups, num_w + den_w), dtype=dtype)  # missing tail slots fold as 0
+    for bid, pa, pb in partials:
+        host[bid, :num_w] = pa
+        host[bid, num_w:] = pb
+    part = torch.from_numpy(host.reshape(n_blk, num_groups, num_w + den_w)).to(_device())
+    da, db = ops.reduce_partials(part, num_w, den_w)
+    return da.cpu().numpy(), db.cpu().numpy()
+
+
 # ---------------------------------------------------------------------------
 # Scalar entry points (rational.py:285-310): one-element fp64 tensors on the GPU
 # ---------------------------------------------------------------------------
