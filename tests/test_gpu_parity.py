@@ -263,3 +263,52 @@ def test_full_size_properties_kat_b():
     assert torch.equal(da2, da1 * 2) and torch.equal(db2, db1 * 2)
     dx3, da3, db3 = ops().rational_backward(xd, ud, a, b, exact=True)
     assert torch.equal(dx3, dx1) and torch.equal(da3, da1) and torch.equal(db3, db1)
+
+
+def _terms64(x, u, a, b, ng, chunk_rows=4096):
+    """fp64 sums of the EXACT per-element terms (bitwise the reference's), chunked."""
+    from paper_2505_13813_b200 import _native as N
+    rows, d = x.shape
+    acc = torch.zeros(10, ng, dtype=torch.float64, device=x.device)
+    dxc = torch.empty(chunk_rows, d, dtype=x.dtype, device=x.device)
+    t = torch.empty(10 * chunk_rows * d, dtype=torch.float32, device=x.device)
+    dt = N.DT_BF16 if x.dtype == torch.bfloat16 else N.DT_F32
+    for r0 in range(0, rows, chunk_rows):
+        r = min(chunk_rows, rows - r0)
+        rc = N.lib().grkan_bwd_terms(x[r0].data_ptr(), u[r0].data_ptr(), a.data_ptr(), b.data_ptr(),
+                                     dxc.data_ptr(), t.data_ptr(), r, d, ng, 6, 4, dt, N.FLAG_EXACT,
+                                     torch.cuda.current_stream().cuda_stream)
+        assert rc == 0, N.last_error()
+        acc += t[:10 * r * d].view(10, r, ng, d // ng).double().sum(dim=(1, 3))
+    return acc[:6].T, acc[6:].T
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_more_than_2_31_elements(dtype):
+    """Maximum sizes: E > 2^31 elements (64-bit indexing in every kernel).  Rows
+    past the 2^31 boundary must equal, bit for bit, the same rows computed as a
+    small tensor of their own (EXACT is elementwise); da/db within 1e-5
+    max-scaled of the fp64 sum of the reference's own terms."""
+    d, ng = 3072, 8
+    rows = (1 << 31) // d + 64
+    g = torch.Generator(device=DEV).manual_seed(31)
+    x = torch.randn(rows, d, device=DEV, generator=g).to(dtype)
+    u = torch.randn(rows, d, device=DEV, generator=g).to(dtype)
+    a = torch.randn(ng, 6, device=DEV, generator=g)
+    b = torch.randn(ng, 4, device=DEV, generator=g)
+    assert x.numel() > (1 << 31)
+    y = ops().rational_forward(x, a, b, exact=True)
+    tail = slice(rows - 80, rows)  # straddles element 2^31
+    assert torch.equal(y[tail], ops().rational_forward(x[tail].clone(), a, b, exact=True))
+    del y
+    dx, da, db = ops().rational_backward(x, u, a, b, exact=True, check_overflow=True)
+    dx_t, _, _ = ops().rational_backward(x[tail].clone(), u[tail].clone(), a, b, exact=True)
+    assert torch.equal(dx[tail], dx_t)
+    del dx
+    ta, tb = _terms64(x, u, a, b, ng)
+    for got_a, got_b in [(da, db),
+                         ops().rational_backward(x, u, a, b, check_overflow=True)[1:],
+                         ops().rational_backward(x, u, a, b, deterministic=True, check_overflow=True)[1:]]:
+        ea = float((got_a.double() - ta).abs().max() / ta.abs().max())
+        eb = float((got_b.double() - tb).abs().max() / tb.abs().max())
+        assert ea <= 1e-5 and eb <= 1e-5, (dtype, ea, eb)
