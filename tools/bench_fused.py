@@ -18,18 +18,28 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2505_13813_b200 import ops  # noqa: E402
+from bench import ClockSampler  # noqa: E402
 
 
-def timed(fn, reps, warm=5):
+CLOCKS = {}  # label -> NVML clock summary of its timed loop
+
+
+def timed(fn, reps, warm=5, label=None):
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(0) if label else None
+    if sampler:
+        sampler.start()
     e0.record()
     for _ in range(reps):
         fn()
     e1.record()
     torch.cuda.synchronize()
+    if sampler:
+        sampler.stop()
+        CLOCKS[label] = sampler.summary()
     return e0.elapsed_time(e1) / reps * 1e3  # us
 
 
@@ -55,9 +65,9 @@ def main():
         w = (torch.randn(K, F, generator=g) / K ** 0.5).to(torch.bfloat16).to(dev)
         a = torch.randn(8, 6, generator=g).to(dev)
         b = torch.randn(8, 4, generator=g).to(dev)
-        t_fused = timed(lambda: ops.linear_backward_fused(dy, w, x, a, b), args.reps)
+        t_fused = timed(lambda: ops.linear_backward_fused(dy, w, x, a, b), args.reps, label="bwd_fused")
         dF = torch.empty(M, F, dtype=torch.bfloat16, device=dev)
-        t_gemm = timed(lambda: torch.matmul(dy, w, out=dF), args.reps)
+        t_gemm = timed(lambda: torch.matmul(dy, w, out=dF), args.reps, label="bwd_gemm")
         t_rat = timed(lambda: ops.rational_backward(x, dF, a, b), args.reps)
         flops = 2.0 * M * F * K
         # forward of the same layer: y = R(x) w^T, w = torch weight [out = K, in = F]
@@ -81,6 +91,8 @@ def main():
             "speedup": (t_gemm + t_rat) / t_fused, "bf16_peak_tflops": tc_peak,
             "hbm_bytes_fused": 2.0 * (M * K + K * F + 2 * M * F),
             "hbm_bytes_unfused": 2.0 * (M * K + K * F + M * F) + 2.0 * 3 * M * F,
+            # NVML during the timed loops: tensor-core work runs the B200 into its power cap
+            "fused_clocks": CLOCKS.get("bwd_fused"), "gemm_clocks": CLOCKS.get("bwd_gemm"),
         }), flush=True)
 
 
