@@ -57,7 +57,7 @@ constexpr int kSmemBudget = GRKAN_FUSED_SMEM_KB * 1024;  // operand ring + X til
 constexpr int kKC = 10;           // coefficient terms (degrees (5, 4))
 constexpr int kMaxGroups = 64;    // coefficient table in shared memory
 #ifndef GRKAN_FUSED_PROBE_NOEPI
-#define GRKAN_FUSED_PROBE_NOEPI 0  // diagnostic only: backward epilogue skips the rational math
+#define GRKAN_FUSED_PROBE_NOEPI 0  // diagnostic only: 1 = backward epilogue skips the rational math and dX; 2 = math only skipped
 #endif
 #ifndef GRKAN_FUSED_SK_BN
 #define GRKAN_FUSED_SK_BN 192     // short-K (X staged) tile width ...
@@ -455,6 +455,15 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
               mbar_arrive_leader(&tempty[acc]);
             else
               mbar_arrive(&tempty[acc]);
+          }
+        }
+        if (live && GRKAN_FUSED_PROBE_NOEPI == 2) {  // probe: dX traffic without the math
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            float o[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) o[k] = u[v * 8 + k];
+            __stcs(reinterpret_cast<uint4*>(dxrow + c * CH) + v, Raw16<__nv_bfloat16>::pack(o));
           }
         }
         if (live && !GRKAN_FUSED_PROBE_NOEPI) {
