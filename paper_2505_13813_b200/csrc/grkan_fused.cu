@@ -747,7 +747,13 @@ struct TileShape {
   int bn, atom, es, ch;
   bool xs;
 };
-constexpr TileShape kShapesLongK[] = {{256, 64, 4, 16, false}, {192, 64, 4, 16, false}, {256, 64, 2, 32, false},
+#ifndef GRKAN_FUSED_LK_BN  // tuning knobs: the long-K shape tried first
+#define GRKAN_FUSED_LK_BN 256
+#define GRKAN_FUSED_LK_ATOM 64
+#define GRKAN_FUSED_LK_ES 4
+#define GRKAN_FUSED_LK_CH 16
+#endif
+constexpr TileShape kShapesLongK[] = {{GRKAN_FUSED_LK_BN, GRKAN_FUSED_LK_ATOM, GRKAN_FUSED_LK_ES, GRKAN_FUSED_LK_CH, false}, {192, 64, 4, 16, false}, {256, 64, 2, 32, false},
                                       {192, 64, 2, 32, false}, {128, 64, 4, 16, false}, {128, 64, 2, 32, false},
                                       {96, 32, 1, 32, false},  {64, 64, 2, 32, false},  {64, 64, 1, 32, false},
                                       {32, 32, 1, 32, false}};
