@@ -163,12 +163,16 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
-def config_block(args, cfg):
+def config_block(args, cfg, world=1):
     batch, seq, dim, groups = cfg
+    if args.scaling == "strong":  # the global batch is fixed and split over the ranks
+        global_batch, batch = batch, max(1, batch // world)
+    else:
+        global_batch = batch * world
     return {
         "workload": "GR-KAN group-rational fwd+bwd, %s shape [B=%d, L=%d, D=%d] per GPU, %d groups, "
                     "degrees (5,4)" % (args.config.upper(), batch, seq, dim, groups),
-        "batch_per_gpu": batch, "seq_len": seq, "dim": dim, "groups": groups,
+        "batch_per_gpu": batch, "global_batch": global_batch, "seq_len": seq, "dim": dim, "groups": groups,
         "degrees": [M1 - 1, NDEN], "mode": args.mode, "io_dtype": args.dtype,
         "parallelism": "dp%d" % args.gpus, "collective": args.collective,
         "l2": "inputs larger than L2 (no flush): %d MB per tensor vs 126 MB L2"
@@ -578,7 +582,7 @@ def run_b200(args, rank, world, local_rank):
         "dtype": "f32" if args.dtype == "fp32" else "bf16-io/f32-math",
         "data": "synthetic: x, dy ~ N(0,1) (torch seeded per rank), coefficients ~ N(0,1) "
                 "(run_bench protocol, pkg/src/grkan/cli.py:146-158)",
-        "config": config_block(args, cfg),
+        "config": config_block(args, cfg, world),
         "hbm_gbs": (5 * es * E) / (ms_step / 1e3) / 1e9,
         "roofline": {
             "bound": "hbm", "kernel": "grkan_bwd (K2 bwd_main + K3 reduce)",

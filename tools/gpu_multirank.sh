@@ -13,3 +13,8 @@ timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --mast
   --master-port $((29500 + RANDOM % 1000)) bench.py --config kat-t-train --gpus 2 --steps 5 --warmup 3 \
   --dist-backend gloo > gpurun_out/multirank_train.json 2> gpurun_out/multirank_train.err
 echo "train rc=$?"
+# strong scaling: global B=256 split over the two ranks
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+  --master-port $((29500 + RANDOM % 1000)) bench.py --gpus 2 --steps 10 --warmup 3 --dist-backend gloo \
+  --scaling strong --no-cpu-baseline --e2e-steps 1 > gpurun_out/multirank_strong.json 2> gpurun_out/multirank_strong.err
+echo "strong rc=$?"
