@@ -31,3 +31,14 @@ def test_reference_arm_non_zero_rank_is_silent():
                           "--steps", "1", "--warmup", "0", "--cpu-sample-batch", "1"],
                          capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def test_config_block_weak_and_strong():
+    sys.path.insert(0, ROOT)
+    import bench
+    weak = bench.config_block(bench.parse_args(["--gpus", "4"]), bench.CONFIGS["kat-b"], world=4)
+    assert weak["batch_per_gpu"] == 256 and weak["global_batch"] == 1024 and weak["parallelism"] == "dp4"
+    strong = bench.config_block(bench.parse_args(["--gpus", "4", "--scaling", "strong"]),
+                                bench.CONFIGS["kat-b"], world=4)
+    assert strong["batch_per_gpu"] == 64 and strong["global_batch"] == 256
+    assert "B=64" in strong["workload"]
