@@ -22,7 +22,9 @@ full KAT-B batch (B=256), so per-GPU work is fixed as N grows.
 ``e2e``    the same metric through the public streaming API
            (streaming.HostPipeline.fwd_bwd) with x, dy copied from pinned host
            memory and y, dx, da, db copied back every step; the plain
-           autograd path (GroupRationalFn + backward) is reported beside it.
+           autograd path (GroupRationalFn + backward) is reported beside it, and
+           ``e2e.reference_api``: the reference-facing functions themselves
+           (shim forward_tensor + backward_blocked on pageable NumPy arrays).
 ``roofline`` the dominant kernel (the backward call: K2 + its tiny K3 fold),
            algorithmic bytes 3*s*E per launch / its CUDA-event duration.
 ``cpu_baseline`` the oracle port of the reference path (NumPy, all host
@@ -563,6 +565,35 @@ def run_b200(args, rank, world, local_rank):
     e2e_ms = time_e2e(e2e_stream)
     e2e_auto_ms = time_e2e(e2e_autograd)
     e2e_value = world * E / (e2e_ms / 1e3)
+
+    # (c) the reference-facing API itself: the shim's forward_tensor + backward_blocked
+    # on pageable NumPy arrays (what a caller of the reference holds), host-synchronous,
+    # wall clock; fp32 only (the reference has no bf16), one process
+    shim = None
+    if args.dtype == "fp32" and world == 1:
+        from paper_2505_13813_b200 import grkan as G
+        xt = G.ActivationTensor(np.array(xh.numpy()))
+        ut = G.ActivationTensor(np.array(dyh.numpy()))
+        params = G.GroupRationalParams(a.double().cpu().numpy(), b.double().cpu().numpy())
+        layout = G.GroupLayout(dim, groups)
+        plan = G.ExecutionPlan.blocked(batch, seq, layout)
+
+        def shim_step():
+            G.forward_tensor(xt, params, layout, validate=False, exact=exact)
+            G.backward_blocked(xt, ut, params, plan, validate=False, exact=exact)
+
+        shim_step()
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            shim_step()
+            ts.append(time.perf_counter() - t0)
+        shim_ms = statistics.fmean(ts) * 1e3
+        shim = {"value": E / (shim_ms / 1e3), "ms_per_step": shim_ms, "steps": len(ts),
+                "h2d_bytes_per_step": 3 * es * E, "d2h_bytes_per_step": 2 * es * E + 4 * groups * (M1 + NDEN),
+                "api": "paper_2505_13813_b200.grkan.forward_tensor + backward_blocked (the reference's "
+                       "functions and types; pageable NumPy in/out, wall clock)"}
+        del xt, ut
     del xh, dyh, yh, dxh, pipe
 
     if rank != 0:
@@ -603,7 +634,8 @@ def run_b200(args, rank, world, local_rank):
                 "api": "paper_2505_13813_b200.streaming.HostPipeline.fwd_bwd (pinned host x, dy -> "
                        "y, dx, da, db; chunked, copies overlapped with compute)",
                 "autograd_ms_per_step": e2e_auto_ms,
-                "autograd_value": world * E / (e2e_auto_ms / 1e3)},
+                "autograd_value": world * E / (e2e_auto_ms / 1e3),
+                "reference_api": shim},
         "clocks": sampler.summary(),
         "gpu_launches": 3 * K,
         "alg1_atomic_comparator": None if alg1_us is None else {

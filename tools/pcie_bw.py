@@ -3,7 +3,9 @@
     python tools/pcie_bw.py  -> one JSON line (GB/s)
 """
 import json
+import time
 
+import numpy as np
 import torch
 
 
@@ -46,8 +48,26 @@ def main():
         cur.wait_stream(s2)
 
     t1, t2, t3 = timed(h2d), timed(d2h), timed(both)
+
+    # pageable NumPy memory, as a caller of the reference-API shim holds it (wall clock,
+    # synchronous): an existing array uploaded, and a download into a FRESH array (first
+    # touch of its pages included, as .cpu().numpy() does)
+    arr = np.ones(n, dtype=np.float32)
+
+    def wall(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) / reps
+
+    t4 = wall(lambda: d_in.copy_(torch.from_numpy(arr)))
+    t5 = wall(lambda: d_out.cpu().numpy())
     print(json.dumps({"h2d_gbs": nbytes / t1 / 1e9, "d2h_gbs": nbytes / t2 / 1e9,
-                      "bidirectional_gbs_each_way": nbytes / t3 / 1e9, "bytes": nbytes}))
+                      "bidirectional_gbs_each_way": nbytes / t3 / 1e9, "bytes": nbytes,
+                      "pageable_h2d_gbs": nbytes / t4 / 1e9, "pageable_d2h_fresh_gbs": nbytes / t5 / 1e9}))
 
 
 if __name__ == "__main__":
