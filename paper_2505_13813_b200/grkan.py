@@ -262,6 +262,48 @@ def _coeffs(params: GroupRationalParams, tdtype: torch.dtype, device):
     return a, b
 
 
+_STAGE_BYTES = 32 << 20
+_stage_cache = {}  # device index -> (two pinned staging chunks, copy stream, two events)
+
+
+def _download(t: torch.Tensor) -> np.ndarray:
+    """Device tensor -> a fresh NumPy array, through two pinned staging chunks.
+
+    ``t.cpu()`` into fresh pageable memory runs at ~2 GB/s on the B200 host
+    (driver staging + first-touch page faults); here the D2H of chunk k+1
+    (56 GB/s pinned) overlaps the host copy of chunk k, so the cost is about the
+    host's own first-touch copy rate (~5 GB/s measured, tools/pcie_bw.py).
+    """
+    nb = t.numel() * t.element_size()
+    if nb <= 2 * _STAGE_BYTES:
+        return t.cpu().numpy()
+    bufs, stream, evs = _stage(t.device)
+    dev = t.device
+    src = t.contiguous().reshape(-1).view(torch.uint8)
+    out = np.empty(t.shape, dtype=torch.empty(0, dtype=t.dtype).numpy().dtype)
+    dst = out.reshape(-1).view(np.uint8)
+    views = [b.numpy() for b in bufs]
+    n = -(-nb // _STAGE_BYTES)
+    stream.wait_stream(torch.cuda.current_stream(dev))
+
+    def issue(k):
+        lo = k * _STAGE_BYTES
+        hi = min(nb, lo + _STAGE_BYTES)
+        with torch.cuda.stream(stream):
+            bufs[k & 1][: hi - lo].copy_(src[lo:hi], non_blocking=True)
+            evs[k & 1].record(stream)
+
+    issue(0)
+    for k in range(n):
+        if k + 1 < n:
+            issue(k + 1)  # its buffer's previous chunk (k - 1) was copied out last iteration
+        evs[k & 1].synchronize()
+        lo = k * _STAGE_BYTES
+        hi = min(nb, lo + _STAGE_BYTES)
+        np.copyto(dst[lo:hi], views[k & 1][: hi - lo])
+    return out
+
+
 def check_compatible(x: ActivationTensor, params: GroupRationalParams, layout: GroupLayout) -> None:
     """rational.py:313-322."""
     if x.feature != layout.feature_dim:
@@ -272,8 +314,39 @@ def check_compatible(x: ActivationTensor, params: GroupRationalParams, layout: G
                                   % (params.num_groups, layout.num_groups))
 
 
+def _stage(dev):
+    if dev.index not in _stage_cache:
+        _stage_cache[dev.index] = ([torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)],
+                                   torch.cuda.Stream(dev), [torch.cuda.Event() for _ in range(2)])
+    return _stage_cache[dev.index]
+
+
 def _to_device(t: ActivationTensor):
-    return torch.from_numpy(t.data).to(_device(), non_blocking=False)
+    """Host array -> device tensor; large arrays go through the pinned staging chunks
+    (host copy of chunk k+1 overlaps the H2D of chunk k), small ones directly."""
+    dev = _device()
+    arr = t.data
+    if arr.nbytes <= 2 * _STAGE_BYTES:
+        return torch.from_numpy(arr).to(dev, non_blocking=False)
+    bufs, stream, evs = _stage(dev)
+    out = torch.empty(arr.shape, dtype=torch.from_numpy(arr[:0].reshape(-1)).dtype, device=dev)
+    dst = out.reshape(-1).view(torch.uint8)
+    src = arr.reshape(-1).view(np.uint8)
+    views = [b.numpy() for b in bufs]
+    nb = arr.nbytes
+    n = -(-nb // _STAGE_BYTES)
+    stream.wait_stream(torch.cuda.current_stream(dev))  # `out`'s memory may be reused from that stream
+    for k in range(n):
+        lo = k * _STAGE_BYTES
+        hi = min(nb, lo + _STAGE_BYTES)
+        evs[k & 1].synchronize()  # whatever last read this staging chunk (this call or an earlier one) is done
+        np.copyto(views[k & 1][: hi - lo], src[lo:hi])
+        with torch.cuda.stream(stream):
+            dst[lo:hi].copy_(bufs[k & 1][: hi - lo], non_blocking=True)
+            evs[k & 1].record(stream)
+    torch.cuda.current_stream(dev).wait_stream(stream)
+    out.record_stream(stream)
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -290,7 +363,7 @@ def forward_tensor(x: ActivationTensor, params: GroupRationalParams, layout: Gro
     y = ops.rational_forward(xd, a, b, exact=_exact(exact), check_finite=check)
     if check:
         x.validated = True
-    return ActivationTensor(y.cpu().numpy(), validated=False)
+    return ActivationTensor(_download(y), validated=False)
 
 
 def _prepare_bwd(x, upstream, params, plan, default_plan):
@@ -328,7 +401,7 @@ def backward_blocked(x: ActivationTensor, upstream: ActivationTensor, params: Gr
                                        check_overflow=True)
     if check:
         x.validated = upstream.validated = True
-    return GradBundle(d_x=ActivationTensor(dx.cpu().numpy()), d_a=da.cpu().numpy(),
+    return GradBundle(d_x=ActivationTensor(_download(dx)), d_a=da.cpu().numpy(),
                       d_b=db.cpu().numpy(), strategy=STRATEGY_BLOCKED, precision=x.precision,
                       combine_mode=combine_mode)
 
@@ -347,7 +420,7 @@ def backward_naive(x: ActivationTensor, upstream: ActivationTensor, params: Grou
                                                      else torch.float32)
     a, b = _coeffs(params, xd.dtype, xd.device)
     dx, da, db = ops.rational_backward_atomic(xd, ud, a, b, exact=_exact(exact), check_overflow=True)
-    return GradBundle(d_x=ActivationTensor(dx.cpu().numpy()), d_a=da.cpu().numpy(),
+    return GradBundle(d_x=ActivationTensor(_download(dx)), d_a=da.cpu().numpy(),
                       d_b=db.cpu().numpy(), strategy=STRATEGY_NAIVE, precision=x.precision,
                       combine_mode=COMBINE_ORDERED)
 
@@ -455,7 +528,7 @@ def rational_values(x: np.ndarray, numerator, denominator, exact: bool | None = 
     if flat.numel() == 0:
         return np.empty_like(x)
     y = ops.rational_forward(flat, a, b, exact=_exact(exact))
-    return y.cpu().numpy().reshape(x.shape)
+    return _download(y).reshape(x.shape)
 
 
 def gradient_terms(x: np.ndarray, upstream: np.ndarray, numerator, denominator, exact: bool | None = None):

@@ -442,3 +442,46 @@ def test_gradient_terms_bitwise_vs_reference_restatement(dtype, degrees):
         assert got.dtype == ref.dtype and got.tobytes() == ref.tobytes()
     y = shim.rational_values(x, num, den)
     assert y.tobytes() == orc.rational(x, num, den).tobytes()
+
+
+def test_large_outputs_through_the_staged_download():
+    """Outputs above two 32 MB staging chunks take the pinned double-buffered download;
+    bytes must equal the device result (fp32 and fp64, ragged last chunk)."""
+    import torch
+    from paper_2505_13813_b200 import grkan as G
+    from paper_2505_13813_b200 import ops
+    for dtype, shape in ((np.float32, (5, 1031, 4096)), (np.float64, (3, 1000, 4096))):
+        rng = np.random.default_rng(3)
+        x = G.ActivationTensor(rng.standard_normal(shape).astype(dtype))
+        params = G.GroupRationalParams(rng.standard_normal((8, 6)), rng.standard_normal((8, 4)))
+        layout = G.GroupLayout(shape[2], 8)
+        y = G.forward_tensor(x, params, layout)
+        xd = torch.from_numpy(x.data).cuda()
+        cd = torch.float64 if dtype == np.float64 else torch.float32
+        a = torch.from_numpy(params.numerator).to(cd).cuda()
+        b = torch.from_numpy(params.denominator).to(cd).cuda()
+        want = ops.rational_forward(xd, a, b, exact=True).cpu().numpy()
+        assert y.data.dtype == dtype and y.data.tobytes() == want.tobytes()
+
+
+def test_large_inputs_through_the_staged_upload():
+    """Inputs above two staging chunks are uploaded through the pinned chunks: backward
+    on them equals the direct device computation bit for bit (back-to-back calls reuse
+    the chunks)."""
+    import torch
+    from paper_2505_13813_b200 import grkan as G
+    from paper_2505_13813_b200 import ops
+    rng = np.random.default_rng(5)
+    shape = (5, 1031, 4096)
+    x = G.ActivationTensor(rng.standard_normal(shape).astype(np.float32))
+    u = G.ActivationTensor(rng.standard_normal(shape).astype(np.float32))
+    params = G.GroupRationalParams(rng.standard_normal((8, 6)), rng.standard_normal((8, 4)))
+    plan = G.ExecutionPlan.blocked(shape[0], shape[1], G.GroupLayout(shape[2], 8))
+    bundles = [G.backward_blocked(x, u, params, plan) for _ in range(2)]
+    a = torch.from_numpy(params.numerator).float().cuda()
+    b = torch.from_numpy(params.denominator).float().cuda()
+    dx, da, db = ops.rational_backward(torch.from_numpy(x.data).cuda(), torch.from_numpy(u.data).cuda(), a, b,
+                                       exact=True)
+    for bd in bundles:
+        assert bd.d_x.data.tobytes() == dx.cpu().numpy().tobytes()
+        assert bd.d_a.tobytes() == da.cpu().numpy().tobytes() and bd.d_b.tobytes() == db.cpu().numpy().tobytes()
