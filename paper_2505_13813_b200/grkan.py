@@ -24,6 +24,7 @@ strategy models, so its d_a/d_b are not bit-reproducible.
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass, field
 from typing import Iterator
 
@@ -263,7 +264,9 @@ def _coeffs(params: GroupRationalParams, tdtype: torch.dtype, device):
 
 
 _STAGE_BYTES = 32 << 20
-_stage_cache = {}  # device index -> (two pinned staging chunks, copy stream, two events)
+# per thread (the reference's functions are safe from concurrent callers):
+# device index -> (two pinned staging chunks, copy stream, two events)
+_stage_local = threading.local()
 
 
 def _download(t: torch.Tensor) -> np.ndarray:
@@ -315,10 +318,13 @@ def check_compatible(x: ActivationTensor, params: GroupRationalParams, layout: G
 
 
 def _stage(dev):
-    if dev.index not in _stage_cache:
-        _stage_cache[dev.index] = ([torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)],
-                                   torch.cuda.Stream(dev), [torch.cuda.Event() for _ in range(2)])
-    return _stage_cache[dev.index]
+    cache = getattr(_stage_local, "by_device", None)
+    if cache is None:
+        cache = _stage_local.by_device = {}
+    if dev.index not in cache:
+        cache[dev.index] = ([torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)],
+                            torch.cuda.Stream(dev), [torch.cuda.Event() for _ in range(2)])
+    return cache[dev.index]
 
 
 def _to_device(t: ActivationTensor):

@@ -485,3 +485,31 @@ def test_large_inputs_through_the_staged_upload():
     for bd in bundles:
         assert bd.d_x.data.tobytes() == dx.cpu().numpy().tobytes()
         assert bd.d_a.tobytes() == da.cpu().numpy().tobytes() and bd.d_b.tobytes() == db.cpu().numpy().tobytes()
+
+
+def test_concurrent_callers_with_large_arrays():
+    """The reference's functions are safe from concurrent callers: two
+    threads pushing large arrays through the shim's staging chunks get their own results."""
+    import threading
+    from paper_2505_13813_b200 import grkan as G
+    shape = (5, 1031, 4096)
+    params = G.GroupRationalParams(np.random.default_rng(9).standard_normal((8, 6)),
+                                   np.random.default_rng(10).standard_normal((8, 4)))
+    layout = G.GroupLayout(shape[2], 8)
+    inputs = [G.ActivationTensor(np.random.default_rng(20 + i).standard_normal(shape).astype(np.float32))
+              for i in range(2)]
+    want = [G.forward_tensor(x, params, layout).data for x in inputs]
+    got = [[None, None], [None, None]]
+
+    def work(i):
+        for r in range(2):
+            got[i][r] = G.forward_tensor(inputs[i], params, layout).data
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for i in range(2):
+        for r in range(2):
+            assert got[i][r].tobytes() == want[i].tobytes()
