@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import torch
 from torch import nn
+from torch.autograd.function import once_differentiable
 
 from . import ops  # noqa: F401  (registers torch.ops.grkan_b200.*)
 from .presets import preset_row
@@ -29,6 +30,7 @@ class GroupRationalFn(torch.autograd.Function):
         return torch.ops.grkan_b200.rational_fwd(x, a, b, ctx.exact)
 
     @staticmethod
+    @once_differentiable  # the reference has no second derivative either; double backward raises
     def backward(ctx, dy):
         x, a, b = ctx.saved_tensors
         dx, da, db = torch.ops.grkan_b200.rational_bwd(x, dy.contiguous(), a, b, ctx.exact)
@@ -95,6 +97,7 @@ class GroupRationalLinearFn(torch.autograd.Function):
         return y
 
     @staticmethod
+    @once_differentiable
     def backward(ctx, dy):
         x, a, b, w, f = ctx.saved_tensors
         dy = dy.contiguous()

@@ -513,3 +513,17 @@ def test_concurrent_callers_with_large_arrays():
     for i in range(2):
         for r in range(2):
             assert got[i][r].tobytes() == want[i].tobytes()
+
+
+def test_double_backward_raises():
+    """The backward is first-order only (as the reference's): asking for a second
+    derivative through it fails loudly instead of returning silent zeros."""
+    import torch
+    from paper_2505_13813_b200 import GroupRationalFn
+    x = torch.randn(4, 16, device="cuda", requires_grad=True)
+    a = torch.randn(2, 6, device="cuda", requires_grad=True)
+    b = torch.randn(2, 4, device="cuda", requires_grad=True)
+    y = GroupRationalFn.apply(x, a, b)
+    (gx,) = torch.autograd.grad(y.sum(), x, create_graph=True)
+    with pytest.raises(RuntimeError):
+        gx.sum().backward()
