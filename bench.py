@@ -205,6 +205,7 @@ class ClockSampler:
     def __init__(self, index):
         self.samples = []
         self.power_mw = []
+        self.power_inst_mw = []
         self.reasons = 0
         self.max_mhz = None
         self._stop = threading.Event()
@@ -217,6 +218,9 @@ class ClockSampler:
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
         except Exception:
             self._nv = None
+        if self._nv is not None:  # the first queries are slow (NVML lazy init): not inside the region
+            self._sample()
+            self.samples, self.power_mw, self.power_inst_mw, self.reasons = [], [], [], 0
 
     def _run(self):
         nv = self._nv
@@ -230,6 +234,12 @@ class ClockSampler:
             self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
             self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
             self.power_mw.append(nv.nvmlDeviceGetPowerUsage(self._h))
+        except Exception:
+            pass
+        try:  # instantaneous board power (nvmlDeviceGetPowerUsage is a ~1 s average)
+            fv = nv.nvmlDeviceGetFieldValues(self._h, [nv.NVML_FI_DEV_POWER_INSTANT])[0]
+            if fv.nvmlReturn == 0:
+                self.power_inst_mw.append(fv.value.uiVal)
         except Exception:
             pass
 
@@ -264,6 +274,9 @@ class ClockSampler:
                "reasons": reasons, "reasons_mask": hex(self.reasons), "samples": len(self.samples)}
         try:  # power draw vs the enforced limit: a power-capped run shows median power at the limit
             out["power_w_median"] = statistics.median(self.power_mw) / 1e3 if self.power_mw else None
+            if self.power_inst_mw:
+                out["power_inst_w_median"] = statistics.median(self.power_inst_mw) / 1e3
+                out["power_inst_w_max"] = max(self.power_inst_mw) / 1e3
             out["power_limit_w"] = self._nv.nvmlDeviceGetEnforcedPowerLimit(self._h) / 1e3
         except Exception:
             pass
