@@ -77,6 +77,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// TMA prefetch of a tensor box into L2 (no shared memory, no barrier).
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
+#ifndef GRKAN_FUSED_XPF
+#define GRKAN_FUSED_XPF 0  // long-K backward: TMA-prefetch each tile's X block into L2 when its MMA starts
+#endif
+
 // UMMA shared-memory matrix descriptor (sm_100 format: version 1, base offset 0).
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
@@ -314,6 +325,10 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
       for (int64_t tile = unit0; tile < n_tiles; tile += ustep, ++i) {
         const int n0 = static_cast<int>(tile % geo.n_tiles_n) * BN;
         const int m0 = static_cast<int>((tile / geo.n_tiles_n) * (PAIR ? 2 : 1) * kBM + crank * kBM);
+        if constexpr (!XS && GRKAN_FUSED_XPF) {  // the epilogue's X reads then hit L2
+#pragma unroll
+          for (int a = 0; a < (BN + 63) / 64; ++a) tma_prefetch_2d(&map_x, n0 + a * 64, m0);
+        }
         if constexpr (XS) {  // the tile's X block, into buffer i & 1
           const int xb = i & 1;
           mbar_wait(&xempty[xb], ((i >> 1) & 1) ^ 1);
