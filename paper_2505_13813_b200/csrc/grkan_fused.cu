@@ -59,6 +59,9 @@ constexpr int kMaxGroups = 64;    // coefficient table in shared memory
 #ifndef GRKAN_FUSED_PROBE_NOEPI
 #define GRKAN_FUSED_PROBE_NOEPI 0  // diagnostic only: 1 = backward epilogue skips the rational math and dX; 2 = math only skipped
 #endif
+#ifndef GRKAN_FUSED_PROBE_NOMMA
+#define GRKAN_FUSED_PROBE_NOMMA 0  // diagnostic only: one MMA per tile (wrong results), times the epilogue side
+#endif
 #ifndef GRKAN_FUSED_SK_BN
 #define GRKAN_FUSED_SK_BN 192     // short-K (X staged) tile width ...
 #endif
@@ -382,6 +385,7 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
             const uint64_t ad = smem_desc(sa + k * 32, 16, 1024, 2);
             // B: MN-major, K step = two 8-row groups
             const uint64_t bd = smem_desc(sb + k * 2 * B_SBO, ATOM_BYTES, B_SBO, B_LAYOUT);
+            if (GRKAN_FUSED_PROBE_NOMMA && (kb | k) != 0) continue;  // probe: epilogue-only timing
             if constexpr (PAIR)
               umma_bf16_pair(dcol, ad, bd, idesc, (kb | k) != 0);
             else
