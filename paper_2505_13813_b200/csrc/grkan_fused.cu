@@ -87,6 +87,9 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, 
                : "memory");
 }
 
+#ifndef GRKAN_FUSED_XALL
+#define GRKAN_FUSED_XALL 1  // backward epilogue: load all of a warp's X columns before the accumulator wait
+#endif
 #ifndef GRKAN_FUSED_XPF
 #define GRKAN_FUSED_XPF 0  // long-K backward: TMA-prefetch each tile's X block into L2 when its MMA starts
 #endif
@@ -429,11 +432,16 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
       }
       const __nv_bfloat16* xrow = x + grow * geo.N + c0;
       __nv_bfloat16* dxrow = dx + grow * geo.N + c0;
-      // X for the first 32 columns is independent of the MMA: fetch it first
-      uint4 xr[2][NV];
+      // X is independent of the MMA: fetch the first chunk (or, XALL, every
+      // chunk of this warp's columns) before waiting for the accumulator
+      constexpr bool XALL = GRKAN_FUSED_XALL && !XS;
+      constexpr int XB = XALL ? CW / CH : 2;  // X register buffers
+      uint4 xr[XB][NV];
       if (!XS && live) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) xr[0][v] = __ldcs(reinterpret_cast<const uint4*>(xrow) + v);
+        for (int cc = 0; cc < (XALL ? CW / CH : 1); ++cc)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) xr[cc][v] = __ldcs(reinterpret_cast<const uint4*>(xrow + cc * CH) + v);
       }
       const unsigned char* xtile = xs + acc * XBYTES;
       if constexpr (XS) mbar_wait(&xfull[acc], (i >> 1) & 1);
@@ -448,16 +456,16 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
       const uint32_t taddr = tmem_d + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + cs * CW);
 #pragma unroll
       for (int c = 0; c < CW / CH; ++c) {
-        if (!XS && live && c + 1 < CW / CH) {
+        if (!XS && !XALL && live && c + 1 < CW / CH) {
 #pragma unroll
-          for (int v = 0; v < NV; ++v) xr[(c + 1) & 1][v] = __ldcs(reinterpret_cast<const uint4*>(xrow + (c + 1) * CH) + v);
+          for (int v = 0; v < NV; ++v) xr[(c + 1) % XB][v] = __ldcs(reinterpret_cast<const uint4*>(xrow + (c + 1) * CH) + v);
         }
         if constexpr (XS) {  // 128B-swizzled box: 16-byte chunk j of row r sits at (j ^ (r & 7))
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
             const int col = cs * CW + c * CH + v * 8;
             const int j = (col & 63) >> 3;
-            xr[c & 1][v] = *reinterpret_cast<const uint4*>(xtile + (col >> 6) * XBOX + row * 128 + ((j ^ (row & 7)) << 4));
+            xr[c % XB][v] = *reinterpret_cast<const uint4*>(xtile + (col >> 6) * XBOX + row * 128 + ((j ^ (row & 7)) << 4));
           }
           if (c + 1 == CW / CH) {  // done with this X buffer
             __syncwarp();
@@ -490,7 +498,7 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
             float xv[8], o[8], uv[8];
-            Raw16<__nv_bfloat16>::unpack(xr[c & 1][v], xv);
+            Raw16<__nv_bfloat16>::unpack(xr[c % XB][v], xv);
 #pragma unroll
             for (int k = 0; k < 8; ++k) uv[k] = u[v * 8 + k];
             rp.template grad_n<4, false, AccT>(xv, uv, o, sacc);
