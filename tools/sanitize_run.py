@@ -38,7 +38,7 @@ for dtype in (torch.float32, torch.bfloat16, torch.float64):
             _, p0 = ops.backward_partials(x2, u2, a, b)
             ops.reduce_partials(p0, m1, n, check_overflow=True)
 # fused tcgen05 layer backward: both B-atom swizzles, X staged and direct, M tail
-for M, F, K, g in [(200, 256, 128, 2), (130, 768, 192, 8), (256, 256, 1536, 2)]:
+for M, F, K, g in [(200, 256, 128, 2), (130, 768, 192, 8), (256, 256, 1536, 2), (130, 768, 3072, 8)]:
     x = torch.randn(M, F, device=dev).to(torch.bfloat16)
     dy = torch.randn(M, K, device=dev).to(torch.bfloat16)
     w = torch.randn(K, F, device=dev).to(torch.bfloat16)
