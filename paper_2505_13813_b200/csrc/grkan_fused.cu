@@ -87,6 +87,9 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, 
                : "memory");
 }
 
+#ifndef GRKAN_FUSED_NACC
+#define GRKAN_FUSED_NACC 2  // backward: TMEM accumulator buffers (more than 2 only where NACC * BN <= 512)
+#endif
 #ifndef GRKAN_FUSED_XALL
 #define GRKAN_FUSED_XALL 1  // backward epilogue: load all of a warp's X columns before the accumulator wait
 #endif
@@ -260,7 +263,9 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
   static_assert(!PAIR || (BN / 2) % ATOM == 0, "each CTA of a pair loads whole B atoms");
   constexpr uint32_t B_LAYOUT = ATOM == 64 ? 2u : 4u;      // SWIZZLE_128B / SWIZZLE_64B
   constexpr uint32_t B_SBO = ATOM * 2 * 8;                 // 8 K-rows of one atom
-  constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  // TMEM accumulator buffers: NACC tiles in flight between the MMA and the epilogue
+  constexpr int NACC = (GRKAN_FUSED_NACC > 2 && GRKAN_FUSED_NACC * BN <= 512) ? GRKAN_FUSED_NACC : 2;
+  constexpr int TMEM_COLS = NACC * BN <= 64 ? 64 : NACC * BN <= 128 ? 128 : NACC * BN <= 256 ? 256 : 512;
   constexpr int NE = 4 * ES;                        // epilogue warps
   constexpr int CW = BN / ES;                       // columns per epilogue warp
   static_assert(CW % CH == 0, "epilogue columns come in CH-column TMEM loads");
@@ -271,7 +276,7 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], xfull[2], xempty[2];
+  __shared__ uint64_t full[kStages], empty[kStages], tfull[NACC], tempty[NACC], xfull[2], xempty[2];
   __shared__ uint32_t tmem_base;
   __shared__ float scoef[kMaxGroups * kKC];  // every group's a (6) || b (4)
   unsigned char* const xs = smem + kStages * STAGE;  // X tile buffers (XS)
@@ -290,9 +295,11 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NACC; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], PAIR ? 2 * NE : NE);  // PAIR: both CTAs' epilogues drain into the leader's
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&xfull[s], 1);
       mbar_init(&xempty[s], NE);
     }
@@ -373,8 +380,8 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
       uint32_t phase = 0;
       int i = 0;
       for (int64_t tile = unit0; tile < n_tiles; tile += ustep, ++i) {
-        const int acc = i & 1;
-        mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);  // epilogue has drained this buffer
+        const int acc = i % NACC;
+        mbar_wait(&tempty[acc], ((i / NACC) & 1) ^ 1);  // epilogue has drained this buffer
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dcol = tmem_d + static_cast<uint32_t>(acc * BN);
         for (int kb = 0; kb < kblocks; ++kb) {
@@ -419,7 +426,8 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
     int g_loaded = -1;
     RationalX2<false> rp;  // the warp's column block lies in one group (CW | dg)
     for (int64_t tile = unit0; tile < n_tiles; tile += ustep, ++i) {
-      const int acc = i & 1;
+      const int acc = i % NACC;  // TMEM accumulator buffer
+      const int xb = i & 1;      // X staging buffer (XS)
       const int n0 = static_cast<int>(tile % geo.n_tiles_n) * BN;
       const int64_t m_tile = (tile / geo.n_tiles_n) * (PAIR ? 2 : 1) + crank;  // 128-row tile index
       const int64_t grow = m_tile * kBM + row;
@@ -443,15 +451,15 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
 #pragma unroll
           for (int v = 0; v < NV; ++v) xr[cc][v] = __ldcs(reinterpret_cast<const uint4*>(xrow + cc * CH) + v);
       }
-      const unsigned char* xtile = xs + acc * XBYTES;
-      if constexpr (XS) mbar_wait(&xfull[acc], (i >> 1) & 1);
+      const unsigned char* xtile = xs + xb * XBYTES;
+      if constexpr (XS) mbar_wait(&xfull[xb], (i >> 1) & 1);
       // accumulators: float2 (packed FFMA2) when the register budget allows
       // (ES <= 3: <= 14 warps, 128 registers), else one float per coefficient
       using AccT = std::conditional_t<(ES <= 3 || CH <= 8), float2, float>;
       AccT sacc[kKC];
 #pragma unroll
       for (int k = 0; k < kKC; ++k) sacc[k] = AccT{};
-      mbar_wait(&tfull[acc], (i >> 1) & 1);
+      mbar_wait(&tfull[acc], (i / NACC) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t taddr = tmem_d + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + cs * CW);
 #pragma unroll
@@ -469,7 +477,7 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
           }
           if (c + 1 == CW / CH) {  // done with this X buffer
             __syncwarp();
-            if (lane == 0) mbar_arrive(&xempty[acc]);
+            if (lane == 0) mbar_arrive(&xempty[xb]);
           }
         }
         float u[CH];
