@@ -82,3 +82,21 @@ def test_measured_traffic_recorded_in_profiles():
             assert r["model_bytes"] == m.total_bytes
             assert 0.8 < r["dram_over_model"] < 1.05, (shape, op)
             assert r["red_thread_ops"] == m.atomics, (shape, op)
+
+
+def test_summary_reproduces_from_the_committed_ncu_csvs():
+    """tools/access_ncu.py summarize, re-run here on the committed raw ncu CSVs,
+    gives the committed profiles/r1/access_model_vs_ncu.json numbers."""
+    import subprocess
+    import sys
+    root = os.path.dirname(HERE)
+    csvs = [os.path.join(root, "profiles", "r1", "access", "access_%s.csv" % s) for s in ("kat-s", "kat-b")]
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "access_ncu.py"), "summarize", *csvs],
+                         capture_output=True, text=True, timeout=120, cwd=root)
+    assert out.returncode == 0, out.stderr
+    got = json.loads(out.stdout)["shapes"]
+    want = json.load(open(os.path.join(root, "profiles", "r1", "access_model_vs_ncu.json")))["shapes"]
+    for shape in want:
+        for op in ("fwd", "bwd", "bwd_atomic"):
+            for key in ("dram_bytes", "model_bytes", "red_thread_ops", "reference_bytes"):
+                assert got[shape][op][key] == want[shape][op][key], (shape, op, key)
