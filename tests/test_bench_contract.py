@@ -1,9 +1,11 @@
-"""bench.py contract checks that run without a GPU: the reference arm's JSON line."""
+"""bench.py contract checks: the reference arm (no GPU), the config block, and one small GPU-arm line (-m gpu)."""
 
 import json
 import os
 import subprocess
 import sys
+
+import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -42,3 +44,25 @@ def test_config_block_weak_and_strong():
                                 bench.CONFIGS["kat-b"], world=4)
     assert strong["batch_per_gpu"] == 64 and strong["global_batch"] == 256
     assert "B=64" in strong["workload"]
+
+
+@pytest.mark.gpu
+def test_b200_arm_json_line_small_config():
+    """The GPU arm's JSON line carries every key the driver reads (KAT-T, a few steps)."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "kat-t", "--steps", "3",
+                          "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "clocks", "gpu_launches"):
+        assert key in d, key
+    assert d["value"] > 0 and d["steps"] == 3 and d["gpu_launches"] == 3 * 3
+    for key in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert key in d["roofline"], key
+    for key in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+        assert key in d["e2e"], key
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["reference_api"]["value"] > 0
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
