@@ -1,8 +1,16 @@
 #!/usr/bin/env python
 """Benchmark: GR-KAN group-rational fwd+bwd throughput at KAT-B shape on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--dtype fp32|bf16]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--dtype fp32|bf16|fp64]
                     [--config kat-b|kat-s|kat-t] [--mode fast|exact] [--impl b200|reference]
+                    [--batch B --seqlen L --dim D --groups G --num-coeffs M1 --den-coeffs N
+                     --seed S --block-size S --strategy blocked|naive|both --dump PATH]
+
+``--gpus N`` without a launcher re-executes itself under torch.distributed.run
+with N ranks (one per GPU); under a launcher WORLD_SIZE must equal N.  The
+shape / degree / seed flags are run_bench's (pkg/src/grkan/cli.py:341-361);
+inputs follow its draw order (x, upstream, numerator, denominator from
+default_rng(seed), cli.py:143-158; rank r > 0 draws from default_rng([seed, r])).
 
 One step = one forward (K1) + one backward (K2 + K3) of the group-rational
 unit over one synthetic [B, L, D] batch (run_bench --include-forward,
@@ -27,8 +35,11 @@ full KAT-B batch (B=256), so per-GPU work is fixed as N grows.
            (shim forward_tensor + backward_blocked on pageable NumPy arrays).
 ``roofline`` the dominant kernel (the backward call: K2 + its tiny K3 fold),
            algorithmic bytes 3*s*E per launch / its CUDA-event duration.
-``cpu_baseline`` the oracle port of the reference path (NumPy, all host
-           threads) on a bounded sample of the same workload (rank 0, N=1).
+``cpu_baseline`` the reference itself (``grkan`` installed from /root/reference
+           into baseline/_ref, kind "reference"; the oracle port, kind "port",
+           only if that install is absent): forward_tensor + backward_blocked
+           with all host threads on a bounded sample of the same workload
+           (rank 0, N=1).
 
 ``--impl reference`` times only that CPU path (rank 0; other ranks exit 0).
 Inputs exceed L2 (KAT-B fp32: 620 MB per tensor vs 126 MB L2), so no flush.
@@ -68,9 +79,23 @@ def parse_args(argv=None):
     p.add_argument("--steps", type=int, default=100)  # repeats 100, as the paper and run_bench (cli.py:73-74)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=("b200", "reference"), default="b200")
-    p.add_argument("--dtype", choices=("fp32", "bf16"), default="fp32")
+    p.add_argument("--dtype", choices=("fp32", "bf16", "fp64"), default="fp32")
     p.add_argument("--config", choices=tuple(CONFIGS) + tuple(TRAIN_CONFIGS), default="kat-b")
-    p.add_argument("--batch", type=int, default=128, help="images per GPU for the *-train configs")
+    # run_bench's workload flags (pkg/src/grkan/cli.py:341-361); unset = the --config preset
+    p.add_argument("--batch", type=int, default=None,
+                   help="batch per GPU (the config's B; images per GPU for the *-train configs, default 128)")
+    p.add_argument("--seqlen", type=int, default=None)
+    p.add_argument("--dim", type=int, default=None)
+    p.add_argument("--groups", type=int, default=None)
+    p.add_argument("--num-coeffs", type=int, default=6, help="numerator coefficients per group (m + 1)")
+    p.add_argument("--den-coeffs", type=int, default=4, help="denominator coefficients per group (n)")
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--block-size", type=int, default=256,
+                   help="row block of the CPU reference's blocked strategy (backward.py:48)")
+    p.add_argument("--strategy", choices=("blocked", "naive", "both"), default="both",
+                   help="blocked: K2+K3 timed; naive: the Alg.-1 atomic comparator (K4) timed as the "
+                        "backward; both: blocked timed, the comparator reported beside it")
+    p.add_argument("--dump", default=None, help="write the final dx as a GRKB tensor dump (cli.py:105-118)")
     p.add_argument("--mode", choices=("fast", "exact"), default="fast")
     p.add_argument("--scaling", choices=("weak", "strong"), default="weak")
     p.add_argument("--e2e-steps", type=int, default=None)
@@ -82,7 +107,8 @@ def parse_args(argv=None):
                         "fused with the exchange over CUDA-IPC peer memory (grkan_bwd_p2p, no NCCL)")
     p.add_argument("--e2e-chunks", type=int, default=16,
                    help="row chunks of the streaming e2e pipeline (fill + drain cost one chunk each)")
-    p.add_argument("--cpu-sample-batch", type=int, default=16)
+    p.add_argument("--cpu-sample-batch", type=int, default=64,
+                   help="rows B of the bounded CPU-reference sample (KAT-B: 64 of 256)")
     p.add_argument("--cpu-passes", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--single-thread-baseline", action=argparse.BooleanOptionalAction, default=True,
@@ -92,11 +118,37 @@ def parse_args(argv=None):
     p.add_argument("--dist-backend", default="nccl",
                    help="torch.distributed backend for N > 1 (gloo only to exercise the multi-rank "
                         "code path when several ranks share one GPU)")
-    return p.parse_args(argv)
+    args = p.parse_args(argv)
+    if args.gpus < 1:
+        p.error("--gpus must be >= 1")
+    return args
+
+
+def workload(args):
+    """(batch per GPU, seq, dim, groups): the --config preset with run_bench's overrides."""
+    batch, seq, dim, groups = CONFIGS[args.config]
+    batch = args.batch if args.batch is not None else batch
+    seq = args.seqlen if args.seqlen is not None else seq
+    dim = args.dim if args.dim is not None else dim
+    groups = args.groups if args.groups is not None else groups
+    if min(batch, seq, dim, groups) < 1:
+        raise SystemExit("error: dimensions must be positive")
+    if dim % groups:
+        raise SystemExit("error: layout mismatch: dim %d not divisible by groups %d" % (dim, groups))
+    if args.num_coeffs < 1 or args.den_coeffs < 0:
+        raise SystemExit("error: need at least one numerator coefficient and den_coeffs >= 0")
+    return batch, seq, dim, groups
+
+
+def is_preset(args):
+    return (args.batch, args.seqlen, args.dim, args.groups) == (None,) * 4 and \
+        (args.num_coeffs, args.den_coeffs) == (M1, NDEN)
 
 
 def ncu_traffic(args, kind):
     """DRAM bytes per launch for this workload from the committed ncu capture, or None."""
+    if not is_preset(args):
+        return None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             d = json.load(fh)
@@ -119,66 +171,113 @@ def peaks():
 # CPU path: the oracle port of the reference (forward_tensor + backward_blocked)
 # ---------------------------------------------------------------------------
 
-def cpu_reference_rate(cfg, batch, passes, warmup=1, workers=None):
-    """elements/s of the NumPy restatement of the reference path on this host."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def reference_module():
+    """The reference package installed into baseline/_ref (build() / oracle/install_reference.sh),
+    or None when that install is absent (then the oracle port stands in)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isfile(os.path.join(ref, "grkan", "backward.py")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import grkan.backward
+    import grkan.rational
+    return grkan
+
+
+def cpu_reference_rate(args, shape, batch, passes, warmup=1, workers=None):
+    """elements/s of the reference's CPU path (forward_tensor + backward_blocked,
+    run_bench --include-forward, pkg/src/grkan/cli.py:178-193) on this host."""
     from oracle import grkan_oracle as orc
 
-    _, seq, dim, groups = cfg
-    x, u, num, den = orc.bench_inputs(batch, seq, dim, groups, M1, NDEN, seed=0)
+    _, seq, dim, groups = shape
+    x, u, num, den = orc.bench_inputs(batch, seq, dim, groups, args.num_coeffs, args.den_coeffs, seed=args.seed)
     workers = workers or os.cpu_count() or 1
+    ref = reference_module()
+    if ref is not None:
+        R, B = ref.rational, ref.backward
+        layout = R.GroupLayout(dim, groups)
+        xt, ut = R.ActivationTensor(x, validated=True), R.ActivationTensor(u, validated=True)
+        params = R.GroupRationalParams(num, den)
+        plan = B.ExecutionPlan.blocked(batch, seq, layout, args.block_size)
+
+        def step():
+            R.forward_tensor(xt, params, layout, validate=False)
+            B.backward_blocked(xt, ut, params, plan, workers=workers, validate=False)
+        kind, what = "reference", "the reference package grkan (pkg/src/grkan, installed into baseline/_ref)"
+    else:
+        def step():
+            orc.cpu_step(x, u, num, den, block_size=args.block_size, workers=workers)
+        kind, what = "port", "the NumPy port of the reference (oracle/grkan_oracle.py)"
     for _ in range(warmup):
-        orc.cpu_step(x, u, num, den, workers=workers)
+        step()
     times = []
     for _ in range(passes):
         t0 = time.perf_counter()
-        orc.cpu_step(x, u, num, den, workers=workers)
+        step()
         times.append(time.perf_counter() - t0)
     mean = statistics.fmean(times)
-    return x.size / mean, workers, times
+    return x.size / mean, workers, times, kind, what
 
 
 def run_reference(args, rank):
     if rank != 0:
         return
-    cfg = CONFIGS[args.config]
-    batch = min(args.cpu_sample_batch, cfg[0])
-    # each step = one reference-style fwd+bwd pass over a bounded sample
-    rate, workers, times = cpu_reference_rate(cfg, batch, max(1, args.steps), warmup=args.warmup)
+    shape = workload(args)
+    batch = min(args.cpu_sample_batch, shape[0])
+    # each step = one reference fwd+bwd pass over a bounded sample
+    rate, workers, times, kind, what = cpu_reference_rate(args, shape, batch, max(1, args.steps),
+                                                          warmup=args.warmup)
     ms = statistics.fmean(times) * 1e3
-    sample = "%s rows B=%d of %d (E=%d), NumPy port of forward_tensor+backward_blocked, block 256, " \
-             "workers=%d" % (args.config, batch, cfg[0], batch * cfg[1] * cfg[2], workers)
+    sample = "%s rows B=%d of %d (E=%d): %s, forward_tensor + backward_blocked (block %d), workers=%d" % (
+        args.config, batch, shape[0], batch * shape[1] * shape[2], what, args.block_size, workers)
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (run_bench draw order, seed 0)",
-        "config": config_block(args, cfg),
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": workers, "kind": "port",
-                         "sample": sample},
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "f64" if args.dtype == "fp64" else "f32",
+        "data": "synthetic (run_bench draw order, seed %d)" % args.seed,
+        "config": config_block(args, shape, args.gpus),
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": workers, "kind": kind,
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     if args.single_thread_baseline:  # SURVEY 8d: also time workers=1 (one pass, B=4 rows sample)
-        r1, _, t1 = cpu_reference_rate(cfg, min(4, batch), 1, warmup=0, workers=1)
+        r1, _, t1, _, _ = cpu_reference_rate(args, shape, min(4, batch), 1, warmup=0, workers=1)
         line["cpu_baseline"]["single_thread"] = {
             "value": r1, "unit": UNIT, "cores": 1,
             "sample": "%s rows B=%d, workers=1, one pass (%.2f s)" % (args.config, min(4, batch), t1[0])}
     print(json.dumps(line), flush=True)
 
 
-def config_block(args, cfg, world=1):
-    batch, seq, dim, groups = cfg
+def config_block(args, shape, world=1):
+    batch, seq, dim, groups = shape
     if args.scaling == "strong":  # the global batch is fixed and split over the ranks
         global_batch, batch = batch, max(1, batch // world)
     else:
         global_batch = batch * world
+    es = {"fp32": 4, "bf16": 2, "fp64": 8}[args.dtype]
+    name = args.config.upper() if is_preset(args) else "custom (%s-based)" % args.config.upper()
     return {
         "workload": "GR-KAN group-rational fwd+bwd, %s shape [B=%d, L=%d, D=%d] per GPU, %d groups, "
-                    "degrees (5,4)" % (args.config.upper(), batch, seq, dim, groups),
+                    "degrees (%d,%d)" % (name, batch, seq, dim, groups, args.num_coeffs - 1, args.den_coeffs),
         "batch_per_gpu": batch, "global_batch": global_batch, "seq_len": seq, "dim": dim, "groups": groups,
-        "degrees": [M1 - 1, NDEN], "mode": args.mode, "io_dtype": args.dtype,
-        "parallelism": "dp%d" % args.gpus, "collective": args.collective,
-        "l2": "inputs larger than L2 (no flush): %d MB per tensor vs 126 MB L2"
-              % (batch * seq * dim * (4 if args.dtype == "fp32" else 2) // 2**20),
+        "degrees": [args.num_coeffs - 1, args.den_coeffs], "seed": args.seed, "mode": args.mode,
+        "io_dtype": args.dtype, "strategy": args.strategy,
+        "parallelism": "dp%d" % world, "collective": args.collective,
+        "l2": ("inputs larger than L2 (no flush): %d MB per tensor vs 126 MB L2"
+               % (batch * seq * dim * es // 2**20)) if batch * seq * dim * es > 126 * 2**20 else
+              ("inputs smaller than L2: a >=256 MB buffer is written between timed steps (L2 flush)"),
     }
 
 
@@ -302,45 +401,79 @@ def run_b200(args, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    cfg = CONFIGS[args.config]
-    batch, seq, dim, groups = cfg
+    shape = workload(args)
+    batch, seq, dim, groups = shape
     if args.scaling == "strong":
         batch = max(1, batch // world)
-    tdt = torch.float32 if args.dtype == "fp32" else torch.bfloat16
-    es = 4 if args.dtype == "fp32" else 2
+    m1, nden = args.num_coeffs, args.den_coeffs
+    tdt = {"fp32": torch.float32, "bf16": torch.bfloat16, "fp64": torch.float64}[args.dtype]
+    es = {"fp32": 4, "bf16": 2, "fp64": 8}[args.dtype]
+    cdt = torch.float64 if args.dtype == "fp64" else torch.float32  # coefficient / gradient dtype
+    ces = 8 if args.dtype == "fp64" else 4
     E = batch * seq * dim
     rows = batch * seq
-    dt_code = N.DT_F32 if args.dtype == "fp32" else N.DT_BF16
+    dt_code = {"fp32": N.DT_F32, "bf16": N.DT_BF16, "fp64": N.DT_F64}[args.dtype]
     flags = N.FLAG_EXACT if args.mode == "exact" else N.FLAG_FAST
 
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1234 + rank)
-    x = torch.randn((batch, seq, dim), generator=gen, device=dev, dtype=torch.float32).to(tdt)
-    dy = torch.randn((batch, seq, dim), generator=gen, device=dev, dtype=torch.float32).to(tdt)
-    crng = np.random.default_rng(0)  # identical coefficients on every rank
-    a = torch.from_numpy(crng.standard_normal((groups, M1)).astype(np.float32)).to(dev)
-    b = torch.from_numpy(crng.standard_normal((groups, NDEN)).astype(np.float32)).to(dev)
+    # run_bench's inputs (pkg/src/grkan/cli.py:143-158): x, upstream, numerator,
+    # denominator from one default_rng(seed) -- rank 0 gets exactly the reference's
+    # draw; rank r > 0 draws from default_rng([seed, r]) (independent shards).
+    # bf16 runs round the fp32 draw.  The coefficients are identical on every rank.
+    rng = np.random.default_rng(args.seed if rank == 0 else [args.seed, rank])
+    host_dt = np.float64 if args.dtype == "fp64" else np.float32
+
+    def draw():
+        t = torch.empty((batch, seq, dim), dtype=tdt, device=dev)
+        step_b = max(1, (64 << 20) // (seq * dim))  # chunked: bounded host memory
+        for b0 in range(0, batch, step_b):
+            nb = min(step_b, batch - b0)
+            t[b0:b0 + nb].copy_(torch.from_numpy(rng.standard_normal((nb, seq, dim)).astype(host_dt)))
+        return t
+
+    x = draw()
+    dy = draw()
+    crng = np.random.default_rng(args.seed)
+    if rank == 0:
+        crng = rng  # continue the reference's stream after x and upstream
+    num = crng.standard_normal((groups, m1))
+    den = crng.standard_normal((groups, nden))
+    if world > 1:  # every rank must use rank 0's coefficients
+        import torch.distributed as dist_
+        cbuf = torch.from_numpy(np.concatenate([num.ravel(), den.ravel()])).to(dev)
+        dist_.broadcast(cbuf, 0)
+        cbuf = cbuf.cpu().numpy()
+        num, den = cbuf[: groups * m1].reshape(groups, m1), cbuf[groups * m1:].reshape(groups, nden)
+    a = torch.from_numpy(num).to(cdt).to(dev)
+    b = torch.from_numpy(den).to(cdt).to(dev).reshape(groups, nden)
     y = torch.empty_like(x)
     dx = torch.empty_like(x)
-    grads = torch.empty(groups * (M1 + NDEN), dtype=torch.float32, device=dev)  # da || db, one buffer
-    da = grads[: groups * M1].view(groups, M1)
-    db = grads[groups * M1:].view(groups, NDEN)
-    ws_bytes = ops.workspace_bytes(rows, dim, groups, M1, NDEN, tdt)
+    grads = torch.empty(groups * (m1 + nden), dtype=cdt, device=dev)  # da || db, one buffer
+    da = grads[: groups * m1].view(groups, m1)
+    db = grads[groups * m1:].view(groups, nden)
+    ws_bytes = ops.workspace_bytes(rows, dim, groups, m1, nden, tdt)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     L = N.lib()
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
+    # workloads smaller than L2 (126 MB): write a 256 MB buffer between timed steps
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if 3 * es * E <= 256 << 20 else None
+    st_naive = torch.zeros(ops.STATUS_WORDS, dtype=torch.int32, device=dev)
 
     def fwd():
-        rc = L.grkan_fwd(x.data_ptr(), y.data_ptr(), a.data_ptr(), b.data_ptr(), rows, dim, groups,
-                         M1, NDEN, dt_code, flags, None, sp)
+        rc = L.grkan_fwd(x.data_ptr(), y.data_ptr(), a.data_ptr(), ops._ptr(b), rows, dim, groups,
+                         m1, nden, dt_code, flags, None, sp)
         assert rc == 0, N.last_error()
 
     def bwd():
         join_comm()  # the previous step's all-reduce still reads grads
-        rc = L.grkan_bwd(x.data_ptr(), dy.data_ptr(), a.data_ptr(), b.data_ptr(), dx.data_ptr(),
-                         da.data_ptr(), db.data_ptr(), ws.data_ptr(), ws_bytes, rows, dim, groups,
-                         M1, NDEN, dt_code, flags, sp)
+        if args.strategy == "naive":  # the paper's Alg. 1: per-element atomics (K4) as the backward
+            rc = L.grkan_bwd_atomic(x.data_ptr(), dy.data_ptr(), a.data_ptr(), ops._ptr(b), dx.data_ptr(),
+                                    da.data_ptr(), ops._ptr(db), rows, dim, groups, m1, nden, dt_code,
+                                    flags, None, sp)
+        else:
+            rc = L.grkan_bwd(x.data_ptr(), dy.data_ptr(), a.data_ptr(), ops._ptr(b), dx.data_ptr(),
+                             da.data_ptr(), ops._ptr(db), ws.data_ptr(), ws_bytes, rows, dim, groups,
+                             m1, nden, dt_code, flags, sp)
         assert rc == 0, N.last_error()
 
     # da||db all-reduce on a side stream: it overlaps the next step's forward
@@ -374,14 +507,14 @@ def run_b200(args, rank, world, local_rank):
     if args.collective == "p2p":
         from paper_2505_13813_b200.parallel import PeerExchange
 
-        pex = PeerExchange(groups, M1, NDEN, dev)
+        pex = PeerExchange(groups, m1, nden, dev)
         ws_p2p = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
 
         def bwd():
             pex.epoch += 1
             rc = L.grkan_bwd_p2p(x.data_ptr(), dy.data_ptr(), a.data_ptr(), b.data_ptr(), dx.data_ptr(),
                                  da.data_ptr(), db.data_ptr(), ws_p2p.data_ptr(), ws_bytes, rows, dim, groups,
-                                 M1, NDEN, dt_code, flags, pex.ptrs.data_ptr(), pex.rank, pex.world, pex.epoch, sp)
+                                 m1, nden, dt_code, flags, pex.ptrs.data_ptr(), pex.rank, pex.world, pex.epoch, sp)
             assert rc == 0, N.last_error()
 
         def allreduce(timed=False):
@@ -393,14 +526,14 @@ def run_b200(args, rank, world, local_rank):
         # rank runs the same fixed-order K3 fold (parallel.deterministic_backward)
         rb = ops.det_block_rows(dim, groups, tdt)
         n_blk = -(-rows // rb)
-        part = torch.empty((n_blk, groups, M1 + NDEN), dtype=torch.float32, device=dev)
-        gathered = torch.empty((world * n_blk, groups, M1 + NDEN), dtype=torch.float32, device=dev)
+        part = torch.empty((n_blk, groups, m1 + nden), dtype=cdt, device=dev)
+        gathered = torch.empty((world * n_blk, groups, m1 + nden), dtype=cdt, device=dev)
         parts_list = list(gathered.chunk(world))
-        st = torch.zeros(2, dtype=torch.int32, device=dev)
+        st = torch.zeros(ops.STATUS_WORDS, dtype=torch.int32, device=dev)
 
         def bwd():
             rc = L.grkan_bwd_partials(x.data_ptr(), dy.data_ptr(), a.data_ptr(), b.data_ptr(), dx.data_ptr(),
-                                      part.data_ptr(), part.numel() * 4, rows, dim, groups, M1, NDEN, dt_code,
+                                      part.data_ptr(), part.numel() * ces, rows, dim, groups, m1, nden, dt_code,
                                       flags, None, sp)
             assert rc == 0, N.last_error()
 
@@ -412,8 +545,8 @@ def run_b200(args, rank, world, local_rank):
                 else:
                     dist.all_gather(parts_list, part)
                 src = gathered
-            rc = L.grkan_reduce_partials(src.data_ptr(), src.shape[0], groups, M1, NDEN, da.data_ptr(),
-                                         db.data_ptr(), N.DT_F32, st.data_ptr(), sp)
+            rc = L.grkan_reduce_partials(src.data_ptr(), src.shape[0], groups, m1, nden, da.data_ptr(),
+                                         ops._ptr(db), N.DT_F64 if args.dtype == "fp64" else N.DT_F32, st.data_ptr(), sp)
             assert rc == 0, N.last_error()
 
     # warm-up: at least W steps and at least 150 ms of device work (clocks and
@@ -451,6 +584,8 @@ def run_b200(args, rank, world, local_rank):
     t_enq = time.perf_counter()
     t_start.record(stream)
     for k in range(K):
+        if flush_buf is not None:  # L2 flush outside the step's events (workload < L2)
+            flush_buf.zero_()
         ev[k][0].record(stream)
         fwd()
         ev[k][1].record(stream)
@@ -469,6 +604,8 @@ def run_b200(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     ms_total = t_start.elapsed_time(t_end)
+    if flush_buf is not None:  # the flushes sit between the steps: sum the steps themselves
+        ms_total = sum(e[0].elapsed_time(e[3]) for e in ev)
     fwd_ms = statistics.fmean(e[0].elapsed_time(e[1]) for e in ev)
     bwd_ms = statistics.fmean(e[1].elapsed_time(e[2]) for e in ev)
     if comm_ev:  # overlapped all-reduce: its own duration on the comm stream
@@ -497,15 +634,19 @@ def run_b200(args, rank, world, local_rank):
     ci95_ms = 1.96 * statistics.stdev(step_ms) / math.sqrt(len(step_ms)) if len(step_ms) > 1 else None
     value = world * E / (ms_step / 1e3)
 
+    if args.dump and rank == 0:  # run_bench --dump: the final dx as a GRKB tensor dump
+        from paper_2505_13813_b200 import grkb
+        grkb.save(args.dump, dx.float() if args.dtype == "bf16" else dx)
+
     # ---- the paper's Alg. 1 comparator (per-element atomicAdd), same inputs ----------------
     alg1_us = None
-    if world == 1:
-        st = torch.zeros(2, dtype=torch.int32, device=dev)
+    if world == 1 and args.strategy == "both":
+        st = torch.zeros(ops.STATUS_WORDS, dtype=torch.int32, device=dev)
         ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         for it in range(2):
             ea.record(stream)
-            rc = L.grkan_bwd_atomic(x.data_ptr(), dy.data_ptr(), a.data_ptr(), b.data_ptr(), dx.data_ptr(),
-                                    da.data_ptr(), db.data_ptr(), rows, dim, groups, M1, NDEN, dt_code,
+            rc = L.grkan_bwd_atomic(x.data_ptr(), dy.data_ptr(), a.data_ptr(), ops._ptr(b), dx.data_ptr(),
+                                    da.data_ptr(), ops._ptr(db), rows, dim, groups, m1, nden, dt_code,
                                     flags, st.data_ptr(), sp)
             eb.record(stream)
             assert rc == 0, N.last_error()
@@ -524,11 +665,11 @@ def run_b200(args, rank, world, local_rank):
     dyh.copy_(dy.cpu())
     yh = torch.empty_like(xh, pin_memory=True)
     dxh = torch.empty_like(xh, pin_memory=True)
-    gh = torch.empty(groups * (M1 + NDEN), dtype=torch.float32, pin_memory=True)
+    gh = torch.empty(groups * (m1 + nden), dtype=cdt, pin_memory=True)
     exact = args.mode == "exact"
     del y, dx, ws
     torch.cuda.empty_cache()
-    pipe = HostPipeline(dev, dim, groups, M1, NDEN, tdt,
+    pipe = HostPipeline(dev, dim, groups, m1, nden, tdt,
                         chunk_rows=max(rows // args.e2e_chunks, -(-(4 << 20) // (dim * es))))
 
     def e2e_stream():
@@ -603,7 +744,7 @@ def run_b200(args, rank, world, local_rank):
             ts.append(time.perf_counter() - t0)
         shim_ms = statistics.fmean(ts) * 1e3
         shim = {"value": E / (shim_ms / 1e3), "ms_per_step": shim_ms, "steps": len(ts),
-                "h2d_bytes_per_step": 3 * es * E, "d2h_bytes_per_step": 2 * es * E + 4 * groups * (M1 + NDEN),
+                "h2d_bytes_per_step": 3 * es * E, "d2h_bytes_per_step": 2 * es * E + 4 * groups * (m1 + nden),
                 "api": "paper_2505_13813_b200.grkan.forward_tensor + backward_blocked (the reference's "
                        "functions and types; pageable NumPy in/out, wall clock)"}
         del xt, ut
@@ -626,7 +767,7 @@ def run_b200(args, rank, world, local_rank):
         "dtype": "f32" if args.dtype == "fp32" else "bf16-io/f32-math",
         "data": "synthetic: x, dy ~ N(0,1) (torch seeded per rank), coefficients ~ N(0,1) "
                 "(run_bench protocol, pkg/src/grkan/cli.py:146-158)",
-        "config": config_block(args, cfg, world),
+        "config": config_block(args, shape, world),
         "hbm_gbs": (5 * es * E) / (ms_step / 1e3) / 1e9,
         "roofline": {
             "bound": "hbm", "kernel": "grkan_bwd (K2 bwd_main + K3 reduce)",
@@ -642,7 +783,7 @@ def run_b200(args, rank, world, local_rank):
             "collective_check": coll_check,
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * es * E,
-                "d2h_bytes_per_step": 2 * es * E + 4 * groups * (M1 + NDEN),
+                "d2h_bytes_per_step": 2 * es * E + ces * groups * (m1 + nden),
                 "ms_per_step": e2e_ms,
                 "api": "paper_2505_13813_b200.streaming.HostPipeline.fwd_bwd (pinned host x, dy -> "
                        "y, dx, da, db; chunked, copies overlapped with compute)",
@@ -650,19 +791,22 @@ def run_b200(args, rank, world, local_rank):
                 "autograd_value": world * E / (e2e_auto_ms / 1e3),
                 "reference_api": shim},
         "clocks": sampler.summary(),
-        "gpu_launches": 3 * K,
+        "gpu_launches": (2 if args.strategy == "naive" else 3) * K,
+        "dist": None if world == 1 else {
+            "backend": dist.get_backend(), "world_size": dist.get_world_size(),
+            "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if args.dist_backend == "nccl" else None},
         "alg1_atomic_comparator": None if alg1_us is None else {
             "bwd_us": alg1_us, "speedup_of_staged_bwd": alg1_us / (bwd_ms * 1e3),
             "note": "paper: FlashKAT bwd 140.5x faster than KAT's atomic bwd on RTX 4060 Ti (PAPER.md:402)"},
     }
     if world == 1 and not args.no_cpu_baseline:
-        sb = min(args.cpu_sample_batch, cfg[0])
-        rate, workers, times = cpu_reference_rate(cfg, sb, args.cpu_passes)
+        sb = min(args.cpu_sample_batch, shape[0])
+        rate, workers, times, kind, what = cpu_reference_rate(args, shape, sb, args.cpu_passes)
         line["cpu_baseline"] = {
-            "value": rate, "unit": UNIT, "cores": workers, "kind": "port",
-            "sample": "%s with B=%d (E=%d), NumPy port of forward_tensor + backward_blocked "
-                      "(block 256, %d threads), %d timed passes after 1 warm-up"
-                      % (args.config, sb, sb * cfg[1] * cfg[2], workers, len(times)),
+            "value": rate, "unit": UNIT, "cores": workers, "kind": kind, "cpu_model": cpu_model(),
+            "sample": "%s with B=%d (E=%d): %s, forward_tensor + backward_blocked (block %d, %d threads), "
+                      "%d timed passes after 1 warm-up"
+                      % (args.config, sb, sb * shape[1] * shape[2], what, args.block_size, workers, len(times)),
         }
     print(json.dumps(line), flush=True)
 
@@ -684,7 +828,7 @@ def run_train(args, rank, world, local_rank):
     if world > 1:
         model = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local_rank])
     opt = torch.optim.AdamW(model.parameters(), lr=1e-4, weight_decay=0.05, fused=True)
-    B = args.batch
+    B = args.batch or 128
     imgs = torch.randn(B, 3, 224, 224, device=dev)
     labels = torch.randint(0, 1000, (B,), device=dev)
     loss_fn = torch.nn.CrossEntropyLoss()
@@ -732,30 +876,66 @@ def run_train(args, rank, world, local_rank):
         }), flush=True)
 
 
+def free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(args, argv):
+    """--gpus N with no launcher: re-execute this script under torch.distributed.run
+    with N ranks on this node (127.0.0.1 rendezvous), forwarding its output."""
+    import subprocess
+
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)]
+    cmd += list(sys.argv[1:] if argv is None else argv)
+    env = dict(os.environ, GRKAN_BENCH_SPAWNED="1")
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main(argv=None):
     args = parse_args(argv)
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    env_world = os.environ.get("WORLD_SIZE")
+    world = int(env_world or "1")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
+    if args.impl == "reference":  # rank 0 alone times the CPU path, however it was launched
         run_reference(args, rank)
-        return
+        return 0
+    if env_world is None and args.gpus > 1:
+        return spawn_ranks(args, argv)
+    if world != args.gpus:
+        print("error: --gpus %d but WORLD_SIZE=%d: launch one rank per GPU (or omit the launcher and let "
+              "bench.py spawn --gpus ranks itself)" % (args.gpus, world), file=sys.stderr)
+        return 2
     if world > 1:
         import torch
         import torch.distributed as dist
 
         ngpu = torch.cuda.device_count()
+        if args.dist_backend == "nccl" and ngpu < world:
+            print("error: %d ranks over NCCL need %d GPUs, this node has %d" % (world, world, ngpu),
+                  file=sys.stderr)
+            return 2
         local_rank = local_rank % ngpu  # ranks may share a GPU when testing with gloo
         torch.cuda.set_device(local_rank)
         if args.dist_backend == "nccl":
+            # communicator setup (ranks, NVLink/NVLS transport) goes to stderr, not the JSON stdout
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
             dist.init_process_group(args.dist_backend)
+        assert dist.get_world_size() == args.gpus, (dist.get_world_size(), args.gpus)
     try:
         if args.config in TRAIN_CONFIGS:
             run_train(args, rank, world, local_rank)
-            return
+            return 0
         run_b200(args, rank, world, local_rank)
+        return 0
     finally:
         if world > 1:
             import torch.distributed as dist
@@ -764,4 +944,4 @@ def main(argv=None):
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -55,7 +55,8 @@ typedef enum grkan_status {
   GRKAN_ERR_ACCUM_OVERFLOW = 4,    /* AccumulationOverflowError (backward.py:182-184)    */
   GRKAN_ERR_UNSUPPORTED = 5,       /* dtype / degree this build does not provide         */
   GRKAN_ERR_CUDA = 6,              /* a CUDA runtime call failed                         */
-  GRKAN_ERR_INVALID = 7            /* null pointer, short workspace, bad flag            */
+  GRKAN_ERR_INVALID = 7,           /* null pointer, short workspace, bad flag            */
+  GRKAN_ERR_PEER_TIMEOUT = 8       /* grkan_bwd_p2p: a peer rank never arrived            */
 } grkan_status;
 
 /* Element types; 0/1 match the GRKB dump dtype codes (cli.py:54). */
@@ -80,6 +81,8 @@ GRKAN_API const char* grkan_last_error(void);
 typedef struct grkan_device_status {
   int32_t nonfinite_input; /* 1 if any x / dy element was NaN or Inf (CHECK_FINITE) */
   int32_t accum_overflow;  /* 1 if any da / db entry is non-finite                  */
+  int32_t peer_timeout;    /* 1 if grkan_bwd_p2p's wait for the peers expired        */
+  int32_t reserved;
 } grkan_device_status;
 
 /* Forward: y = P(x) / (1 + |A(x)|) per group.  `status` may be NULL unless
@@ -194,7 +197,8 @@ GRKAN_API int grkan_bwd_terms(const void* x, const void* dy, const void* a, cons
                               uint32_t flags, void* stream);
 
 /* Synchronise `stream` and copy the device status to the host; maps it to a
- * status code (NONFINITE_INPUT first, then ACCUM_OVERFLOW, else OK). */
+ * status code (NONFINITE_INPUT first, then PEER_TIMEOUT, then ACCUM_OVERFLOW,
+ * else OK). */
 GRKAN_API int grkan_read_status(const grkan_device_status* status, void* stream,
                       grkan_device_status* host_out);
 

@@ -23,6 +23,7 @@ ERR_ACCUM_OVERFLOW = 4
 ERR_UNSUPPORTED = 5
 ERR_CUDA = 6
 ERR_INVALID = 7
+ERR_PEER_TIMEOUT = 8
 
 DT_F32 = 0
 DT_F64 = 1
@@ -52,7 +53,8 @@ class NativeLibraryError(RuntimeError):
 
 
 class DeviceStatus(ctypes.Structure):
-    _fields_ = [("nonfinite_input", ctypes.c_int32), ("accum_overflow", ctypes.c_int32)]
+    _fields_ = [("nonfinite_input", ctypes.c_int32), ("accum_overflow", ctypes.c_int32),
+                ("peer_timeout", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 _lib = None

@@ -263,6 +263,7 @@ const char* grkan_status_string(int status) {
     case GRKAN_ERR_UNSUPPORTED: return "unsupported";
     case GRKAN_ERR_CUDA: return "cuda error";
     case GRKAN_ERR_INVALID: return "invalid argument";
+    case GRKAN_ERR_PEER_TIMEOUT: return "peer exchange timed out";
     default: return "unknown status";
   }
 }
@@ -564,6 +565,8 @@ int grkan_read_status(const grkan_device_status* status, void* stream,
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(e, "grkan_read_status");
   if (host_out->nonfinite_input) return fail(GRKAN_ERR_NONFINITE_INPUT, "non-finite input");
+  if (host_out->peer_timeout)
+    return fail(GRKAN_ERR_PEER_TIMEOUT, "peer exchange timed out: a rank never arrived (grkan_bwd_p2p)");
   if (host_out->accum_overflow) return fail(GRKAN_ERR_ACCUM_OVERFLOW, "accumulation overflow");
   return GRKAN_OK;
 }

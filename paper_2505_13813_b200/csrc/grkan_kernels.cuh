@@ -448,8 +448,9 @@ __global__ void __launch_bounds__(kBlock)
 // Overflow check for K4's outputs (one thread per coefficient).
 template <typename A>
 __global__ void k_check_finite(const A* __restrict__ v, int64_t cnt, DevStatus* __restrict__ st) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < cnt && nonfinite(v[i])) st->accum_overflow = 1;
+  // grid-stride: any coefficient count (n_groups * (m + 1) is unbounded)
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+    if (nonfinite(v[i])) st->accum_overflow = 1;
 }
 
 }  // namespace grkan

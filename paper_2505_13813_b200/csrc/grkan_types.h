@@ -30,6 +30,8 @@ struct Geom {
 struct DevStatus {
   int32_t nonfinite_input;
   int32_t accum_overflow;
+  int32_t peer_timeout;  // grkan_bwd_p2p: a peer never arrived (bounded wait expired)
+  int32_t reserved;
 };
 
 constexpr int kBlock = 256;    // threads per CTA for K1 / K2 / K4

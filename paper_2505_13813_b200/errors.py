@@ -51,6 +51,10 @@ class CudaError(GrkanError):
     """A CUDA runtime call inside the library failed."""
 
 
+class PeerExchangeTimeoutError(CudaError):
+    """grkan_bwd_p2p: a peer rank never arrived at the da/db exchange (bounded wait expired)."""
+
+
 def raise_for_status(code: int, message: str = "") -> None:
     from . import _native as N
 
@@ -64,5 +68,6 @@ def raise_for_status(code: int, message: str = "") -> None:
         N.ERR_UNSUPPORTED: UnsupportedError,
         N.ERR_CUDA: CudaError,
         N.ERR_INVALID: ValueError,
+        N.ERR_PEER_TIMEOUT: PeerExchangeTimeoutError,
     }.get(code, GrkanError)
     raise cls(message or "grkan status %d" % code)

@@ -27,6 +27,8 @@ import torch
 from . import _native as N
 from .errors import LayoutMismatchError, UnsupportedError, raise_for_status
 
+STATUS_WORDS = 4  # grkan_device_status: nonfinite_input, accum_overflow, peer_timeout, reserved
+STATUS_BYTES = 4 * STATUS_WORDS
 _DT = {torch.float32: N.DT_F32, torch.bfloat16: N.DT_BF16, torch.float64: N.DT_F64}
 
 
@@ -98,7 +100,7 @@ def rational_forward(x: torch.Tensor, a: torch.Tensor, b: torch.Tensor, exact: b
     y = torch.empty_like(x) if out is None else out
     if y.shape != x.shape or y.dtype != x.dtype or not y.is_contiguous():
         raise ValueError("out must be a contiguous tensor like x")
-    status = torch.zeros(2, dtype=torch.int32, device=x.device) if check_finite else None
+    status = torch.zeros(STATUS_WORDS, dtype=torch.int32, device=x.device) if check_finite else None
     with torch.cuda.device(x.device):
         rc = N.lib().grkan_fwd(x.data_ptr(), y.data_ptr(), a.data_ptr(), _ptr(b), rows, d, ng, m1, n,
                                _DT[x.dtype], _flags(exact, check_finite), _ptr(status),
@@ -163,7 +165,7 @@ def rational_backward(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor, b: tor
                                _stream(x.device))
         _raise(rc)
         if check_finite or check_overflow:
-            read_status(workspace[:8])
+            read_status(workspace[:STATUS_BYTES])
     return dx, da, db
 
 
@@ -196,7 +198,7 @@ def backward_partials(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor, b: tor
     if part.shape != (n_blocks, ng, m1 + n) or part.dtype != a.dtype or not part.is_contiguous():
         raise ValueError("part_out must be a contiguous %s tensor of shape %s"
                          % (a.dtype, (n_blocks, ng, m1 + n)))
-    status = torch.zeros(2, dtype=torch.int32, device=x.device) if check_finite else None
+    status = torch.zeros(STATUS_WORDS, dtype=torch.int32, device=x.device) if check_finite else None
     with torch.cuda.device(x.device):
         rc = N.lib().grkan_bwd_partials(x.data_ptr(), dy.data_ptr(), a.data_ptr(), _ptr(b), dx.data_ptr(),
                                         part.data_ptr(), part.numel() * part.element_size(), rows, d, ng,
@@ -218,7 +220,7 @@ def reduce_partials(part: torch.Tensor, m1: int, n: int, check_overflow: bool = 
     nb, ng = part.shape[0], part.shape[1]
     da = torch.empty((ng, m1), dtype=part.dtype, device=part.device) if da_out is None else da_out
     db = torch.empty((ng, n), dtype=part.dtype, device=part.device) if db_out is None else db_out
-    status = torch.zeros(2, dtype=torch.int32, device=part.device)
+    status = torch.zeros(STATUS_WORDS, dtype=torch.int32, device=part.device)
     dt = N.DT_F64 if part.dtype == torch.float64 else N.DT_F32
     with torch.cuda.device(part.device):
         rc = N.lib().grkan_reduce_partials(part.data_ptr(), nb, ng, m1, n, da.data_ptr(), _ptr(db), dt,
@@ -237,7 +239,7 @@ def rational_backward_atomic(x, dy, a, b, exact: bool = False, check_overflow: b
     dx = torch.empty_like(x)
     da = torch.empty((ng, m1), dtype=a.dtype, device=x.device)
     db = torch.empty((ng, n), dtype=a.dtype, device=x.device)
-    status = torch.zeros(2, dtype=torch.int32, device=x.device)
+    status = torch.zeros(STATUS_WORDS, dtype=torch.int32, device=x.device)
     with torch.cuda.device(x.device):
         rc = N.lib().grkan_bwd_atomic(x.data_ptr(), dy.data_ptr(), a.contiguous().data_ptr(),
                                       _ptr(b.contiguous()), dx.data_ptr(), da.data_ptr(), _ptr(db),
@@ -313,7 +315,7 @@ def linear_backward_fused(dy: torch.Tensor, w: torch.Tensor, x: torch.Tensor, a:
                                       rows, feat, k, ng, N.FLAG_FAST, _stream(x.device))
         _raise(rc)
         if check_overflow:
-            read_status(ws[:8])
+            read_status(ws[:STATUS_BYTES])
     return dx, da, db
 
 

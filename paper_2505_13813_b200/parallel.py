@@ -248,7 +248,7 @@ class PeerExchange:
                                        self.rank, self.world, self.epoch, ops._stream(x.device))
             self._check(rc)
             if check_overflow:
-                ops.read_status(ws[:8])
+                ops.read_status(ws[:ops.STATUS_BYTES])
         return dx, da, db
 
     def close(self):

@@ -59,14 +59,16 @@ class HostPipeline:
             r0, r1 = i * self.chunk_rows, min(rows, (i + 1) * self.chunk_rows)
             nr = r1 - r0
             with torch.cuda.stream(self.h2d):
-                if i >= 2:
-                    self.h2d.wait_event(self.ev_comp[s])  # slot's inputs consumed
+                # The slot's inputs must be consumed before they are overwritten --
+                # also across calls: chunks 0/1 of this call reuse the slots the
+                # previous call's last chunks may still be reading.  An event that
+                # was never recorded is already complete, so the first call is free.
+                self.h2d.wait_event(self.ev_comp[s])
                 self.x[s][:nr].copy_(xr[r0:r1], non_blocking=True)
                 self.dy[s][:nr].copy_(dyr[r0:r1], non_blocking=True)
                 self.ev_in[s].record(self.h2d)
             comp.wait_event(self.ev_in[s])
-            if i >= 2:
-                comp.wait_event(self.ev_out[s])  # slot's outputs drained to the host
+            comp.wait_event(self.ev_out[s])  # slot's outputs drained to the host (this or the previous call)
             ops.rational_forward(self.x[s][:nr], a, b, exact=exact, out=self.y[s][:nr])
             dx_s = self.dx[s][:nr]
             ops.rational_backward(self.x[s][:nr], self.dy[s][:nr], a, b, exact=exact,

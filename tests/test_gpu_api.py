@@ -385,6 +385,32 @@ def test_host_pipeline_matches_one_shot():
         assert torch.equal(da, da2) and torch.equal(db, db2)  # deterministic
 
 
+def test_host_pipeline_back_to_back_calls_do_not_race():
+    """Two fwd_bwd calls with different inputs and no synchronisation in between:
+    the second call's first chunks reuse the device slots the first call's last
+    chunks read, so it must wait for them (write-after-read across calls)."""
+    from paper_2505_13813_b200 import ops
+    from paper_2505_13813_b200.streaming import HostPipeline
+    torch.manual_seed(16)
+    xs = [torch.randn(1379, 768) for _ in range(3)]
+    dys = [torch.randn(1379, 768) for _ in range(3)]
+    a = torch.randn(8, 6, device=DEV)
+    b = torch.randn(8, 4, device=DEV)
+    pipe = HostPipeline(DEV, 768, 8, chunk_rows=300)
+    pin = lambda t: t.pin_memory()  # noqa: E731
+    xh, dyh = [pin(t) for t in xs], [pin(t) for t in dys]
+    yh = [torch.empty_like(t).pin_memory() for t in xs]
+    dxh = [torch.empty_like(t).pin_memory() for t in xs]
+    grads = [pipe.fwd_bwd(xh[k], dyh[k], a, b, yh[k], dxh[k]) for k in range(3)]  # no sync between
+    torch.cuda.synchronize()
+    for k in range(3):
+        y_ref = ops.rational_forward(xs[k].to(DEV), a, b)
+        dx_ref, da_ref, db_ref = ops.rational_backward(xs[k].to(DEV), dys[k].to(DEV), a, b)
+        assert torch.equal(yh[k], y_ref.cpu()) and torch.equal(dxh[k], dx_ref.cpu()), k
+        rel = lambda u, v: ((u - v).abs().max() / v.abs().max()).item()  # noqa: E731
+        assert rel(grads[k][0], da_ref) <= 1e-6 and rel(grads[k][1], db_ref) <= 1e-6, k
+
+
 def test_kat_training_smoke():
     """KAT-T (GR-KAN MLPs on the B200 unit) fits a fixed tiny batch (cf. pkg/tests/test_acceptance.py:174-229)."""
     from paper_2505_13813_b200 import kat

@@ -115,3 +115,68 @@ def test_peer_exchange_empty_shard():
             assert float(da.abs().sum()) == 0.0 and float(db.abs().sum()) == 0.0
     finally:
         ex.close()
+
+
+def test_peer_exchange_more_columns_than_ctas():
+    """192 groups x (5, 4) = 1920 columns: the fixed grid of <= 128 CTAs loops over
+    them (no whole-grid co-residency needed); one rank == K2 + K3 bits."""
+    from paper_2505_13813_b200 import ops, parallel
+
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device="cpu").manual_seed(5)
+    x = torch.randn(300, 1536, generator=g).to(dev)
+    u = torch.randn(300, 1536, generator=g).to(dev)
+    a = torch.randn(192, 6, generator=g).to(dev)
+    b = torch.randn(192, 4, generator=g).to(dev)
+    ex = parallel.PeerExchange(192, 6, 4, dev)
+    try:
+        for _ in range(2):
+            dx, da, db = ex.backward(x, u, a, b, check_overflow=True)
+            dx0, da0, db0 = ops.rational_backward(x, u, a, b)
+            assert torch.equal(dx, dx0) and torch.equal(da, da0) and torch.equal(db, db0)
+    finally:
+        ex.close()
+
+
+def _timeout_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2505_13813_b200 import parallel
+    from paper_2505_13813_b200.errors import PeerExchangeTimeoutError
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["GRKAN_P2P_TIMEOUT_MS"] = "1500"
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    ex = parallel.PeerExchange(8, 6, 4, dev)
+    outcome = "no-call"
+    try:
+        if rank == 0:  # rank 1 "fails before launching": it never joins the exchange
+            x, u, a, b = [torch.from_numpy(t[0] if t.ndim == 3 else t).to(dev) for t in _inputs(0)]
+            try:
+                ex.backward(x, u, a, b, check_overflow=True)
+                outcome = "returned"
+            except PeerExchangeTimeoutError:
+                outcome = "timeout"
+        dist.barrier()  # rank 1 keeps its buffer mapped until rank 0 is done
+        q.put((rank, outcome))
+    finally:
+        ex.close()
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_missing_rank_times_out_instead_of_hanging():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_timeout_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] == "timeout" and res[1] == "no-call"
