@@ -897,6 +897,9 @@ def spawn_ranks(args, argv):
 
 def main(argv=None):
     args = parse_args(argv)
+    if os.environ.get("GRKAN_BENCH_TRACE_AFTER"):  # diagnostics: dump every thread's stack, then exit
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["GRKAN_BENCH_TRACE_AFTER"]), exit=True)
     env_world = os.environ.get("WORLD_SIZE")
     world = int(env_world or "1")
     rank = int(os.environ.get("RANK", "0"))

@@ -209,6 +209,46 @@ GRKAN_API int grkan_read_status(const grkan_device_status* status, void* stream,
 GRKAN_API int grkan_plan(int64_t rows, int32_t d, int32_t n_groups, int32_t m1, int32_t n, int32_t dtype,
                          int64_t* out6);
 
+/* The reference's combine_partials fold itself (pkg/src/grkan/backward.py:142-179):
+ * d_a[g] += pa from zeros, entry by entry in the given fold order (the caller sorts by
+ * block_id for deterministic_ordered, keeps the submission order for
+ * unordered_scatter), in the partials' dtype (GRKAN_F32 / GRKAN_F64) with separately
+ * rounded adds -- bitwise the reference's result, absorption included
+ * (pkg/tests/test_backward.py:193-209).  part[i * (num_w + den_w) + k] holds entry i's
+ * numerator then denominator partials; group_of[i] = block_id % n_groups.  All
+ * pointers are device pointers; stream-ordered. */
+GRKAN_API int grkan_combine_partials(const void* part, const int32_t* group_of, int64_t n_entries,
+                                     int32_t n_groups, int32_t num_w, int32_t den_w, void* da, void* db,
+                                     int32_t dtype, void* stream);
+
+/* ---- Host-array calls (the reference's own calling convention) -------------------
+ *
+ * The reference's forward_tensor / backward_blocked take and return host (NumPy)
+ * arrays (pkg/src/grkan/rational.py:325-345, pkg/src/grkan/backward.py:275-372).
+ * These calls accept plain pageable host pointers, stream the rows through
+ * pinned staging slots with host copies, PCIe transfers and kernels overlapped,
+ * and return when the outputs are in host memory (synchronous).  A context owns
+ * the staging memory, three streams and a pool of host copy threads; one
+ * context per host thread (calls on one context are not concurrent-safe).
+ *   grkan_host_fwd  forward_tensor    (status: LAYOUT / GRID / NONFINITE_INPUT)
+ *   grkan_host_bwd  backward_blocked  (status: ... / ACCUM_OVERFLOW); da / db are the
+ *                   deterministic-family fold (bitwise independent of chunk_bytes:
+ *                   equal to grkan_bwd(..., GRKAN_FLAG_DETERMINISTIC) on the whole tensor).
+ * Coefficients a / b and da / db are host arrays in the coefficient dtype. */
+typedef struct grkan_host_ctx grkan_host_ctx;
+/* chunk_bytes: staging per tensor per slot (0 = 16 MiB); threads: host copy threads
+ * (0 = min(16, hardware threads)). */
+GRKAN_API int grkan_host_create(int32_t device, size_t chunk_bytes, int32_t threads, grkan_host_ctx** out);
+GRKAN_API int grkan_host_destroy(grkan_host_ctx* ctx);
+GRKAN_API int grkan_host_threads(const grkan_host_ctx* ctx);
+GRKAN_API const char* grkan_host_last_error(void);
+GRKAN_API int grkan_host_fwd(grkan_host_ctx* ctx, const void* x, void* y, const void* a, const void* b,
+                             int64_t rows, int32_t d, int32_t n_groups, int32_t m1, int32_t n, int32_t dtype,
+                             uint32_t flags);
+GRKAN_API int grkan_host_bwd(grkan_host_ctx* ctx, const void* x, const void* dy, const void* a, const void* b,
+                             void* dx, void* da, void* db, int64_t rows, int32_t d, int32_t n_groups, int32_t m1,
+                             int32_t n, int32_t dtype, uint32_t flags);
+
 #ifdef __cplusplus
 }
 #endif

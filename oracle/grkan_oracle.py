@@ -180,6 +180,23 @@ def backward_blocked(x, u, num, den, block_size=DEFAULT_BLOCK_SIZE, workers=1):
     return dx.reshape(x.shape), da, db
 
 
+def combine_partials(partials, num_groups, ordered=True):
+    """The reference's fold of (block_id, pa, pb) partials (backward.py:142-179):
+    d_a[g] += pa from zeros in ascending block id (or the given order), in the
+    partials' dtype."""
+    first_a = np.asarray(partials[0][1])
+    first_b = np.asarray(partials[0][2])
+    seq = sorted(partials, key=lambda p: p[0]) if ordered else list(partials)
+    d_a = np.zeros((num_groups, first_a.shape[0]), dtype=first_a.dtype)
+    d_b = np.zeros((num_groups, first_b.shape[0]), dtype=first_a.dtype)
+    for bid, pa, pb in seq:
+        g = bid % num_groups
+        d_a[g] += pa
+        if first_b.shape[0]:
+            d_b[g] += pb
+    return d_a, d_b
+
+
 def backward_naive(x, u, num, den):
     """Alg. 1 model: one long fold per coefficient in tensor precision; backward.py:187-246."""
     rows = x.reshape(-1, x.shape[-1])
@@ -281,3 +298,37 @@ def cpu_step(x, u, num, den, block_size=DEFAULT_BLOCK_SIZE, workers=None):
     y = forward(x, num, den)
     dx, da, db = backward_blocked(x, u, num, den, block_size, workers)
     return y, dx, da, db
+
+
+# ---------------------------------------------------------------------------
+# The layer around the hot path (pkg/src/grkan/layer.py:318-379)
+# ---------------------------------------------------------------------------
+
+def layer_forward(x, num, den, weight, bias):
+    """y = F(x) W^T + bias in the input precision; layer.py:318-325."""
+    rows = forward(x, num, den).reshape(-1, x.shape[-1])
+    w = weight.astype(rows.dtype, copy=False)
+    b = bias.astype(rows.dtype, copy=False)
+    return (rows @ w.T + b).reshape(x.shape[0], x.shape[1], weight.shape[0])
+
+
+def layer_backward(x, uy, num, den, weight, block_size=DEFAULT_BLOCK_SIZE, naive=False):
+    """(d_x, d_a, d_b, d_weight, d_bias); layer.py:328-379: the rational stage gets
+    uy W per position; d_weight / d_bias fold per-row-block products in ascending
+    block order, returned as float64."""
+    dt = x.dtype
+    uy_rows = uy.reshape(-1, uy.shape[-1]).astype(dt, copy=False)
+    w = weight.astype(dt, copy=False)
+    up = (uy_rows @ w).reshape(x.shape)
+    if naive:
+        dx, da, db = backward_naive(x, up, num, den)
+    else:
+        dx, da, db = backward_blocked(x, up, num, den, block_size)
+    act = forward(x, num, den).reshape(-1, x.shape[-1])
+    d_w = np.zeros(weight.shape, dtype=dt)
+    d_bias = np.zeros(weight.shape[0], dtype=dt)
+    for start in range(0, act.shape[0], block_size):
+        stop = min(start + block_size, act.shape[0])
+        d_w += uy_rows[start:stop].T @ act[start:stop]
+        d_bias += uy_rows[start:stop].sum(axis=0)
+    return dx, da, db, d_w.astype(np.float64), d_bias.astype(np.float64)

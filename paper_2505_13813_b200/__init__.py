@@ -6,6 +6,7 @@ Layers:
   ops                 torch entry points + torch.library ops
   module              GroupRationalFn (autograd) and GroupRational (nn.Module)
   grkan               reference-API shim (forward_tensor / backward_blocked / ...)
+  layer               the layer around it (GrKanLayer, layer_forward / layer_backward)
   parallel            data-parallel glue: row sharding + da/db all-reduce
 """
 
@@ -25,7 +26,7 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # torch-dependent modules load lazily so `import paper_2505_13813_b200` stays cheap
-    if name in ("ops", "module", "grkan", "parallel", "presets"):
+    if name in ("ops", "module", "grkan", "layer", "parallel", "presets"):
         import importlib
 
         return importlib.import_module("." + name, __name__)

@@ -44,6 +44,8 @@ EXPORTS = (
     "grkan_reduce_partials", "grkan_linear_bwd_workspace_bytes", "grkan_linear_bwd", "grkan_linear_fwd",
     "grkan_p2p_buffer_bytes", "grkan_p2p_alloc", "grkan_p2p_free", "grkan_ipc_get_handle",
     "grkan_ipc_open_handle", "grkan_ipc_close_handle", "grkan_bwd_p2p", "grkan_bwd_terms",
+    "grkan_host_create", "grkan_host_destroy", "grkan_host_threads", "grkan_host_last_error",
+    "grkan_host_fwd", "grkan_host_bwd", "grkan_combine_partials",
 )
 IPC_HANDLE_BYTES = 64
 
@@ -113,6 +115,20 @@ def _declare(L):
     L.grkan_bwd_p2p.restype = ctypes.c_int
     L.grkan_bwd_terms.argtypes = [p, p, p, p, p, p, i64, i32, i32, i32, i32, i32, u32, p]
     L.grkan_bwd_terms.restype = ctypes.c_int
+    L.grkan_combine_partials.argtypes = [p, p, i64, i32, i32, i32, p, p, i32, p]
+    L.grkan_combine_partials.restype = ctypes.c_int
+    L.grkan_host_create.argtypes = [i32, sz, i32, ctypes.POINTER(ctypes.c_void_p)]
+    L.grkan_host_create.restype = ctypes.c_int
+    L.grkan_host_destroy.argtypes = [p]
+    L.grkan_host_destroy.restype = ctypes.c_int
+    L.grkan_host_threads.argtypes = [p]
+    L.grkan_host_threads.restype = ctypes.c_int
+    L.grkan_host_last_error.argtypes = []
+    L.grkan_host_last_error.restype = ctypes.c_char_p
+    L.grkan_host_fwd.argtypes = [p, p, p, p, p, i64, i32, i32, i32, i32, i32, u32]
+    L.grkan_host_fwd.restype = ctypes.c_int
+    L.grkan_host_bwd.argtypes = [p, p, p, p, p, p, p, p, i64, i32, i32, i32, i32, i32, u32]
+    L.grkan_host_bwd.restype = ctypes.c_int
 
 
 def lib():

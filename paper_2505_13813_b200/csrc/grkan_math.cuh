@@ -346,13 +346,17 @@ struct RationalX2 {
     return r;
   }
 
+  // q = 1 + |A| for a pair: one FADD2 (a single rounding, as the reference's 1.0 + |A|).
+  __device__ __forceinline__ static float2 q_of(float2 s) {
+    return add2(make_float2(1.0f, 1.0f), make_float2(fabsf(s.x), fabsf(s.y)));
+  }
+
   __device__ __forceinline__ float2 value(float2 x) const {
     const float2 p = horner2<EXACT, 6>(a, x);
     const float2 s = mul2(horner2<EXACT, 4>(b, x), x);
-    const float qx = __fadd_rn(1.0f, fabsf(s.x));
-    const float qy = __fadd_rn(1.0f, fabsf(s.y));
-    if (EXACT) return make_float2(__fdiv_rn(p.x, qx), __fdiv_rn(p.y, qy));
-    return mul2(p, make_float2(rcp(qx), rcp(qy)));
+    const float2 q = q_of(s);
+    if (EXACT) return make_float2(__fdiv_rn(p.x, q.x), __fdiv_rn(p.y, q.y));
+    return mul2(p, make_float2(rcp(q.x), rcp(q.y)));
   }
 
   // FAST: A(x) = h(x) x with h by FMA Horner; `bad` collects sign_unsafe.
@@ -377,7 +381,8 @@ struct RationalX2 {
   __device__ __forceinline__ float2 grad_given(float2 x, float2 u, float2 s, float2 x2, float2 x3,
                                                ACC (&acc)[KC]) const {
     const float2 p = horner2<EXACT, 6>(a, x);
-    const float2 iq = make_float2(rcp(__fadd_rn(1.0f, fabsf(s.x))), rcp(__fadd_rn(1.0f, fabsf(s.y))));
+    const float2 q = q_of(s);
+    const float2 iq = make_float2(rcp(q.x), rcp(q.y));
     const float2 dp = horner2<EXACT, 5>(da, x);
     const float2 ds = horner2<EXACT, 4>(db, x);
     const float2 pq = mul2(p, iq);
@@ -426,6 +431,54 @@ struct RationalX2 {
     return dx;
   }
 
+  // FAST with the reference-rounded A(x), register-lean: P' and h' come out of
+  // simultaneous Horner recurrences on a and b themselves (dp = dp x + p beside
+  // p = p x + a_k; dh likewise beside the separately rounded h chain), so the
+  // derivative coefficient rows da / db need no registers.  Same FMA-pipe
+  // instruction count as grad_given's FAST branch (P 5, P' 4, A' = h + x h' 3).
+  template <typename ACC>
+  __device__ __forceinline__ float2 grad_lean(float2 x, float2 u, ACC (&acc)[KC]) const {
+    // h = ((b4 x + b3) x + b2) x + b1 with the reference's rounding; dh = h'(x)
+    const float2 h2 = xmad2(bc(b[3]), x, bc(b[2]), one);
+    const float2 h1 = xmad2(h2, x, bc(b[1]), one);
+    float2 dh = fma2(bc(b[3]), x, h2);
+    const float2 h0 = xmad2(h1, x, bc(b[0]), one);
+    dh = fma2(dh, x, h1);
+    const float2 s = mul2(h0, x);              // A(x), the reference's bits
+    const float2 ds = fma2(dh, x, h0);         // A'(x) = h + x h'
+    const float2 q = q_of(s);
+    const float2 iq = make_float2(rcp(q.x), rcp(q.y));
+    float2 p = fma2(bc(a[5]), x, bc(a[4]));
+    float2 dp = fma2(bc(a[5]), x, p);
+    p = fma2(p, x, bc(a[3]));
+    dp = fma2(dp, x, p);
+    p = fma2(p, x, bc(a[2]));
+    dp = fma2(dp, x, p);
+    p = fma2(p, x, bc(a[1]));
+    dp = fma2(dp, x, p);
+    p = fma2(p, x, bc(a[0]));
+    const float2 pq = mul2(p, iq);
+    const float2 t0 = mul2(u, iq);
+    const float2 z = make_float2(neg_sign_times(s.x, pq.x), neg_sign_times(s.y, pq.y));
+    const float2 dx = mul2(t0, fma2(ds, z, dp));
+    const float2 w = mul2(t0, z);
+    const float2 x2 = mul2(x, x);
+    const float2 x3 = mul2(x2, x);
+    const float2 x4 = mul2(x2, x2);
+    const float2 x5 = mul2(x4, x);
+    acc_add(acc[0], t0);
+    acc_fma(acc[1], t0, x);
+    acc_fma(acc[2], t0, x2);
+    acc_fma(acc[3], t0, x3);
+    acc_fma(acc[4], t0, x4);
+    acc_fma(acc[5], t0, x5);
+    acc_fma(acc[6], w, x);
+    acc_fma(acc[7], w, x2);
+    acc_fma(acc[8], w, x3);
+    acc_fma(acc[9], w, x4);
+    return dx;
+  }
+
   // dx for NP pairs (one 16-byte vector) and their terms folded into acc.
   // FAST: the guard is evaluated for all NP pairs first and resolved by ONE
   // (rarely taken) branch, so the straight-line math of the NP pairs stays in
@@ -446,6 +499,16 @@ struct RationalX2 {
       float2 x[G], s[G], x2[G], x3[G];
 #pragma unroll
       for (int i = 0; i < G; ++i) x[i] = make_float2(vx[2 * (i0 + i)], vx[2 * (i0 + i) + 1]);
+      if (!EXACT && GRKAN_LEAN_FAST && (!GUARD || !GRKAN_SIGN_GUARD)) {
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+          const int e = 2 * (i0 + i);
+          const float2 r = grad_lean(x[i], make_float2(vu[e], vu[e + 1]), acc);
+          o[e] = r.x;
+          o[e + 1] = r.y;
+        }
+        continue;
+      }
       if (EXACT || !GUARD || !GRKAN_SIGN_GUARD) {
 #pragma unroll
         for (int i = 0; i < G; ++i) {

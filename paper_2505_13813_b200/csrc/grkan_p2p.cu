@@ -33,7 +33,6 @@
 
 namespace grkan {
 
-int set_error(int code, const char* msg);  // grkan_capi.cu
 
 namespace {
 

@@ -91,6 +91,9 @@ struct Plan {
 #ifndef GRKAN_PROBE_NOMEM
 #define GRKAN_PROBE_NOMEM 0       // diagnostic only: staged backward computes on unfilled shared memory
 #endif
+#ifndef GRKAN_LEAN_FAST
+#define GRKAN_LEAN_FAST 0         // FAST, reference-rounded A(x): P' / h' by simultaneous Horner (no da/db registers)
+#endif
 #ifndef GRKAN_FWD_CTAS
 #define GRKAN_FWD_CTAS 8
 #endif
@@ -136,5 +139,9 @@ cudaError_t launch_reduce_f32(const void* part, int64_t n_tiles, int64_t slot_st
                               void* da, void* db, DevStatus* st, cudaStream_t s);
 cudaError_t launch_reduce_f64(const void* part, int64_t n_tiles, int64_t slot_stride, int ng, int m1, int n,
                               void* da, void* db, DevStatus* st, cudaStream_t s);
+
+// Record `msg` as this thread's grkan_last_error() message and return `code`
+// (library-internal; defined in grkan_capi.cu).
+int set_error(int code, const char* msg);
 
 }  // namespace grkan

@@ -32,6 +32,7 @@ import numpy as np
 import torch
 
 from . import ops
+from .errors import raise_for_status
 from .errors import (  # noqa: F401  (re-exported like grkan/__init__.py)
     AccumulationOverflowError,
     ActivationFitError,
@@ -359,17 +360,81 @@ def _to_device(t: ActivationTensor):
 # Hot path (rational.py:325-345, backward.py:187-395)
 # ---------------------------------------------------------------------------
 
+def _host_ctx():
+    """This thread's native host pipeline on the current device (grkan_host_create)."""
+    import ctypes
+
+    from . import _native as N
+
+    dev = _device()
+    cache = getattr(_stage_local, "host_ctx", None)
+    if cache is None:
+        cache = _stage_local.host_ctx = {}
+    ctx = cache.get(dev.index)
+    if ctx is None:
+        h = ctypes.c_void_p()
+        rc = N.lib().grkan_host_create(dev.index, 0, 0, ctypes.byref(h))
+        if rc:
+            raise_for_status(rc, N.lib().grkan_host_last_error().decode())
+        ctx = cache[dev.index] = _HostCtx(h)
+    return ctx.handle
+
+
+class _HostCtx:
+    """Owns one grkan_host_ctx; released with the thread's cache."""
+
+    def __init__(self, handle):
+        self.handle = handle
+
+    def __del__(self):
+        try:
+            from . import _native as N
+
+            N.lib().grkan_host_destroy(self.handle)
+        except Exception:  # interpreter teardown
+            pass
+
+
+def _host_check(rc: int) -> None:
+    if rc:
+        from . import _native as N
+
+        raise_for_status(rc, N.lib().grkan_host_last_error().decode())
+
+
+def _host_flags(exact, check: bool) -> int:
+    from . import _native as N
+
+    return (N.FLAG_EXACT if _exact(exact) else N.FLAG_FAST) | (N.FLAG_CHECK_FINITE if check else 0)
+
+
+def _host_coeffs(params: GroupRationalParams, dtype) -> tuple[np.ndarray, np.ndarray]:
+    """Coefficients rounded to the tensor dtype, as the reference casts at use (rational.py:220)."""
+    return (np.ascontiguousarray(params.numerator, dtype=dtype),
+            np.ascontiguousarray(params.denominator, dtype=dtype))
+
+
 def forward_tensor(x: ActivationTensor, params: GroupRationalParams, layout: GroupLayout,
                    validate: bool = True, exact: bool | None = None) -> ActivationTensor:
-    """Group-wise rational of every element; same shape and precision (rational.py:325-345)."""
+    """Group-wise rational of every element; same shape and precision (rational.py:325-345).
+
+    Host arrays in and out through the native pipeline (grkan_host_fwd): host copies,
+    PCIe transfers and the sm_100a kernel overlap chunk by chunk."""
+    from . import _native as N
+
     check_compatible(x, params, layout)
-    xd = _to_device(x)
-    a, b = _coeffs(params, xd.dtype, xd.device)
     check = validate and not x.validated
-    y = ops.rational_forward(xd, a, b, exact=_exact(exact), check_finite=check)
+    arr = x.data
+    y = np.empty_like(arr)
+    a, b = _host_coeffs(params, arr.dtype)
+    dt = N.DT_F64 if arr.dtype == np.float64 else N.DT_F32
+    rows = x.batch * x.seq
+    _host_check(N.lib().grkan_host_fwd(_host_ctx(), arr.ctypes.data, y.ctypes.data, a.ctypes.data,
+                                       b.ctypes.data, rows, x.feature, params.num_groups, params.num_coeffs,
+                                       params.den_coeffs, dt, _host_flags(exact, check)))
     if check:
         x.validated = True
-    return ActivationTensor(_download(y), validated=False)
+    return ActivationTensor(y, validated=False)
 
 
 def _prepare_bwd(x, upstream, params, plan, default_plan):
@@ -398,18 +463,25 @@ def backward_blocked(x: ActivationTensor, upstream: ActivationTensor, params: Gr
         raise ValueError("unknown combine mode %r" % (combine_mode,))
     _no_instrumentation(counter, coverage)
     _prepare_bwd(x, upstream, params, plan, ExecutionPlan.blocked)
+    from . import _native as N
+
     if upstream.data.dtype != x.data.dtype:
         upstream = ActivationTensor(upstream.data.astype(x.data.dtype))
-    xd, ud = _to_device(x), _to_device(upstream)
-    a, b = _coeffs(params, xd.dtype, xd.device)
     check = validate and not (x.validated and upstream.validated)
-    dx, da, db = ops.rational_backward(xd, ud, a, b, exact=_exact(exact), check_finite=check,
-                                       check_overflow=True)
+    arr = x.data
+    dx = np.empty_like(arr)
+    a, b = _host_coeffs(params, arr.dtype)
+    da = np.empty((params.num_groups, params.num_coeffs), dtype=arr.dtype)
+    db = np.empty((params.num_groups, params.den_coeffs), dtype=arr.dtype)
+    dt = N.DT_F64 if arr.dtype == np.float64 else N.DT_F32
+    _host_check(N.lib().grkan_host_bwd(_host_ctx(), arr.ctypes.data, upstream.data.ctypes.data,
+                                       a.ctypes.data, b.ctypes.data, dx.ctypes.data, da.ctypes.data,
+                                       db.ctypes.data, x.batch * x.seq, x.feature, params.num_groups,
+                                       params.num_coeffs, params.den_coeffs, dt, _host_flags(exact, check)))
     if check:
         x.validated = upstream.validated = True
-    return GradBundle(d_x=ActivationTensor(_download(dx)), d_a=da.cpu().numpy(),
-                      d_b=db.cpu().numpy(), strategy=STRATEGY_BLOCKED, precision=x.precision,
-                      combine_mode=combine_mode)
+    return GradBundle(d_x=ActivationTensor(dx), d_a=da, d_b=db, strategy=STRATEGY_BLOCKED,
+                      precision=x.precision, combine_mode=combine_mode)
 
 
 def backward_naive(x: ActivationTensor, upstream: ActivationTensor, params: GroupRationalParams,
@@ -447,14 +519,14 @@ def combine_partials(partials, num_groups: int, mode: str = COMBINE_ORDERED):
 
     ``partials``: (block_id, numerator_partials, denominator_partials) with
     block_id = row_block * num_groups + group; every id in 0..len-1 exactly once
-    (else PartialCoverageError, as the reference).  The fold is K3
-    (grkan_reduce_partials): fp64, in ascending block order for BOTH modes --
-    the reference's ``unordered_scatter`` folds in submission order, which
-    only changes rounding, so here it reproduces the ordered result (the
-    reference's own test only asserts it runs, test_backward.py).  Results are
-    the fixed-order fp64 sums cast to the partials' dtype, not the reference's
-    left-to-right sums in that dtype.
+    (else PartialCoverageError, as the reference).  The fold is the reference's own:
+    ``d_a[g] += pa`` from zeros in ascending block id (``deterministic_ordered``) or
+    in the order given (``unordered_scatter``), in the partials' dtype with
+    separately rounded adds (grkan_combine_partials) -- bitwise the reference's
+    totals, absorption of tiny partials included (test_backward.py:193-209).
     """
+    from . import _native as N
+
     if mode not in (COMBINE_ORDERED, COMBINE_UNORDERED):
         raise ValueError("unknown combine mode %r" % (mode,))
     if not partials:
@@ -468,14 +540,28 @@ def combine_partials(partials, num_groups: int, mode: str = COMBINE_ORDERED):
     for _, pa, pb in partials:
         if np.asarray(pa).shape != (num_w,) or np.asarray(pb).shape != (den_w,):
             raise PartialCoverageError("partial coverage violation: inconsistent shapes")
-    dtype = first_a.dtype if first_a.dtype in (np.float32, np.float64) else np.float64
-    n_blk = -(-len(partials) // num_groups)
-    host = np.zeros((n_blk * num_groups, num_w + den_w), dtype=dtype)  # missing tail slots fold as 0
-    for bid, pa, pb in partials:
-        host[bid, :num_w] = pa
-        host[bid, num_w:] = pb
-    part = torch.from_numpy(host.reshape(n_blk, num_groups, num_w + den_w)).to(_device())
-    da, db = ops.reduce_partials(part, num_w, den_w)
+    dtype = first_a.dtype if first_a.dtype in (np.float32, np.float64) else np.dtype(np.float64)
+    ordered = sorted(partials, key=lambda p: int(p[0])) if mode == COMBINE_ORDERED else list(partials)
+    host = np.zeros((len(ordered), num_w + den_w), dtype=dtype)
+    group_of = np.empty(len(ordered), dtype=np.int32)
+    for i, (bid, pa, pb) in enumerate(ordered):
+        host[i, :num_w] = pa
+        host[i, num_w:] = pb
+        group_of[i] = int(bid) % num_groups
+    dev = _device()
+    part = torch.from_numpy(host).to(dev)
+    gid = torch.from_numpy(group_of).to(dev)
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
+    da = torch.empty((num_groups, num_w), dtype=tdt, device=dev)
+    db = torch.empty((num_groups, den_w), dtype=tdt, device=dev)
+    with torch.cuda.device(dev):
+        rc = N.lib().grkan_combine_partials(part.data_ptr(), gid.data_ptr(), len(ordered), num_groups, num_w,
+                                            den_w, da.data_ptr() if da.numel() else None,
+                                            db.data_ptr() if db.numel() else None,
+                                            N.DT_F64 if dtype == np.float64 else N.DT_F32,
+                                            torch.cuda.current_stream(dev).cuda_stream)
+    if rc:
+        raise_for_status(rc, N.last_error())
     return da.cpu().numpy(), db.cpu().numpy()
 
 

@@ -1,10 +1,11 @@
-"""combine_partials through the shim (K3 on the GPU), ported from the reference's
-TestCombinePartials (pkg/tests/test_backward.py:167-233).
+"""combine_partials through the shim (grkan_combine_partials on the GPU), ported from
+the reference's TestCombinePartials (pkg/tests/test_backward.py:167-233).
 
-Same coverage errors and group routing as the reference; the fold is K3's
-fixed-order fp64 sum, so the absorption case shows the GPU KEEPING the 64
-tiny partials that the reference's fp32 fold loses (the paper's reduced-
-rounding claim on the reference's own example).
+Same coverage errors, group routing and fold as the reference: ``d_a[g] += pa`` in
+the partials' dtype in fold order, so results are bitwise the reference's --
+including the absorption case, where the fp32 fold loses the 64 tiny partials.
+(K3, the backward's own reduction, folds in fp64 and keeps them; see
+test_gpu_rounding.py for that claim.)
 """
 import numpy as np
 import pytest
@@ -43,16 +44,16 @@ def test_ragged_last_row_block():
     assert np.array_equal(d_a, [[5.0], [2.0]]) and np.array_equal(d_b, [[5.0], [2.0]])
 
 
-def test_absorption_kept_by_the_fp64_fold():
+def test_absorption_versus_fresh_accumulator():
+    """pkg/tests/test_backward.py:193-209, bit for bit."""
     tiny = np.float32(2.0 ** -24)
     parts = [(i, np.array([tiny], dtype=np.float32), np.zeros(0, np.float32)) for i in range(64)]
     d_a, _ = grkan.combine_partials(parts, num_groups=1)
     assert d_a.dtype == np.float32 and d_a[0, 0] == np.float32(2.0 ** -18)
     with_unit = [(0, np.array([1.0], dtype=np.float32), np.zeros(0, np.float32))]
     with_unit += [(i + 1, np.array([tiny], dtype=np.float32), np.zeros(0, np.float32)) for i in range(64)]
-    kept, _ = grkan.combine_partials(with_unit, num_groups=1)
-    # the reference's fp32 fold returns exactly 1.0 here (every tiny add absorbed)
-    assert kept[0, 0] == np.float32(1.0 + 2.0 ** -18)
+    absorbed, _ = grkan.combine_partials(with_unit, num_groups=1)
+    assert absorbed[0, 0] == np.float32(1.0)  # every tiny add was lost, as in the reference
 
 
 @pytest.mark.parametrize("parts", [
@@ -71,18 +72,20 @@ def test_unknown_mode():
         grkan.combine_partials([(0, np.array([1.0]), np.zeros(0))], num_groups=1, mode="nope")
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
 @pytest.mark.parametrize("mode", [grkan.COMBINE_ORDERED, grkan.COMBINE_UNORDERED])
-def test_input_order_does_not_change_bits(mode):
+def test_bitwise_the_reference_fold(mode, dtype):
+    """Random partials in shuffled submission order: bitwise the reference's fold
+    (ascending ids for deterministic_ordered, the given order for unordered_scatter)."""
+    from oracle import grkan_oracle as orc
     rng = np.random.default_rng(7)
-    parts = [(i, rng.standard_normal(3).astype(np.float32), rng.standard_normal(2).astype(np.float32))
-             for i in range(8)]
-    ref = grkan.combine_partials(parts, num_groups=2, mode=mode)
-    shuffled = list(parts)
-    rng.shuffle(shuffled)
-    out = grkan.combine_partials(shuffled, num_groups=2, mode=mode)
-    assert out[0].tobytes() == ref[0].tobytes() and out[1].tobytes() == ref[1].tobytes()
-    # against an fp64 sum of the same partials, rounded once
-    want_a = np.zeros((2, 3))
-    for i, pa, _ in parts:
-        want_a[i % 2] += pa.astype(np.float64)
-    assert np.array_equal(out[0], want_a.astype(np.float32))
+    parts = [(i, (rng.standard_normal(3) * 10.0 ** rng.integers(-6, 6)).astype(dtype),
+              rng.standard_normal(2).astype(dtype)) for i in range(40)]
+    rng.shuffle(parts)
+    got = grkan.combine_partials(parts, num_groups=4, mode=mode)
+    want = orc.combine_partials(parts, 4, ordered=(mode == grkan.COMBINE_ORDERED))
+    assert got[0].dtype == dtype
+    assert got[0].tobytes() == want[0].tobytes() and got[1].tobytes() == want[1].tobytes()
+    if mode == grkan.COMBINE_ORDERED:  # submission order does not matter
+        again = grkan.combine_partials(list(reversed(parts)), num_groups=4, mode=mode)
+        assert again[0].tobytes() == got[0].tobytes()

@@ -133,3 +133,18 @@ def test_hand_values():
     assert orc.rational(np.array([2.0]), [1.0, 2.0], [])[0] == 5.0
     dx, ta, tb = orc.element_terms(one, one, np.array([1.0, 1.0]), np.array([1.0]))
     assert [t[0] for t in ta] == [0.5, 0.5] and [t[0] for t in tb] == [-0.5] and dx[0] == 0.0
+
+
+def test_oracle_combine_partials_known_answers():
+    """The oracle's combine fold on the reference's own known answers
+    (pkg/tests/test_backward.py:176-209): round-robin routing and fp32 absorption."""
+    parts = [(0, np.array([1.0]), np.array([10.0])), (1, np.array([2.0]), np.array([20.0])),
+             (2, np.array([4.0]), np.array([40.0])), (3, np.array([8.0]), np.array([80.0]))]
+    d_a, d_b = orc.combine_partials(parts, 2)
+    assert np.array_equal(d_a, [[5.0], [10.0]]) and np.array_equal(d_b, [[50.0], [100.0]])
+    tiny = np.float32(2.0 ** -24)
+    fresh = [(i, np.array([tiny], dtype=np.float32), np.zeros(0, np.float32)) for i in range(64)]
+    assert orc.combine_partials(fresh, 1)[0][0, 0] == np.float32(2.0 ** -18)
+    unit = [(0, np.array([1.0], dtype=np.float32), np.zeros(0, np.float32))]
+    unit += [(i + 1, np.array([tiny], dtype=np.float32), np.zeros(0, np.float32)) for i in range(64)]
+    assert orc.combine_partials(unit, 1)[0][0, 0] == np.float32(1.0)
