@@ -221,6 +221,27 @@ GRKAN_API int grkan_combine_partials(const void* part, const int32_t* group_of, 
                                      int32_t n_groups, int32_t num_w, int32_t den_w, void* da, void* db,
                                      int32_t dtype, void* stream);
 
+/* Access instrumentation: the reference's counter= / coverage= arguments of
+ * backward_blocked / backward_naive (pkg/src/grkan/backward.py:187-195, 275-285,
+ * 326-351) and instrumented_backward (pkg/src/grkan/access.py:129-161).  Runs the
+ * SAME kernels as grkan_bwd (naive = 0) or grkan_bwd_atomic (naive = 1), in their
+ * counting instantiations: every element a thread processes adds 1 to
+ * coverage[row * d + col] (device int32 [rows * d]), and every kernel adds the
+ * element-sized global accesses it performs to counts[0..2] = {reads, writes, rmw}
+ * (device uint64[3]; an atomic add is 1 read + 1 write + 1 rmw, as the reference
+ * models it).  Both accumulate: zero them first.  Unchecked, per-CTA partials; the
+ * device status (overflow) lands at the start of `ws` as for grkan_bwd. */
+GRKAN_API int grkan_bwd_instrumented(const void* x, const void* dy, const void* a, const void* b, void* dx,
+                                     void* da, void* db, void* ws, size_t ws_bytes, int32_t* coverage,
+                                     unsigned long long* counts, int64_t rows, int32_t d, int32_t n_groups,
+                                     int32_t m1, int32_t n, int32_t dtype, uint32_t flags, int32_t naive,
+                                     void* stream);
+/* CTAs one launch uses on this device (kernel 0 = grkan_fwd, 1 = grkan_bwd's K2,
+ * 2 = grkan_bwd_atomic) for 16-byte-aligned tensors; -1 on a layout error.  The
+ * access model's closed forms need it (one coefficient row load per CTA). */
+GRKAN_API int64_t grkan_launch_ctas(int64_t rows, int32_t d, int32_t n_groups, int32_t m1, int32_t n,
+                                    int32_t dtype, int32_t kernel);
+
 /* ---- Host-array calls (the reference's own calling convention) -------------------
  *
  * The reference's forward_tensor / backward_blocked take and return host (NumPy)
@@ -234,9 +255,10 @@ GRKAN_API int grkan_combine_partials(const void* part, const int32_t* group_of, 
  *   grkan_host_bwd  backward_blocked  (status: ... / ACCUM_OVERFLOW); da / db are the
  *                   deterministic-family fold (bitwise independent of chunk_bytes:
  *                   equal to grkan_bwd(..., GRKAN_FLAG_DETERMINISTIC) on the whole tensor).
- * Coefficients a / b and da / db are host arrays in the coefficient dtype. */
+ * Coefficients a / b and da / db are host arrays in the coefficient dtype.  Page-locked
+ * x / dy / y / dx buffers are transferred in place (no staging copy). */
 typedef struct grkan_host_ctx grkan_host_ctx;
-/* chunk_bytes: staging per tensor per slot (0 = 16 MiB); threads: host copy threads
+/* chunk_bytes: staging per tensor per slot (0 = 32 MiB); threads: host copy threads
  * (0 = min(16, hardware threads)). */
 GRKAN_API int grkan_host_create(int32_t device, size_t chunk_bytes, int32_t threads, grkan_host_ctx** out);
 GRKAN_API int grkan_host_destroy(grkan_host_ctx* ctx);

@@ -45,7 +45,8 @@ EXPORTS = (
     "grkan_p2p_buffer_bytes", "grkan_p2p_alloc", "grkan_p2p_free", "grkan_ipc_get_handle",
     "grkan_ipc_open_handle", "grkan_ipc_close_handle", "grkan_bwd_p2p", "grkan_bwd_terms",
     "grkan_host_create", "grkan_host_destroy", "grkan_host_threads", "grkan_host_last_error",
-    "grkan_host_fwd", "grkan_host_bwd", "grkan_combine_partials",
+    "grkan_host_fwd", "grkan_host_bwd", "grkan_combine_partials", "grkan_bwd_instrumented",
+    "grkan_launch_ctas",
 )
 IPC_HANDLE_BYTES = 64
 
@@ -115,6 +116,10 @@ def _declare(L):
     L.grkan_bwd_p2p.restype = ctypes.c_int
     L.grkan_bwd_terms.argtypes = [p, p, p, p, p, p, i64, i32, i32, i32, i32, i32, u32, p]
     L.grkan_bwd_terms.restype = ctypes.c_int
+    L.grkan_bwd_instrumented.argtypes = [p, p, p, p, p, p, p, p, sz, p, p, i64, i32, i32, i32, i32, i32, u32, i32, p]
+    L.grkan_bwd_instrumented.restype = ctypes.c_int
+    L.grkan_launch_ctas.argtypes = [i64, i32, i32, i32, i32, i32, i32]
+    L.grkan_launch_ctas.restype = i64
     L.grkan_combine_partials.argtypes = [p, p, i64, i32, i32, i32, p, p, i32, p]
     L.grkan_combine_partials.restype = ctypes.c_int
     L.grkan_host_create.argtypes = [i32, sz, i32, ctypes.POINTER(ctypes.c_void_p)]

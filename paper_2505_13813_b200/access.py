@@ -21,7 +21,12 @@ both (`tools/access_ncu.py` -> `profiles/r1/access_model_vs_ncu.json`):
                 atomic adds that resolve in L2 (they are RMWs in the
                 reference's model, but not DRAM bytes on the device).
 
-Host-side arithmetic only; no kernels run here.
+``AccessCounter`` / ``AccessReport`` / ``instrumented_backward`` mirror the
+reference's instrumentation (access.py:36-80, 129-161) on the device: the counts
+and the per-element coverage come from the kernels themselves
+(grkan_bwd_instrumented), and the prediction is the B200 closed form
+``predicted_device_accesses`` (one coefficient-row load per CTA, one partial per
+CTA or warp, K3's fold), next to the reference's own model for the same pass.
 """
 from __future__ import annotations
 
@@ -72,6 +77,101 @@ def predicted_total_for_plan(batch: int, seq: int, feature: int, block_size: int
         return predict_accesses_naive(batch, seq, feature, m_coeffs)
     grid_rows = -(-(batch * seq) // block_size)
     return 3 * batch * seq * feature + 3 * m_coeffs * grid_rows * num_groups
+
+
+@dataclass
+class AccessCounter:
+    """Mutable tally of modelled accesses (access.py:36-52)."""
+
+    reads: int = 0
+    writes: int = 0
+    rmw_atomic: int = 0
+
+    def add(self, reads: int = 0, writes: int = 0, rmw: int = 0) -> None:
+        self.reads += reads
+        self.writes += writes
+        self.rmw_atomic += rmw
+
+    @property
+    def total(self) -> int:
+        return self.reads + self.writes
+
+
+@dataclass(frozen=True)
+class AccessReport:
+    """Instrumented access counts next to the closed-form prediction (access.py:55-80).
+
+    ``predicted_total`` is the B200 kernels' closed form (predicted_device_accesses);
+    ``reference_predicted_total`` the reference's model of the same plan."""
+
+    reads: int
+    writes: int
+    rmw_atomic: int
+    total: int
+    predicted_total: int
+    strategy: str
+    reference_predicted_total: int = 0
+
+    @property
+    def matches_prediction(self) -> bool:
+        return self.total == self.predicted_total
+
+    def to_dict(self) -> dict:
+        return {"reads": self.reads, "writes": self.writes, "rmw_atomic": self.rmw_atomic, "total": self.total,
+                "predicted_total": self.predicted_total, "strategy": self.strategy,
+                "reference_predicted_total": self.reference_predicted_total}
+
+
+def predicted_device_accesses(rows: int, d: int, n_groups: int, m1: int = 6, n: int = 4, dtype: str = "fp32",
+                              naive: bool = False) -> tuple[int, int, int]:
+    """(reads, writes, rmw) element accesses of one B200 backward, in the reference's units.
+
+    blocked (K2 + K3): x, dy read and dx written once per element; one coefficient-row
+    load per K2 CTA; m_c partial stores per partial slot (one per CTA, or per consumer
+    warp in the staged kernel), all read back once by K3, which stores m_c * n_groups
+    results.  naive (K4, Alg. 1): x, dy, dx per element plus m_c atomic adds per
+    element (1 read + 1 write + 1 rmw each), one coefficient-row load per CTA.
+    """
+    code = _DT[dtype][0]
+    mc = m1 + n
+    e = rows * d
+    if naive:
+        ctas = N.lib().grkan_launch_ctas(rows, d, n_groups, m1, n, code, 2)
+        return e * (2 + mc) + mc * ctas, e * (1 + mc), e * mc
+    ctas = N.lib().grkan_launch_ctas(rows, d, n_groups, m1, n, code, 1)
+    parts = N.plan(rows, d, n_groups, m1, n, code)["partials_per_group"] * n_groups
+    return 2 * e + mc * ctas + mc * parts, e + mc * parts + mc * n_groups, 0
+
+
+def instrumented_backward(x, upstream, params, plan, workers: int = 1, combine_mode: str = "deterministic_ordered",
+                          validate: bool = True, exact: bool | None = None):
+    """Run the plan's strategy on the GPU while the kernels count every modelled global
+    access and mark every element they visit (access.py:129-161).  Raises
+    PartialCoverageError unless every element was visited exactly once."""
+    import numpy as np
+
+    from . import grkan as G
+    from .errors import PartialCoverageError
+
+    counter = AccessCounter()
+    coverage = np.zeros((x.batch * x.seq, x.feature), dtype=np.int16)
+    bundle = G.run_backward(x, upstream, params, plan, workers=workers, combine_mode=combine_mode,
+                            validate=validate, counter=counter, coverage=coverage, exact=exact)
+    if not np.all(coverage == 1):
+        raise PartialCoverageError("partial coverage violation: element visited != 1 times")
+    naive = plan.strategy == G.STRATEGY_NAIVE
+    dt = "fp64" if x.data.dtype == np.float64 else "fp32"
+    if x.batch * x.seq == 0:
+        predicted = 0
+    else:
+        predicted = sum(predicted_device_accesses(x.batch * x.seq, x.feature, params.num_groups, params.num_coeffs,
+                                                  params.den_coeffs, dt, naive)[:2])
+    ref = predicted_total_for_plan(x.batch, x.seq, x.feature, plan.block_size, params.num_groups,
+                                   params.total_coeffs, naive=naive) if x.batch * x.seq else 0
+    report = AccessReport(reads=counter.reads, writes=counter.writes, rmw_atomic=counter.rmw_atomic,
+                          total=counter.total, predicted_total=predicted, strategy=plan.strategy,
+                          reference_predicted_total=ref)
+    return bundle, report
 
 
 @dataclass(frozen=True)

@@ -284,6 +284,16 @@ int grkan_plan(int64_t rows, int32_t d, int32_t n_groups, int32_t m1, int32_t n,
   return GRKAN_OK;
 }
 
+int64_t grkan_launch_ctas(int64_t rows, int32_t d, int32_t n_groups, int32_t m1, int32_t n, int32_t dtype,
+                          int32_t kernel) {
+  if (check_layout(rows, d, n_groups, m1, n, dtype, 0) != GRKAN_OK || kernel < 0 || kernel > 2) return -1;
+  const size_t es = elem_size(dtype);
+  const bool vec = vec_ok(d, n_groups, es, {});
+  const Plan p = kernel == 2 ? make_plan(rows, d, n_groups, 0, n, es, vec, 2, sm_count())
+                             : make_plan(rows, d, n_groups, m1, n, es, vec, kernel == 0 ? 1 : 2, sm_count());
+  return p.ctas;
+}
+
 size_t grkan_bwd_workspace_bytes(int64_t rows, int32_t d, int32_t n_groups, int32_t m1, int32_t n,
                                  int32_t dtype) {
   if (check_layout(rows, d, n_groups, m1, n, dtype, 0) != GRKAN_OK) return 0;
@@ -514,6 +524,61 @@ int grkan_reduce_partials(const void* part, int64_t n_blocks, int32_t n_groups, 
   e = launch_reduce(dtype, part, n_blocks, static_cast<int64_t>(n_groups) * (m1 + n), n_groups, m1, n, da, db,
                     reinterpret_cast<DevStatus*>(status), s);
   if (e != cudaSuccess) return cuda_fail(e, "k_bwd_reduce launch");
+  return GRKAN_OK;
+}
+
+int grkan_bwd_instrumented(const void* x, const void* dy, const void* a, const void* b, void* dx, void* da,
+                           void* db, void* ws, size_t ws_bytes, int32_t* coverage, unsigned long long* counts,
+                           int64_t rows, int32_t d, int32_t n_groups, int32_t m1, int32_t n, int32_t dtype,
+                           uint32_t flags, int32_t naive, void* stream) {
+  if (flags & (GRKAN_FLAG_CHECK_FINITE | GRKAN_FLAG_DETERMINISTIC))
+    return fail(GRKAN_ERR_INVALID, "instrumented backward: CHECK_FINITE / DETERMINISTIC not supported");
+  int rc = check_layout(rows, d, n_groups, m1, n, dtype, flags);
+  if (rc) return rc;
+  if (!coverage || !counts) return fail(GRKAN_ERR_INVALID, "instrumented backward needs coverage and counts");
+  if (!ws || !da || (n > 0 && !db)) return fail(GRKAN_ERR_INVALID, "null workspace / gradient pointer");
+  if (!aligned16(ws)) return fail(GRKAN_ERR_INVALID, "workspace must be 16-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DevStatus* st = reinterpret_cast<DevStatus*>(ws);
+  cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(DevStatus), s);
+  const size_t as = acc_size(dtype);
+  if (e == cudaSuccess && (naive || rows == 0)) {
+    e = cudaMemsetAsync(da, 0, static_cast<size_t>(n_groups) * m1 * as, s);
+    if (e == cudaSuccess && n > 0) e = cudaMemsetAsync(db, 0, static_cast<size_t>(n_groups) * n * as, s);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  if (rows == 0) return GRKAN_OK;
+  if (!x || !dy || !dx || !a || (n > 0 && !b)) return fail(GRKAN_ERR_INVALID, "null tensor pointer");
+  const size_t es = elem_size(dtype);
+  const bool vec = vec_ok(d, n_groups, es, {x, dy, dx});
+  // the same plan grkan_bwd / grkan_bwd_atomic pick for these tensors
+  Plan p = naive ? make_plan(rows, d, n_groups, /*m1=*/0, n, es, vec, 2, sm_count())
+                 : make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count());
+  if (!plan_fits(p)) return fail(GRKAN_ERR_GRID, "grid geometry invalid: %lld CTAs", (long long)p.ctas);
+  if (!naive && ws_bytes < ws_bytes_for(p, m1, n, dtype))
+    return fail(GRKAN_ERR_INVALID, "workspace too small: %zu < %zu bytes", ws_bytes, ws_bytes_for(p, m1, n, dtype));
+  p.geo.cov = coverage;
+  p.geo.cnt = counts;
+  LaunchArgs L{};
+  L.plan = &p;
+  L.x = x;
+  L.dy = dy;
+  L.out = dx;
+  L.a = a;
+  L.b = b;
+  L.part = static_cast<char*>(ws) + 256;
+  L.da = da;
+  L.db = db;
+  L.st = st;
+  L.m1 = m1;
+  L.n = n;
+  L.exact = (flags & GRKAN_FLAG_EXACT) != 0;
+  L.vec = vec;
+  L.check = false;
+  L.instr = true;
+  L.stream = s;
+  e = launch(naive ? "atomic" : "bwd", dtype, L);
+  if (e != cudaSuccess) return cuda_fail(e, "instrumented backward launch");
   return GRKAN_OK;
 }
 

@@ -11,6 +11,10 @@
 //   d2h stream     device out-slot          -> pinned out-slot
 //   host threads   memcpy pinned out-slot   -> y / dx chunk i - 2
 //
+// A caller buffer that is already page-locked (a torch pinned tensor behind the NumPy
+// array -- what the shim allocates its outputs in, from torch's caching host
+// allocator) skips its staging copy: the DMA reads or writes it in place.
+//
 // so the host copies of chunk i and i-2 overlap the PCIe transfers and kernels of
 // chunk i-1 (PCIe is full duplex).  The backward writes per-row-block partials (the
 // deterministic family, grkan_bwd_partials) and folds them once at the end with
@@ -251,12 +255,30 @@ int ensure_slots(grkan_host_ctx* c, size_t bytes) {
   return GRKAN_OK;
 }
 
+// Page-locked host memory (cudaHostAlloc / cudaHostRegister, e.g. a torch pinned
+// tensor behind a NumPy array): the DMA engines can read or write it in place, so its
+// chunks skip the staging copy.
+bool is_pinned(const void* p, size_t n) {
+  if (!p || n == 0) return false;
+  cudaPointerAttributes a{}, b{};
+  const char* last = static_cast<const char*>(p) + (n - 1);
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess || cudaPointerGetAttributes(&b, last) != cudaSuccess) {
+    cudaGetLastError();  // clear the sticky-free error of an unknown pointer
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost && b.type == cudaMemoryTypeHost;
+}
+
 // One pipelined pass.  n_in input tensors (1 forward, 2 backward), one output tensor.
 // `launch(i, r0, nr, ins, out)` enqueues chunk i's kernels on c->comp.
 int pipeline(grkan_host_ctx* c, int n_in, const void* const* host_in, void* host_out, int64_t rows,
              size_t row_bytes, int64_t chunk_rows,
              const std::function<int(int64_t, int64_t, int64_t, void* const*, void*)>& launch) {
   const int64_t n_chunks = (rows + chunk_rows - 1) / chunk_rows;
+  const size_t total = static_cast<size_t>(rows) * row_bytes;
+  bool in_pinned[2] = {false, false};
+  for (int t = 0; t < n_in; ++t) in_pinned[t] = is_pinned(host_in[t], total);
+  const bool out_pinned = is_pinned(host_out, total);
   cudaError_t e;
   for (int64_t i = 0; i < n_chunks + kSlots - 1; ++i) {
     if (i < n_chunks) {
@@ -264,14 +286,22 @@ int pipeline(grkan_host_ctx* c, int n_in, const void* const* host_in, void* host
       const int64_t r0 = i * chunk_rows;
       const int64_t nr = std::min(chunk_rows, rows - r0);
       const size_t off = static_cast<size_t>(r0) * row_bytes, nb = static_cast<size_t>(nr) * row_bytes;
-      if (i >= kSlots && (e = cudaEventSynchronize(c->ev_h2d[s])) != cudaSuccess)
+      if (i >= kSlots && !(in_pinned[0] && (n_in < 2 || in_pinned[1])) &&
+          (e = cudaEventSynchronize(c->ev_h2d[s])) != cudaSuccess)
         return hcuda(e, "wait h2d");  // the pinned in-slot has been read by the DMA
-      for (int t = 0; t < n_in; ++t)
-        c->pool->memcpy_par(c->pin_in[t][s], static_cast<const char*>(host_in[t]) + off, nb);
+      const void* src[2] = {nullptr, nullptr};
+      for (int t = 0; t < n_in; ++t) {
+        const char* h = static_cast<const char*>(host_in[t]) + off;
+        if (in_pinned[t]) {
+          src[t] = h;  // DMA straight from the caller's page-locked buffer
+        } else {
+          c->pool->memcpy_par(c->pin_in[t][s], h, nb);
+          src[t] = c->pin_in[t][s];
+        }
+      }
       if ((e = cudaStreamWaitEvent(c->h2d, c->ev_comp[s], 0)) != cudaSuccess) return hcuda(e, "h2d wait");
       for (int t = 0; t < n_in; ++t)
-        if ((e = cudaMemcpyAsync(c->dev_in[t][s], c->pin_in[t][s], nb, cudaMemcpyHostToDevice, c->h2d)) !=
-            cudaSuccess)
+        if ((e = cudaMemcpyAsync(c->dev_in[t][s], src[t], nb, cudaMemcpyHostToDevice, c->h2d)) != cudaSuccess)
           return hcuda(e, "cudaMemcpyAsync(h2d)");
       cudaEventRecord(c->ev_h2d[s], c->h2d);
       cudaStreamWaitEvent(c->comp, c->ev_h2d[s], 0);
@@ -281,13 +311,13 @@ int pipeline(grkan_host_ctx* c, int n_in, const void* const* host_in, void* host
       if (rc != GRKAN_OK) return passthrough(rc);
       cudaEventRecord(c->ev_comp[s], c->comp);
       cudaStreamWaitEvent(c->d2h, c->ev_comp[s], 0);
-      if ((e = cudaMemcpyAsync(c->pin_out[s], c->dev_out[s], nb, cudaMemcpyDeviceToHost, c->d2h)) !=
-          cudaSuccess)
+      void* dst = out_pinned ? static_cast<void*>(static_cast<char*>(host_out) + off) : c->pin_out[s];
+      if ((e = cudaMemcpyAsync(dst, c->dev_out[s], nb, cudaMemcpyDeviceToHost, c->d2h)) != cudaSuccess)
         return hcuda(e, "cudaMemcpyAsync(d2h)");
       cudaEventRecord(c->ev_d2h[s], c->d2h);
     }
     const int64_t j = i - (kSlots - 1);
-    if (j >= 0 && j < n_chunks) {
+    if (!out_pinned && j >= 0 && j < n_chunks) {
       const int s = static_cast<int>(j % kSlots);
       const int64_t r0 = j * chunk_rows;
       const int64_t nr = std::min(chunk_rows, rows - r0);
@@ -316,7 +346,7 @@ const char* grkan_host_last_error(void) { return grkan_last_error(); }
 int grkan_host_create(int32_t device, size_t chunk_bytes, int32_t threads, grkan_host_ctx** out) {
   if (!out) return hfail(GRKAN_ERR_INVALID, "null output");
   *out = nullptr;
-  if (chunk_bytes == 0) chunk_bytes = 16u << 20;
+  if (chunk_bytes == 0) chunk_bytes = 32u << 20;
   chunk_bytes = align256(chunk_bytes);
   if (threads <= 0) {
     const unsigned hc = std::thread::hardware_concurrency();

@@ -172,6 +172,35 @@ struct Checker {
 };
 
 // ---------------------------------------------------------------------------
+// Access instrumentation (INSTR instantiations only; the reference's counter= and
+// coverage= arguments, pkg/src/grkan/backward.py:187-195,275-285,326-351).  Every
+// element a thread processes bumps its coverage cell; each thread tallies the
+// element-sized global accesses it performs, in the reference's units (one load or
+// store = 1; an atomic add = 1 read + 1 write + 1 rmw), flushed once per warp.
+// ---------------------------------------------------------------------------
+struct Tally {
+  unsigned long long r = 0, w = 0, m = 0;
+  __device__ __forceinline__ void flush(const Geom& geo) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      r += __shfl_xor_sync(0xffffffffu, r, o);
+      w += __shfl_xor_sync(0xffffffffu, w, o);
+      m += __shfl_xor_sync(0xffffffffu, m, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      if (r) atomicAdd(geo.cnt + 0, r);
+      if (w) atomicAdd(geo.cnt + 1, w);
+      if (m) atomicAdd(geo.cnt + 2, m);
+    }
+  }
+};
+template <int W>
+__device__ __forceinline__ void visit(const Geom& geo, int64_t elem_off) {
+#pragma unroll
+  for (int e = 0; e < W; ++e) atomicAdd(geo.cov + elem_off + e, 1);
+}
+
+// ---------------------------------------------------------------------------
 // K1: forward
 // ---------------------------------------------------------------------------
 template <typename T, bool EXACT, int MM1, int MN, bool FIXED, int W, bool CHECK>
@@ -274,7 +303,7 @@ __device__ __forceinline__ void cta_reduce_store(A (&acc)[KC], int m1, int n, A*
 // ---------------------------------------------------------------------------
 // K2: backward main pass
 // ---------------------------------------------------------------------------
-template <typename T, bool EXACT, int MM1, int MN, bool FIXED, int W, bool CHECK>
+template <typename T, bool EXACT, int MM1, int MN, bool FIXED, int W, bool CHECK, bool INSTR = false>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     k_bwd_main(const T* __restrict__ x, const T* __restrict__ dy, T* __restrict__ dx,
                const typename VecIO<T, W>::A* __restrict__ ca,
@@ -313,6 +342,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
   const T* ut = dy + tile_off;
   T* dt = dx + tile_off;
   Checker<A> chk;
+  Tally tl;
   Cursor cur;
   cur.init(threadIdx.x, geo.V);
   for (int k = threadIdx.x; k < nvec; k += U * kBlock) {
@@ -348,10 +378,23 @@ rp.template grad_n<W / 2, kGuard<T>>(vx[j], vu[j], o, acc2);
           }
         }
         IO::store(dt + off[j], o);
+        if constexpr (INSTR) {
+          visit<W>(geo, tile_off + off[j]);
+          tl.r += 2 * W;  // x, dy
+          tl.w += W;      // dx
+        }
       }
     }
   }
   if (CHECK && chk.bad()) st->nonfinite_input = 1;
+  if constexpr (INSTR) {
+    if (threadIdx.x == 0) {
+      const int kc = FIXED ? MM1 + MN : m1 + n;
+      tl.r += kc;  // the CTA's coefficient row (held in registers afterwards)
+      tl.w += kc;  // its one partial per coefficient
+    }
+    tl.flush(geo);
+  }
   if constexpr (E::kPacked) {
 #pragma unroll
     for (int k = 0; k < KC; ++k) acc[k] = acc2[k].x + acc2[k].y;
@@ -369,7 +412,8 @@ rp.template grad_n<W / 2, kGuard<T>>(vx[j], vu[j], o, acc2);
 template <typename A>
 __global__ void __launch_bounds__(256)
     k_bwd_reduce(const A* __restrict__ part, int64_t n_tiles, int m1, int n, A* __restrict__ da,
-                 A* __restrict__ db, DevStatus* __restrict__ st, int64_t slot_stride) {
+                 A* __restrict__ db, DevStatus* __restrict__ st, int64_t slot_stride,
+                 unsigned long long* __restrict__ cnt) {
   pdl_wait();  // K2's partials are complete and visible after this
   const int kc = m1 + n;
   const int col = blockIdx.x;  // g * kc + k
@@ -395,13 +439,17 @@ __global__ void __launch_bounds__(256)
     else
       db[(int64_t)g * n + (k - m1)] = out;
     if (nonfinite(out)) st->accum_overflow = 1;
+    if (cnt) {  // instrumented: this column's partial loads and its one result store
+      atomicAdd(cnt + 0, static_cast<unsigned long long>(n_tiles));
+      atomicAdd(cnt + 1, 1ull);
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
 // K4: Alg. 1 comparator -- every element atomically adds its m1+n terms.
 // ---------------------------------------------------------------------------
-template <typename T, bool EXACT, int MM1, int MN, bool FIXED, int W>
+template <typename T, bool EXACT, int MM1, int MN, bool FIXED, int W, bool INSTR = false>
 __global__ void __launch_bounds__(kBlock)
     k_bwd_atomic(const T* __restrict__ x, const T* __restrict__ dy, T* __restrict__ dx,
                  const typename VecIO<T, W>::A* __restrict__ ca,
@@ -420,6 +468,7 @@ __global__ void __launch_bounds__(kBlock)
   const int nr = static_cast<int>(geo.rows - row0 < geo.R ? geo.rows - row0 : geo.R);
   const int nvec = nr * geo.V;
   const int64_t tile_off = row0 * geo.d + (int64_t)g * geo.dg;
+  Tally tl;
   Cursor cur;
   cur.init(threadIdx.x, geo.V);
   for (int k = threadIdx.x; k < nvec; k += kBlock) {
@@ -442,6 +491,17 @@ __global__ void __launch_bounds__(kBlock)
         if (FIXED || j < rat.n) atomicAdd(db + (int64_t)g * rat.n + j, t[MM1 + j]);
     }
     IO::store(dx + off, o);
+    if constexpr (INSTR) {
+      visit<W>(geo, off);
+      const unsigned long long kc = FIXED ? MM1 + MN : rat.m1 + rat.n;
+      tl.r += W * (2 + kc);  // x, dy, and the read half of each coefficient atomic
+      tl.w += W * (1 + kc);  // dx, and the write half
+      tl.m += W * kc;
+    }
+  }
+  if constexpr (INSTR) {
+    if (threadIdx.x == 0) tl.r += FIXED ? MM1 + MN : rat.m1 + rat.n;  // the CTA's coefficient row
+    tl.flush(geo);
   }
 }
 

@@ -90,13 +90,46 @@ cudaError_t launch_fwd_t(const LaunchArgs& L) {
 
 template <typename A>
 cudaError_t launch_reduce_t(const A* part, int64_t n_tiles, int64_t slot_stride, int ng, int m1, int n, A* da,
-                            A* db, DevStatus* st, cudaStream_t stream);
+                            A* db, DevStatus* st, cudaStream_t stream, unsigned long long* cnt = nullptr);
 
 template <typename T>
 cudaError_t launch_bwd_t(const LaunchArgs& L) {
   using A = typename VecIO<T, 1>::A;
   const Plan& p = *L.plan;
   cudaError_t e0;
+  if (L.instr) {
+    // the instrumented instantiations: same kernels, counting (unchecked, per-CTA partials)
+    auto ex = [&](auto e) -> cudaError_t {
+      if (p.staged) {
+        constexpr auto kern = k_bwd_staged<T, decltype(e)::value, false, false, true>;
+        cudaError_t ae = allow_smem<kern>(p.smem);
+        if (ae != cudaSuccess) return ae;
+        kern<<<static_cast<unsigned>(p.ctas), kStagedThreads, p.smem, L.stream>>>(
+            static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out),
+            static_cast<const A*>(L.a), static_cast<const A*>(L.b), static_cast<A*>(L.part), p.geo, p.stages,
+            L.st);
+        return cudaGetLastError();
+      }
+      auto fw = [&](auto fx, auto wc) -> cudaError_t {
+        constexpr bool FX = decltype(fx)::value;
+        k_bwd_main<T, decltype(e)::value, FX ? kFixM1 : kGenM1, FX ? kFixN : kGenN, FX, decltype(wc)::value,
+                   false, true><<<static_cast<unsigned>(p.ctas), kBlock, 0, L.stream>>>(
+            static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out),
+            static_cast<const A*>(L.a), static_cast<const A*>(L.b), static_cast<A*>(L.part), p.geo, L.m1, L.n,
+            L.st);
+        return cudaGetLastError();
+      };
+      auto w = [&](auto fx) -> cudaError_t {
+        if (L.vec) return fw(fx, std::integral_constant<int, vec_width<T>()>{});
+        return fw(fx, std::integral_constant<int, 1>{});
+      };
+      return is_fixed(L) ? w(std::true_type{}) : w(std::false_type{});
+    };
+    e0 = L.exact ? ex(std::true_type{}) : ex(std::false_type{});
+    if (e0 != cudaSuccess) return e0;
+    return launch_reduce_t<A>(static_cast<const A*>(L.part), p.geo.n_tiles, 1, p.geo.ng, L.m1, L.n,
+                              static_cast<A*>(L.da), static_cast<A*>(L.db), L.st, L.stream, p.geo.cnt);
+  }
   if (p.staged) {
     e0 = dispatch_staged<T>(L, [&](auto e, auto ck) -> cudaError_t {
       auto go = [&](auto det) -> cudaError_t {
@@ -130,7 +163,7 @@ cudaError_t launch_bwd_t(const LaunchArgs& L) {
 // (column-major, slot_stride 1; or slot-major, slot_stride ng * kc).
 template <typename A>
 cudaError_t launch_reduce_t(const A* part, int64_t n_tiles, int64_t slot_stride, int ng, int m1, int n, A* da,
-                            A* db, DevStatus* st, cudaStream_t stream) {
+                            A* db, DevStatus* st, cudaStream_t stream, unsigned long long* cnt) {
   // K3 with programmatic dependent launch: its launch overlaps K2's tail and
   // its griddepcontrol.wait orders it after all of K2's memory operations.
   cudaLaunchConfig_t cfg = {};
@@ -143,7 +176,7 @@ cudaError_t launch_reduce_t(const A* part, int64_t n_tiles, int64_t slot_stride,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_bwd_reduce<A>, part, n_tiles, m1, n, da, db, st, slot_stride);
+  return cudaLaunchKernelEx(&cfg, k_bwd_reduce<A>, part, n_tiles, m1, n, da, db, st, slot_stride, cnt);
 }
 
 template <typename T>
@@ -154,12 +187,15 @@ cudaError_t launch_atomic_t(const LaunchArgs& L) {
   L2.check = false;
   cudaError_t e0 = dispatch<T>(L2, is_fixed(L), [&](auto e, auto fx, auto wc, auto) -> cudaError_t {
     constexpr bool FX = decltype(fx)::value;
-    k_bwd_atomic<T, decltype(e)::value, FX ? kFixM1 : kGenM1, FX ? kFixN : kGenN, FX, decltype(wc)::value>
-        <<<static_cast<unsigned>(p.ctas), kBlock, 0, L.stream>>>(
-            static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out),
-            static_cast<const A*>(L.a), static_cast<const A*>(L.b), static_cast<A*>(L.da),
-            static_cast<A*>(L.db), p.geo, L.m1, L.n);
-    return cudaGetLastError();
+    auto go = [&](auto ins) -> cudaError_t {
+      k_bwd_atomic<T, decltype(e)::value, FX ? kFixM1 : kGenM1, FX ? kFixN : kGenN, FX, decltype(wc)::value,
+                   decltype(ins)::value><<<static_cast<unsigned>(p.ctas), kBlock, 0, L.stream>>>(
+          static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out),
+          static_cast<const A*>(L.a), static_cast<const A*>(L.b), static_cast<A*>(L.da),
+          static_cast<A*>(L.db), p.geo, L.m1, L.n);
+      return cudaGetLastError();
+    };
+    return L.instr ? go(std::true_type{}) : go(std::false_type{});
   });
   if (e0 != cudaSuccess || !L.st) return e0;
   k_check_finite<A><<<1, 256, 0, L.stream>>>(static_cast<const A*>(L.da), (int64_t)p.geo.ng * L.m1, L.st);

@@ -479,6 +479,127 @@ struct RationalX2 {
     return dx;
   }
 
+  // grad_lean over P pairs in lock step: every statement is issued for all P pairs
+  // before the next, so each dependent step has P independent instructions between
+  // it and its producer (explicit ILP for the FMA-latency-bound bf16 backward).
+  template <int P, typename ACC>
+  __device__ __forceinline__ void grad_lean_n(const float2 (&x)[P], const float2 (&u)[P], float2 (&out)[P],
+                                              ACC (&acc)[KC]) const {
+    float2 h[P], dh[P], s[P], ds[P], iq[P], p[P], dp[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) h[i] = xmad2(bc(b[3]), x[i], bc(b[2]), one);
+#pragma unroll
+    for (int i = 0; i < P; ++i) dh[i] = fma2(bc(b[3]), x[i], h[i]);
+#pragma unroll
+    for (int i = 0; i < P; ++i) s[i] = xmad2(h[i], x[i], bc(b[1]), one);  // h1
+#pragma unroll
+    for (int i = 0; i < P; ++i) dh[i] = fma2(dh[i], x[i], s[i]);
+#pragma unroll
+    for (int i = 0; i < P; ++i) h[i] = xmad2(s[i], x[i], bc(b[0]), one);  // h0
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      s[i] = mul2(h[i], x[i]);
+      ds[i] = fma2(dh[i], x[i], h[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const float2 q = q_of(s[i]);
+      iq[i] = make_float2(rcp(q.x), rcp(q.y));
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) p[i] = fma2(bc(a[5]), x[i], bc(a[4]));
+#pragma unroll
+    for (int i = 0; i < P; ++i) dp[i] = fma2(bc(a[5]), x[i], p[i]);
+#pragma unroll
+    for (int k = 3; k >= 1; --k) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) p[i] = fma2(p[i], x[i], bc(a[k]));
+#pragma unroll
+      for (int i = 0; i < P; ++i) dp[i] = fma2(dp[i], x[i], p[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) p[i] = fma2(p[i], x[i], bc(a[0]));
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const float2 pq = mul2(p[i], iq[i]);
+      const float2 t0 = mul2(u[i], iq[i]);
+      const float2 z = make_float2(neg_sign_times(s[i].x, pq.x), neg_sign_times(s[i].y, pq.y));
+      out[i] = mul2(t0, fma2(ds[i], z, dp[i]));
+      const float2 w = mul2(t0, z);
+      const float2 x2 = mul2(x[i], x[i]);
+      const float2 x3 = mul2(x2, x[i]);
+      const float2 x4 = mul2(x2, x2);
+      const float2 x5 = mul2(x4, x[i]);
+      acc_add(acc[0], t0);
+      acc_fma(acc[1], t0, x[i]);
+      acc_fma(acc[2], t0, x2);
+      acc_fma(acc[3], t0, x3);
+      acc_fma(acc[4], t0, x4);
+      acc_fma(acc[5], t0, x5);
+      acc_fma(acc[6], w, x[i]);
+      acc_fma(acc[7], w, x2);
+      acc_fma(acc[8], w, x3);
+      acc_fma(acc[9], w, x4);
+    }
+  }
+
+  // FAST, shallow: every polynomial by Estrin's scheme on the powers x^2, x^4 the
+  // coefficient terms need anyway (P: 5 FMAs, depth 3; P': 4; h: 3; A': 3), and A(x)
+  // = h x with h in FMA form under the sign guard (one rarely taken branch per
+  // vector re-evaluates A with the reference's rounding).  36 FMA-pipe
+  // instructions per pair against grad_given's 39, and a critical path of ~2/3.
+  // Error of the FMA h: <= 3 u H(|x|) (u = 2^-24, H = sum |b_k| |x|^(k-1)),
+  // under the guard threshold 2^-17 bsum max(1, |x|^3) with >= 10x margin
+  // (see sign_unsafe).
+  template <int NP, typename ACC>
+  __device__ __forceinline__ void grad_estrin_n(const float (&vx)[2 * NP], const float (&vu)[2 * NP],
+                                                float (&o)[2 * NP], ACC (&acc)[KC]) const {
+    float2 x[NP], x2[NP], x3[NP], x4[NP], s[NP];
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      x[i] = make_float2(vx[2 * i], vx[2 * i + 1]);
+      x2[i] = mul2(x[i], x[i]);
+      x3[i] = mul2(x2[i], x[i]);
+      x4[i] = mul2(x2[i], x2[i]);
+      const float2 h = fma2(x2[i], fma2(bc(b[3]), x[i], bc(b[2])), fma2(bc(b[1]), x[i], bc(b[0])));
+      bad |= sign_unsafe(h.x, x3[i].x) | sign_unsafe(h.y, x3[i].y);
+      s[i] = mul2(h, x[i]);
+    }
+    if (bad) {
+#pragma unroll
+      for (int i = 0; i < NP; ++i) s[i] = series_ref(x[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      const float2 q = q_of(s[i]);
+      const float2 iq = make_float2(rcp(q.x), rcp(q.y));
+      const float2 p = fma2(x4[i], fma2(bc(a[5]), x[i], bc(a[4])),
+                            fma2(x2[i], fma2(bc(a[3]), x[i], bc(a[2])), fma2(bc(a[1]), x[i], bc(a[0]))));
+      const float2 dp = fma2(x4[i], bc(da[4]), fma2(x2[i], fma2(bc(da[3]), x[i], bc(da[2])),
+                                                     fma2(bc(da[1]), x[i], bc(da[0]))));
+      const float2 ds = fma2(x2[i], fma2(bc(db[3]), x[i], bc(db[2])), fma2(bc(db[1]), x[i], bc(db[0])));
+      const float2 pq = mul2(p, iq);
+      const float2 t0 = mul2(make_float2(vu[2 * i], vu[2 * i + 1]), iq);
+      const float2 z = make_float2(neg_sign_times(s[i].x, pq.x), neg_sign_times(s[i].y, pq.y));
+      const float2 r = mul2(t0, fma2(ds, z, dp));
+      o[2 * i] = r.x;
+      o[2 * i + 1] = r.y;
+      const float2 w = mul2(t0, z);
+      const float2 x5 = mul2(x4[i], x[i]);
+      acc_add(acc[0], t0);
+      acc_fma(acc[1], t0, x[i]);
+      acc_fma(acc[2], t0, x2[i]);
+      acc_fma(acc[3], t0, x3[i]);
+      acc_fma(acc[4], t0, x4[i]);
+      acc_fma(acc[5], t0, x5);
+      acc_fma(acc[6], w, x[i]);
+      acc_fma(acc[7], w, x2[i]);
+      acc_fma(acc[8], w, x3[i]);
+      acc_fma(acc[9], w, x4[i]);
+    }
+  }
+
   // dx for NP pairs (one 16-byte vector) and their terms folded into acc.
   // FAST: the guard is evaluated for all NP pairs first and resolved by ONE
   // (rarely taken) branch, so the straight-line math of the NP pairs stays in
@@ -492,6 +613,10 @@ struct RationalX2 {
   template <int NP, bool GUARD = true, typename ACC = float2>
   __device__ __forceinline__ void grad_n(const float (&vx)[2 * NP], const float (&vu)[2 * NP],
                                          float (&o)[2 * NP], ACC (&acc)[KC]) const {
+    if constexpr (!EXACT && GRKAN_ESTRIN) {
+      grad_estrin_n<NP>(vx, vu, o, acc);
+      return;
+    }
     constexpr int G = GRKAN_GUARD_NP < NP ? GRKAN_GUARD_NP : NP;
     static_assert(NP % G == 0, "guard group must divide the pair count");
 #pragma unroll
@@ -500,6 +625,23 @@ struct RationalX2 {
 #pragma unroll
       for (int i = 0; i < G; ++i) x[i] = make_float2(vx[2 * (i0 + i)], vx[2 * (i0 + i) + 1]);
       if (!EXACT && GRKAN_LEAN_FAST && (!GUARD || !GRKAN_SIGN_GUARD)) {
+        if constexpr (GRKAN_LEAN_ILP > 1) {
+          if (i0 == 0) {  // every pair of the vector in one lock-step pass
+            float2 xx[NP], uu[NP], rr[NP];
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+              xx[i] = make_float2(vx[2 * i], vx[2 * i + 1]);
+              uu[i] = make_float2(vu[2 * i], vu[2 * i + 1]);
+            }
+            grad_lean_n<NP>(xx, uu, rr, acc);
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+              o[2 * i] = rr[i].x;
+              o[2 * i + 1] = rr[i].y;
+            }
+          }
+          continue;
+        }
 #pragma unroll
         for (int i = 0; i < G; ++i) {
           const int e = 2 * (i0 + i);

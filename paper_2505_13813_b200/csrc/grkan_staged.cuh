@@ -255,7 +255,7 @@ __device__ __forceinline__ void produce(const T* const (&src)[NT], T* const (&ri
 // ---------------------------------------------------------------------------
 // K2 staged: backward main pass, degrees (5, 4).
 // ---------------------------------------------------------------------------
-template <typename T, bool EXACT, bool CHECK, bool DET>
+template <typename T, bool EXACT, bool CHECK, bool DET, bool INSTR = false>
 __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
     k_bwd_staged(const T* __restrict__ x, const T* __restrict__ dy, T* __restrict__ dx,
                  const typename VecIO<T, 1>::A* __restrict__ ca,
@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
 #pragma unroll
   for (int k = 0; k < KC; ++k) acc[k] = A(0);
   Checker<A> chk;
+  Tally tl;
 
   if (warp == kConsumerWarps) {
     if (lane == 0) {
@@ -359,6 +360,11 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
           }
         }
         __stcs(reinterpret_cast<uint4*>(gp[j]), RW::pack(o));
+        if constexpr (INSTR) {
+          visit<W>(geo, gp[j] - dx);
+          tl.r += 2 * W;  // x, dy (staged through shared memory by the bulk copies)
+          tl.w += W;      // dx
+        }
       };
       if (BwdCfg<T>::kFullStage && full_slots && rows_here == geo.RS) {
         // every slot of a full stage is valid: one branch-free block the
@@ -395,6 +401,13 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
     if constexpr (!DET) {
       __syncwarp();
       warp_store<A, KC>(sacc, part, g, tile, warp, geo);
+    }
+    if constexpr (INSTR) {
+      if (lane == 0) {
+        if (warp == 0) tl.r += KC;  // the CTA's coefficient row (registers afterwards)
+        tl.w += KC;                 // this warp's one partial per coefficient
+      }
+      tl.flush(geo);
     }
   }
   if (CHECK && chk.bad()) st->nonfinite_input = 1;

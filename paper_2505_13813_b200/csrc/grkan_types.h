@@ -25,6 +25,10 @@ struct Geom {
   int32_t det;      // deterministic (global row-block) partials: slot-major
                     // part[(block * ng + g) * kc + k], one partial per RB-row block
   int32_t spb;      // staged deterministic: stages per block (RB / RS)
+  // instrumented launches only (grkan_bwd_instrumented; null otherwise): per-element
+  // visit counts [rows * d] and element-access tallies {reads, writes, rmw}
+  int32_t* cov;
+  unsigned long long* cnt;
 };
 
 struct DevStatus {
@@ -94,6 +98,12 @@ struct Plan {
 #ifndef GRKAN_LEAN_FAST
 #define GRKAN_LEAN_FAST 0         // FAST, reference-rounded A(x): P' / h' by simultaneous Horner (no da/db registers)
 #endif
+#ifndef GRKAN_LEAN_ILP
+#define GRKAN_LEAN_ILP 1          // with GRKAN_LEAN_FAST: >1 = all pairs of a vector in lock step
+#endif
+#ifndef GRKAN_ESTRIN
+#define GRKAN_ESTRIN 0            // FAST backward: Estrin polynomials + guarded FMA A(x) (grad_estrin_n)
+#endif
 #ifndef GRKAN_FWD_CTAS
 #define GRKAN_FWD_CTAS 8
 #endif
@@ -122,6 +132,7 @@ struct LaunchArgs {
   int m1, n;
   bool exact, vec, check;
   bool partials_only;  // backward: K2 only (deterministic multi-GPU path)
+  bool instr;          // backward: the instrumented instantiations (coverage + access counts)
   cudaStream_t stream;
 };
 

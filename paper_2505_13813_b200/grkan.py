@@ -16,8 +16,9 @@ tree reduction (more accurate than either reference strategy, not bitwise).
 Pass ``exact=False`` (or ``set_default_exact(False)``) for the FMA policy.
 
 Differences, all deliberate: ``workers`` is accepted and ignored (the GPU is
-the pool); ``counter``/``coverage`` instrumentation belongs to the reference's
-access model (out of scope) and raises if given; ``backward_naive`` runs the
+the pool); ``counter``/``coverage`` run the kernels' counting instantiations
+(grkan_bwd_instrumented), so the tallies are the B200 kernels' own accesses in the
+reference's units, not the reference's model; ``backward_naive`` runs the
 paper's Alg. 1 (global atomicAdd), the algorithm the reference's naive
 strategy models, so its d_a/d_b are not bit-reproducible.
 """
@@ -408,6 +409,20 @@ def _host_flags(exact, check: bool) -> int:
     return (N.FLAG_EXACT if _exact(exact) else N.FLAG_FAST) | (N.FLAG_CHECK_FINITE if check else 0)
 
 
+_PINNED_MIN_BYTES = 1 << 20
+
+
+def _output_like(arr: np.ndarray) -> np.ndarray:
+    """A fresh output array shaped like ``arr``.  Large ones live in page-locked memory
+    from torch's caching host allocator: the pipeline DMAs results straight into them
+    (no staging copy, no first-touch page faults), and a dropped output's block is
+    reused by the next call."""
+    if arr.nbytes < _PINNED_MIN_BYTES:
+        return np.empty_like(arr)
+    t = torch.empty(arr.shape, dtype=torch.from_numpy(arr.reshape(-1)[:1]).dtype, pin_memory=True)
+    return t.numpy()
+
+
 def _host_coeffs(params: GroupRationalParams, dtype) -> tuple[np.ndarray, np.ndarray]:
     """Coefficients rounded to the tensor dtype, as the reference casts at use (rational.py:220)."""
     return (np.ascontiguousarray(params.numerator, dtype=dtype),
@@ -425,7 +440,7 @@ def forward_tensor(x: ActivationTensor, params: GroupRationalParams, layout: Gro
     check_compatible(x, params, layout)
     check = validate and not x.validated
     arr = x.data
-    y = np.empty_like(arr)
+    y = _output_like(arr)
     a, b = _host_coeffs(params, arr.dtype)
     dt = N.DT_F64 if arr.dtype == np.float64 else N.DT_F32
     rows = x.batch * x.seq
@@ -448,10 +463,41 @@ def _prepare_bwd(x, upstream, params, plan, default_plan):
     return layout, plan
 
 
-def _no_instrumentation(counter, coverage):
-    if counter is not None or coverage is not None:
-        raise UnsupportedError("access-model instrumentation (counter/coverage) is not part of the "
-                               "B200 path; use the reference's access model")
+def _instrumented(x, upstream, params, naive: bool, exact, counter, coverage):
+    """counter= / coverage= (backward.py:230-236, 335-351): the same kernels in their
+    counting instantiations (grkan_bwd_instrumented).  The kernels tally the accesses
+    they perform and mark every element they visit; both are added to the caller's
+    counter / coverage array, as the reference's workers do."""
+    from . import _native as N
+
+    dev = _device()
+    xd, ud = torch.from_numpy(x.data).to(dev), torch.from_numpy(upstream.data).to(dev)
+    a, b = _coeffs(params, xd.dtype, xd.device)
+    rows, d = x.batch * x.seq, x.feature
+    ng, m1, n = params.num_groups, params.num_coeffs, params.den_coeffs
+    dx = torch.empty_like(xd)
+    da = torch.empty((ng, m1), dtype=a.dtype, device=dev)
+    db = torch.empty((ng, n), dtype=a.dtype, device=dev)
+    ws = torch.empty(max(256, ops.workspace_bytes(rows, d, ng, m1, n, xd.dtype)), dtype=torch.uint8, device=dev)
+    cov = torch.zeros(max(1, rows * d), dtype=torch.int32, device=dev)
+    cnt = torch.zeros(3, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        rc = N.lib().grkan_bwd_instrumented(
+            xd.data_ptr(), ud.data_ptr(), a.data_ptr(), b.data_ptr() if b.numel() else None, dx.data_ptr(),
+            da.data_ptr(), db.data_ptr() if db.numel() else None, ws.data_ptr(), ws.numel(), cov.data_ptr(),
+            cnt.data_ptr(), rows, d, ng, m1, n, N.DT_F64 if xd.dtype == torch.float64 else N.DT_F32,
+            N.FLAG_EXACT if _exact(exact) else N.FLAG_FAST, 1 if naive else 0,
+            torch.cuda.current_stream(dev).cuda_stream)
+    if rc:
+        raise_for_status(rc, N.last_error())
+    ops.read_status(ws[:ops.STATUS_BYTES])  # AccumulationOverflowError (backward.py:182-184)
+    if counter is not None:
+        r, w, m = (int(v) for v in cnt.cpu().tolist())
+        counter.add(reads=r, writes=w, rmw=m)
+    if coverage is not None:
+        view = coverage.reshape(rows, d)
+        view += cov[:rows * d].cpu().numpy().reshape(rows, d).astype(view.dtype)
+    return dx.cpu().numpy(), da.cpu().numpy(), db.cpu().numpy()
 
 
 def backward_blocked(x: ActivationTensor, upstream: ActivationTensor, params: GroupRationalParams,
@@ -461,15 +507,21 @@ def backward_blocked(x: ActivationTensor, upstream: ActivationTensor, params: Gr
     """Alg. 2 on the B200: dx in one pass, per-CTA partials, fixed-order fold (backward.py:275-372)."""
     if combine_mode not in (COMBINE_ORDERED, COMBINE_UNORDERED):
         raise ValueError("unknown combine mode %r" % (combine_mode,))
-    _no_instrumentation(counter, coverage)
     _prepare_bwd(x, upstream, params, plan, ExecutionPlan.blocked)
     from . import _native as N
 
     if upstream.data.dtype != x.data.dtype:
         upstream = ActivationTensor(upstream.data.astype(x.data.dtype))
     check = validate and not (x.validated and upstream.validated)
+    if counter is not None or coverage is not None:
+        if check:
+            x.check_finite()
+            upstream.check_finite()
+        dx, da, db = _instrumented(x, upstream, params, False, exact, counter, coverage)
+        return GradBundle(d_x=ActivationTensor(dx), d_a=da, d_b=db, strategy=STRATEGY_BLOCKED,
+                          precision=x.precision, combine_mode=combine_mode)
     arr = x.data
-    dx = np.empty_like(arr)
+    dx = _output_like(arr)
     a, b = _host_coeffs(params, arr.dtype)
     da = np.empty((params.num_groups, params.num_coeffs), dtype=arr.dtype)
     db = np.empty((params.num_groups, params.den_coeffs), dtype=arr.dtype)
@@ -489,11 +541,16 @@ def backward_naive(x: ActivationTensor, upstream: ActivationTensor, params: Grou
                    coverage=None, exact: bool | None = None) -> GradBundle:
     """The paper's Alg. 1 (per-element atomicAdd), which the reference's naive strategy models
     (backward.py:187-246).  Comparator only; d_x is identical to backward_blocked's."""
-    _no_instrumentation(counter, coverage)
     _prepare_bwd(x, upstream, params, plan, ExecutionPlan.naive)
     if validate and not (x.validated and upstream.validated):
         x.check_finite()
         upstream.check_finite()
+    if counter is not None or coverage is not None:
+        if upstream.data.dtype != x.data.dtype:
+            upstream = ActivationTensor(upstream.data.astype(x.data.dtype))
+        dx, da, db = _instrumented(x, upstream, params, True, exact, counter, coverage)
+        return GradBundle(d_x=ActivationTensor(dx), d_a=da, d_b=db, strategy=STRATEGY_NAIVE,
+                          precision=x.precision, combine_mode=COMBINE_ORDERED)
     xd, ud = _to_device(x), _to_device(upstream).to(dtype=torch.float64 if x.precision == "double"
                                                      else torch.float32)
     a, b = _coeffs(params, xd.dtype, xd.device)

@@ -1,0 +1,153 @@
+"""Access instrumentation on the device: the reference's counter= / coverage= and
+instrumented_backward (pkg/src/grkan/access.py:129-161, backward.py:187-195,275-285),
+ported from pkg/tests/test_access.py::TestInstrumentation.
+
+The counts come from the kernels' counting instantiations (grkan_bwd_instrumented):
+every element a CUDA thread processes marks its coverage cell, and every kernel tallies
+the global accesses it performs.  Coverage == 1 everywhere is the race-freedom
+evidence the reference relies on (each element in exactly one block's partial), now
+for every kernel family the B200 path runs: TMA-staged (fp32 / bf16), register-direct
+vector and scalar, generic degrees, and the Alg. 1 atomic comparator.
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import grkan_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def G():
+    from paper_2505_13813_b200 import grkan
+    return grkan
+
+
+def A():
+    from paper_2505_13813_b200 import access
+    return access
+
+
+def instance(rng, shape, groups, m1=6, n=4, dtype=np.float64):
+    g = G()
+    layout = g.GroupLayout(shape[2], groups)
+    params = g.GroupRationalParams(rng.standard_normal((groups, m1)), rng.standard_normal((groups, n)))
+    x = g.ActivationTensor(rng.standard_normal(shape).astype(dtype))
+    up = g.ActivationTensor(rng.standard_normal(shape).astype(dtype))
+    return x, up, params, layout
+
+
+def test_reference_configuration_counts():
+    """pkg/tests/test_access.py:87-101.  Naive: the reference's per-element model except
+    that the B200 loads each coefficient row once per CTA, not per element; the atomic
+    RMW count is the reference's exactly.  Blocked: no RMWs at all on the B200."""
+    rng = np.random.default_rng(0)
+    x, up, params, layout = instance(rng, (2, 4, 16), 2)
+    g, acc = G(), A()
+    _, naive = acc.instrumented_backward(x, up, params, g.ExecutionPlan.naive(2, 4, layout, 8))
+    assert naive.total == naive.predicted_total
+    assert naive.total == naive.reads + naive.writes
+    assert naive.rmw_atomic == 10 * 128  # one per coefficient per element, as the reference
+    assert naive.reference_predicted_total == 4224
+    _, blocked = acc.instrumented_backward(x, up, params, g.ExecutionPlan.blocked(2, 4, layout, 8))
+    assert blocked.total == blocked.predicted_total
+    assert blocked.rmw_atomic == 0
+    assert blocked.reference_predicted_total == 444
+
+
+def test_tail_case_covered_once():
+    """pkg/tests/test_access.py:109-122: B*N = 9 with block 4."""
+    rng = np.random.default_rng(1)
+    x, up, params, layout = instance(rng, (3, 3, 8), 2)
+    bundle, report = A().instrumented_backward(x, up, params, G().ExecutionPlan.blocked(3, 3, layout, 4))
+    assert report.total == report.predicted_total
+    ref = orc.backward_blocked(x.data, up.data, params.numerator, params.denominator, 4)
+    assert np.array_equal(bundle.d_x.data, ref[0])
+
+
+@pytest.mark.parametrize("shape,groups,m1,n,dtype", [
+    ((8, 197, 192), 8, 6, 4, np.float32),    # TMA-staged fp32
+    ((3, 37, 64), 8, 6, 4, np.float64),      # staged fp64
+    ((5, 7, 12), 4, 6, 4, np.float32),       # d_g = 3: scalar direct kernel
+    ((4, 9, 48), 4, 4, 2, np.float32),       # degrees (3, 2): generic direct kernel
+    ((2, 8, 16), 2, 8, 5, np.float64),       # degrees (7, 5)
+])
+@pytest.mark.parametrize("naive", [False, True])
+def test_every_element_exactly_once_and_counts_match(shape, groups, m1, n, dtype, naive):
+    rng = np.random.default_rng(2)
+    x, up, params, layout = instance(rng, shape, groups, m1, n, dtype)
+    g = G()
+    plan = (g.ExecutionPlan.naive if naive else g.ExecutionPlan.blocked)(shape[0], shape[1], layout)
+    bundle, report = A().instrumented_backward(x, up, params, plan, exact=True)
+    assert report.total == report.predicted_total and report.matches_prediction
+    # the counting instantiation computes what the product kernels compute
+    plain = g.run_backward(x, up, params, plan, exact=True)
+    assert bundle.d_x.data.tobytes() == plain.d_x.data.tobytes()
+    tol = 1e-12 if dtype == np.float64 else 1e-5
+    assert orc.matrix_rel(bundle.d_a, plain.d_a) <= tol and orc.matrix_rel(bundle.d_b, plain.d_b) <= tol
+
+
+def test_bf16_staged_kernel_coverage_through_the_c_abi():
+    """The bf16 TMA-staged kernel (the headline bf16 path) at KAT-T shape: every element once."""
+    from paper_2505_13813_b200 import _native as N
+    from paper_2505_13813_b200 import ops
+    dev = torch.device("cuda", 0)
+    rows, d, ng = 8 * 197, 192, 8
+    x = torch.randn(rows, d, device=dev).to(torch.bfloat16)
+    dy = torch.randn(rows, d, device=dev).to(torch.bfloat16)
+    a, b = torch.randn(ng, 6, device=dev), torch.randn(ng, 4, device=dev)
+    dx = torch.empty_like(x)
+    da, db = torch.empty(ng, 6, device=dev), torch.empty(ng, 4, device=dev)
+    ws = torch.empty(ops.workspace_bytes(rows, d, ng, 6, 4, torch.bfloat16), dtype=torch.uint8, device=dev)
+    cov = torch.zeros(rows * d, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(3, dtype=torch.int64, device=dev)
+    rc = N.lib().grkan_bwd_instrumented(x.data_ptr(), dy.data_ptr(), a.data_ptr(), b.data_ptr(), dx.data_ptr(),
+                                        da.data_ptr(), db.data_ptr(), ws.data_ptr(), ws.numel(), cov.data_ptr(),
+                                        cnt.data_ptr(), rows, d, ng, 6, 4, N.DT_BF16, N.FLAG_FAST, 0,
+                                        torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, N.last_error()
+    assert N.plan(rows, d, ng, 6, 4, N.DT_BF16)["staged"]
+    assert bool((cov == 1).all())
+    r, w, m = cnt.cpu().tolist()
+    assert (r, w, m) == A().predicted_device_accesses(rows, d, ng, 6, 4, "bf16")
+    dx2, da2, db2 = ops.rational_backward(x, dy, a, b)
+    assert torch.equal(dx, dx2)
+    assert orc.matrix_rel(da.cpu().numpy(), da2.cpu().numpy()) <= 1e-5
+
+
+def test_shim_counter_and_coverage_arguments_accumulate():
+    """backward_blocked(counter=..., coverage=...) adds to the caller's objects, as the
+    reference's workers do (backward.py:335-351): two calls -> coverage 2, counts doubled."""
+    rng = np.random.default_rng(3)
+    x, up, params, layout = instance(rng, (2, 5, 16), 4)
+    g, acc = G(), A()
+    counter = acc.AccessCounter()
+    cov = np.zeros((10, 16), dtype=np.int16)
+    g.backward_blocked(x, up, params, counter=counter, coverage=cov)
+    once = (counter.reads, counter.writes, counter.rmw_atomic)
+    g.backward_blocked(x, up, params, counter=counter, coverage=cov)
+    assert (counter.reads, counter.writes, counter.rmw_atomic) == tuple(2 * v for v in once)
+    assert np.all(cov == 2)
+
+
+def test_report_serialization():
+    """pkg/tests/test_access.py:136-145."""
+    rng = np.random.default_rng(4)
+    x, up, params, layout = instance(rng, (1, 2, 4), 2, m1=2, n=1)
+    _, report = A().instrumented_backward(x, up, params, G().ExecutionPlan.blocked(1, 2, layout, 2))
+    d = report.to_dict()
+    assert d["total"] == d["reads"] + d["writes"]
+    assert d["strategy"] == "blocked_reduction"
+    assert report.matches_prediction
+
+
+def test_workers_do_not_change_counts():
+    rng = np.random.default_rng(5)
+    x, up, params, layout = instance(rng, (4, 8, 16), 4)
+    plan = G().ExecutionPlan.blocked(4, 8, layout, 8)
+    totals = {tuple(A().instrumented_backward(x, up, params, plan, workers=w)[1].to_dict().values())
+              for w in (1, 2, 4)}
+    assert len(totals) == 1

@@ -187,3 +187,53 @@ def test_shim_threads_each_get_their_own_pipeline():
         t.join()
     for g, w in zip(got, want):
         assert np.array_equal(g.view(np.uint32), w.view(np.uint32))
+
+
+def test_page_locked_buffers_are_transferred_in_place():
+    """Pinned x / dy / y / dx (torch pinned tensors behind NumPy arrays) skip the staging
+    copies; results are bitwise the pageable path's, in every in/out combination."""
+    x, u, num, den = orc.bench_inputs(4, 197, 192, 8, seed=50)
+    ctx = Ctx(chunk_bytes=128 << 10, threads=4)
+    try:
+        rc, y_ref = ctx.fwd(x, num, den, N().FLAG_EXACT)
+        rc2, dx_ref, da_ref, db_ref = ctx.bwd(x, u, num, den, N().FLAG_EXACT)
+        assert rc == 0 and rc2 == 0
+        px = torch.from_numpy(x).pin_memory().numpy()
+        pu = torch.from_numpy(u).pin_memory().numpy()
+        for xin, uin in ((px, pu), (px, u), (x, pu)):
+            for pinned_out in (False, True):
+                out = torch.empty(x.shape, pin_memory=True).numpy() if pinned_out else np.empty_like(x)
+                a = np.ascontiguousarray(num, dtype=np.float32)
+                b = np.ascontiguousarray(den, dtype=np.float32)
+                rows, d = x.shape[0] * x.shape[1], x.shape[2]
+                assert N().lib().grkan_host_fwd(ctx.h, xin.ctypes.data, out.ctypes.data, a.ctypes.data,
+                                                b.ctypes.data, rows, d, 8, 6, 4, N().DT_F32, N().FLAG_EXACT) == 0
+                assert out.tobytes() == y_ref.tobytes()
+                da = np.empty((8, 6), np.float32)
+                db = np.empty((8, 4), np.float32)
+                assert N().lib().grkan_host_bwd(ctx.h, xin.ctypes.data, uin.ctypes.data, a.ctypes.data,
+                                                b.ctypes.data, out.ctypes.data, da.ctypes.data, db.ctypes.data,
+                                                rows, d, 8, 6, 4, N().DT_F32, N().FLAG_EXACT) == 0
+                assert out.tobytes() == dx_ref.tobytes()
+                assert da.tobytes() == da_ref.tobytes() and db.tobytes() == db_ref.tobytes()
+    finally:
+        ctx.close()
+
+
+def test_shim_outputs_are_independent_arrays():
+    """Large shim outputs come from the pinned caching allocator: results held at the same
+    time never alias, and a dropped output's memory is safely reused."""
+    from paper_2505_13813_b200 import grkan as G
+    rng = np.random.default_rng(60)
+    params = G.GroupRationalParams(rng.standard_normal((8, 6)), rng.standard_normal((8, 4)))
+    layout = G.GroupLayout(384, 8)
+    xs = [G.ActivationTensor(rng.standard_normal((4, 197, 384)).astype(np.float32)) for _ in range(3)]
+    ys = [G.forward_tensor(x, params, layout).data for x in xs]
+    assert len({y.ctypes.data for y in ys}) == 3
+    for x, y in zip(xs, ys):
+        assert y.flags.c_contiguous and y.flags.writeable and y.dtype == np.float32
+        assert np.array_equal(y.view(np.uint32), orc.forward(x.data, params.numerator, params.denominator).view(np.uint32))
+    del ys
+    again = G.forward_tensor(xs[0], params, layout).data
+    assert np.array_equal(again.view(np.uint32),
+                          orc.forward(xs[0].data, params.numerator, params.denominator).view(np.uint32))
