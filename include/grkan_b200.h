@@ -153,17 +153,6 @@ GRKAN_API int grkan_linear_bwd(const void* dy, const void* w, const void* x, con
                                void* dx, void* da, void* db, void* ws, size_t ws_bytes, int64_t M, int32_t N,
                                int32_t K, int32_t n_groups, uint32_t flags, void* stream);
 
-/* Fused GR-KAN layer forward (the GEMM-prologue half):
- * Y = R(X) W^T (+ bias) with A = R(X) computed in shared memory between the
- * TMA load and the tcgen05 MMA (the reference's layer_forward,
- * pkg/src/grkan/layer.py:318-379, applies the rational then the matmul).
- * X [M, K], W [N, K] (torch Linear weight [out, in]), Y [M, N]: bf16,
- * row-major, 16-byte aligned; bias [N] fp32 or NULL; a [n_groups, 6],
- * b [n_groups, 4] fp32, groups along K.  Needs N % 64 == 0, K % 64 == 0,
- * group width % 8 == 0.  R(X) is recomputed once per 64..256-column N tile. */
-GRKAN_API int grkan_linear_fwd(const void* x, const void* w, const void* bias, const void* a, const void* b,
-                               void* y, int64_t M, int32_t N, int32_t K, int32_t n_groups, uint32_t flags,
-                               void* stream);
 
 /* K3 fused with the cross-GPU da||db sum over peer memory:
  * grkan_bwd_p2p runs K2, then ONE kernel that folds this rank's partials,

@@ -41,7 +41,7 @@ EXPORTS = (
     "grkan_version", "grkan_status_string", "grkan_last_error", "grkan_fwd",
     "grkan_bwd_workspace_bytes", "grkan_bwd", "grkan_bwd_atomic", "grkan_read_status",
     "grkan_plan", "grkan_det_block_rows", "grkan_det_partials_bytes", "grkan_bwd_partials",
-    "grkan_reduce_partials", "grkan_linear_bwd_workspace_bytes", "grkan_linear_bwd", "grkan_linear_fwd",
+    "grkan_reduce_partials", "grkan_linear_bwd_workspace_bytes", "grkan_linear_bwd",
     "grkan_p2p_buffer_bytes", "grkan_p2p_alloc", "grkan_p2p_free", "grkan_ipc_get_handle",
     "grkan_ipc_open_handle", "grkan_ipc_close_handle", "grkan_bwd_p2p", "grkan_bwd_terms",
     "grkan_host_create", "grkan_host_destroy", "grkan_host_threads", "grkan_host_last_error",
@@ -97,8 +97,6 @@ def _declare(L):
     L.grkan_linear_bwd_workspace_bytes.restype = sz
     L.grkan_linear_bwd.argtypes = [p, p, p, p, p, p, p, p, p, sz, i64, i32, i32, i32, u32, p]
     L.grkan_linear_bwd.restype = ctypes.c_int
-    L.grkan_linear_fwd.argtypes = [p, p, p, p, p, p, i64, i32, i32, i32, u32, p]
-    L.grkan_linear_fwd.restype = ctypes.c_int
     L.grkan_p2p_buffer_bytes.argtypes = [i32, i32, i32, i32]
     L.grkan_p2p_buffer_bytes.restype = sz
     L.grkan_p2p_alloc.argtypes = [sz, ctypes.POINTER(ctypes.c_void_p)]

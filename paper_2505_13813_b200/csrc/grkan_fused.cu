@@ -539,209 +539,6 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
   }
 }
 
-// ---------------------------------------------------------------------------
-// Forward prologue fusion: Y = R(X) W^T (+ bias) with A = R(X) produced in
-// shared memory.  The producer TMA-loads the X block [128 x 64] (K-major,
-// 128B swizzle) and the W block [BN x 64] (torch weight [N, K] is already
-// K-major) per stage; NT transform warps apply the rational in place -- each
-// thread rewrites whole 16-byte chunks of the swizzled tile, so the layout the
-// MMA reads is the TMA's -- then fence.proxy.async (generic-proxy smem writes
-// -> tensor-core reads) and arrive on aready; the MMA lane waits aready
-// instead of the TMA barrier.  Four epilogue warps drain the double-buffered
-// TMEM accumulator (+ bias) to bf16 Y.  R(X) is recomputed once per N tile
-// (N / BN times per element): it pays when N / BN is small (KAT's fc2, N=768).
-// ---------------------------------------------------------------------------
-struct FwdGeom {
-  int64_t M;
-  int32_t N, K, ng, dg;
-  int32_t n_tiles_n;
-  float one;
-};
-
-template <int BN, int NT, int kStages>
-__global__ void __launch_bounds__(64 + 32 * NT + 128, 1)
-    k_linear_fwd_fused(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
-                       __nv_bfloat16* __restrict__ y, const float* __restrict__ bias,
-                       const float* __restrict__ ca, const float* __restrict__ cb, FwdGeom geo) {
-  constexpr int A_BYTES = kBM * kBK * 2;
-  constexpr int B_BYTES = BN * kBK * 2;
-  constexpr int STAGE = A_BYTES + B_BYTES;
-  constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
-  constexpr int CHUNKS = kBM * kBK / 8;            // 16-byte chunks per A tile (1024)
-  constexpr int TT = 32 * NT;                       // transform threads
-  constexpr int EPI0 = 2 + NT;                      // first epilogue warp
-  // K-major, both operands: D f32, A/B bf16, M = 128, N = BN
-  constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
-                             (static_cast<uint32_t>(kBM >> 4) << 24);
-
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[kStages], aready[kStages], empty[kStages], tfull[2], tempty[2];
-  __shared__ uint32_t tmem_base;
-  __shared__ float scoef[kMaxGroups * kKC];
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t n_tiles = ((geo.M + kBM - 1) / kBM) * geo.n_tiles_n;
-  const int kblocks = geo.K / kBK;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&aready[s], NT);
-      mbar_init(&empty[s], 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
-                 "n"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  for (int t = threadIdx.x; t < geo.ng * kKC; t += blockDim.x) {
-    const int g = t / kKC, k = t - g * kKC;
-    scoef[t] = k < 6 ? ca[g * 6 + k] : cb[g * 4 + (k - 6)];
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem_d = tmem_base;
-
-  if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer
-      int slot = 0;
-      uint32_t phase = 0;
-      int64_t it = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int n0 = static_cast<int>(tile % geo.n_tiles_n) * BN;
-        const int m0 = static_cast<int>((tile / geo.n_tiles_n) * kBM);
-        for (int kb = 0; kb < kblocks; ++kb, ++it) {
-          if (it >= kStages) mbar_wait(&empty[slot], phase ^ 1);
-          unsigned char* sa = smem + slot * STAGE;
-          mbar_arrive_expect_tx(&full[slot], STAGE);
-          tma_load_2d(sa, &map_x, kb * kBK, m0, &full[slot]);
-          tma_load_2d(sa + A_BYTES, &map_w, kb * kBK, n0, &full[slot]);
-          if (++slot == kStages) {
-            slot = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer
-      int slot = 0;
-      uint32_t phase = 0;
-      int i = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++i) {
-        const int acc = i & 1;
-        mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t dcol = tmem_d + static_cast<uint32_t>(acc * BN);
-        for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&aready[slot], phase);  // A = R(X) written by the transform warps
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t sa = smem_u32(smem + slot * STAGE);
-          const uint32_t sb = sa + A_BYTES;
-#pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            umma_bf16(dcol, smem_desc(sa + k * 32, 16, 1024, 2), smem_desc(sb + k * 32, 16, 1024, 2), IDESC,
-                      (kb | k) != 0);
-          umma_commit(&empty[slot]);
-          if (++slot == kStages) {
-            slot = 0;
-            phase ^= 1;
-          }
-        }
-        umma_commit(&tfull[acc]);
-      }
-    }
-  } else if (warp < EPI0) {
-    // ---- transform warps: A tile <- R(A tile), in place, 16-byte chunks
-    const int tt = threadIdx.x - 64;
-    int slot = 0;
-    uint32_t phase = 0;
-    RationalX2<false> rp;
-    int g_loaded = -1;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      for (int kb = 0; kb < kblocks; ++kb) {
-        mbar_wait(&full[slot], phase);
-        unsigned char* sa = smem + slot * STAGE;
-#pragma unroll 2
-        for (int c = tt; c < CHUNKS; c += TT) {
-          const int r = c >> 3, j = c & 7;  // logical 16-byte chunk j of row r
-          const int g = (kb * kBK + j * 8) / geo.dg;
-          if (g != g_loaded) {
-            rp.load_row(scoef + g * kKC, geo.one);
-            g_loaded = g;
-          }
-          uint4* pch = reinterpret_cast<uint4*>(sa + r * 128 + ((j ^ (r & 7)) << 4));
-          float v[8], o[8];
-          Raw16<__nv_bfloat16>::unpack(*pch, v);
-#pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            const float2 r2 = rp.value(make_float2(v[e], v[e + 1]));
-            o[e] = r2.x;
-            o[e + 1] = r2.y;
-          }
-          *pch = Raw16<__nv_bfloat16>::pack(o);
-        }
-        // generic-proxy smem writes -> visible to the tensor core (async proxy)
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&aready[slot]);
-        if (++slot == kStages) {
-          slot = 0;
-          phase ^= 1;
-        }
-      }
-    }
-  } else {
-    // ---- epilogue warps: TMEM lane quadrant warp % 4, all BN columns
-    const int q = warp & 3;
-    const int row = q * 32 + lane;
-    int i = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++i) {
-      const int acc = i & 1;
-      const int n0 = static_cast<int>(tile % geo.n_tiles_n) * BN;
-      const int64_t grow = (tile / geo.n_tiles_n) * kBM + row;
-      const bool live = grow < geo.M;
-      mbar_wait(&tfull[acc], (i >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t taddr = tmem_d + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
-      __nv_bfloat16* yrow = y + grow * geo.N + n0;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        float v[32];
-        tmem_ld32(taddr + c, v);
-        if (c + 32 == BN) {
-          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-        }
-        if (live) {
-#pragma unroll
-          for (int vq = 0; vq < 4; ++vq) {
-            float o[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) o[e] = v[vq * 8 + e] + (bias ? __ldg(bias + n0 + c + vq * 8 + e) : 0.0f);
-            __stcs(reinterpret_cast<uint4*>(yrow + c) + vq, Raw16<__nv_bfloat16>::pack(o));
-          }
-        }
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "n"(TMEM_COLS) : "memory");
-}
-
 // ---- host -------------------------------------------------------------------
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -871,26 +668,6 @@ bool pair_enabled() {
   return v && v[0] == '1';
 }
 
-#ifndef GRKAN_FUSED_FWD_NT
-#define GRKAN_FUSED_FWD_NT 16
-#endif
-constexpr int kFwdNT = GRKAN_FUSED_FWD_NT;  // transform warps (fused forward)
-
-template <int BN>
-cudaError_t launch_fwd_t(const CUtensorMap& mx, const CUtensorMap& mw, void* y, const float* bias, const float* a,
-                         const float* b, const FwdGeom& geo, int64_t tiles, cudaStream_t s) {
-  constexpr int kStageBytes = kBM * kBK * 2 + kBK * BN * 2;
-  constexpr int kSt = kSmemBudget / kStageBytes > 8 ? 8 : kSmemBudget / kStageBytes;
-  constexpr size_t smem = static_cast<size_t>(kSt) * kStageBytes + 1024;
-  auto kern = k_linear_fwd_fused<BN, kFwdNT, kSt>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  const int64_t grid = tiles < sms_of_device() ? tiles : sms_of_device();
-  kern<<<static_cast<unsigned>(grid), 64 + 32 * kFwdNT + 128, smem, s>>>(
-      mx, mw, static_cast<__nv_bfloat16*>(y), bias, a, b, geo);
-  return cudaGetLastError();
-}
-
 }  // namespace fused
 }  // namespace grkan
 
@@ -996,61 +773,6 @@ int grkan_linear_bwd(const void* dy, const void* w, const void* x, const void* a
 #undef GRKAN_FUSED_CASE
   if (e != cudaSuccess) return grkan::set_error(GRKAN_ERR_CUDA, cudaGetErrorString(e));
   e = grkan::launch_reduce_f32(part, geo.ppg, 1, n_groups, 6, 4, da, db, st, s);
-  if (e != cudaSuccess) return grkan::set_error(GRKAN_ERR_CUDA, cudaGetErrorString(e));
-  return GRKAN_OK;
-}
-
-int grkan_linear_fwd(const void* x, const void* w, const void* bias, const void* a, const void* b, void* y,
-                     int64_t M, int32_t N, int32_t K, int32_t n_groups, uint32_t flags, void* stream) {
-  using namespace grkan::fused;
-  char msg[256];
-  if (K < 1 || n_groups < 1 || K % n_groups) {
-    snprintf(msg, sizeof msg, "layout mismatch: feature_dim %d not divisible by num_groups %d", K, n_groups);
-    return grkan::set_error(GRKAN_ERR_LAYOUT, msg);
-  }
-  if (M < 0 || N < 1) return grkan::set_error(GRKAN_ERR_GRID, "grid geometry invalid: M >= 0 and N >= 1 required");
-  if (flags & ~GRKAN_FLAG_FAST) return grkan::set_error(GRKAN_ERR_UNSUPPORTED, "fused linear forward: FAST policy only");
-  const int dg = K / n_groups;
-  int bn = 0;
-  for (int c : {256, 192, 128, 64})
-    if (N % c == 0) {
-      bn = c;
-      break;
-    }
-  if (!bn || K % kBK || dg % 8 || n_groups > kMaxGroups) {
-    snprintf(msg, sizeof msg,
-             "fused linear forward needs N %% 64 == 0, K %% 64 == 0, group width %% 8 == 0, groups <= %d "
-             "(N=%d, K=%d, dg=%d, groups=%d)", kMaxGroups, N, K, dg, n_groups);
-    return grkan::set_error(GRKAN_ERR_UNSUPPORTED, msg);
-  }
-  if (!x || !w || !a || !b || !y) return grkan::set_error(GRKAN_ERR_INVALID, "null pointer");
-  for (const void* p : {x, w, (const void*)y})
-    if (reinterpret_cast<uintptr_t>(p) & 15) return grkan::set_error(GRKAN_ERR_INVALID, "tensors must be 16-byte aligned");
-  if (M == 0) return GRKAN_OK;
-  CUtensorMap mx, mw;
-  if (!make_map(&mx, x, static_cast<uint64_t>(K), static_cast<uint64_t>(M), kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_map(&mw, w, static_cast<uint64_t>(K), static_cast<uint64_t>(N), kBK, bn, CU_TENSOR_MAP_SWIZZLE_128B))
-    return grkan::set_error(GRKAN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  FwdGeom geo;
-  geo.M = M;
-  geo.N = N;
-  geo.K = K;
-  geo.ng = n_groups;
-  geo.dg = dg;
-  geo.n_tiles_n = N / bn;
-  geo.one = 1.0f;
-  const int64_t tiles = ((M + kBM - 1) / kBM) * geo.n_tiles_n;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const float* fa = static_cast<const float*>(a);
-  const float* fb = static_cast<const float*>(b);
-  const float* fbias = static_cast<const float*>(bias);
-  cudaError_t e;
-  switch (bn) {
-    case 256: e = launch_fwd_t<256>(mx, mw, y, fbias, fa, fb, geo, tiles, s); break;
-    case 192: e = launch_fwd_t<192>(mx, mw, y, fbias, fa, fb, geo, tiles, s); break;
-    case 128: e = launch_fwd_t<128>(mx, mw, y, fbias, fa, fb, geo, tiles, s); break;
-    default: e = launch_fwd_t<64>(mx, mw, y, fbias, fa, fb, geo, tiles, s); break;
-  }
   if (e != cudaSuccess) return grkan::set_error(GRKAN_ERR_CUDA, cudaGetErrorString(e));
   return GRKAN_OK;
 }

@@ -116,7 +116,9 @@ constexpr int kFwdThreadsHost = 32 * (GRKAN_FWD_CONSUMER_WARPS + 1);
 constexpr int kFwdStageVecsHost = GRKAN_FWD_STAGE_VECS;
 static_assert(GRKAN_STAGE_VECS % (32 * GRKAN_CONSUMER_WARPS) == 0, "stage must split evenly over consumers");
 static_assert(GRKAN_FWD_STAGE_VECS % (32 * GRKAN_FWD_CONSUMER_WARPS) == 0, "stage must split evenly over consumers");
-constexpr int kFlushStages = 4;          // per-lane fp32 register chains <= 4 stages x 6 terms
+// per-lane fp32 register chains <= 12 vectors per flush (4 stages at 3 vectors per thread)
+constexpr int kFlushStages = (12 * 32 * GRKAN_CONSUMER_WARPS / GRKAN_STAGE_VECS) > 0
+                                 ? (12 * 32 * GRKAN_CONSUMER_WARPS / GRKAN_STAGE_VECS) : 1;
 
 struct LaunchArgs {
   const Plan* plan;

@@ -14,8 +14,6 @@ Public functions
   reduce_partials(part, ...)           -> da, db (grkan_reduce_partials)
   linear_backward_fused(dy, w, x, a, b)-> dx, da, db (grkan_linear_bwd: tcgen05 dY.W + rational
                                         backward epilogue, dF never in HBM)
-  linear_forward_fused(x, w, a, b, bias)-> y = R(x) w^T + bias (grkan_linear_fwd: rational in the
-                                        tcgen05 GEMM prologue, R(x) never in HBM)
 and the torch.library ops ``grkan_b200::rational_fwd`` / ``rational_bwd``
 (graph-capturable, torch.compile-traceable through their fake kernels).
 """
@@ -319,31 +317,3 @@ def linear_backward_fused(dy: torch.Tensor, w: torch.Tensor, x: torch.Tensor, a:
     return dx, da, db
 
 
-def linear_forward_fused(x: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tensor,
-                         bias: torch.Tensor | None = None) -> torch.Tensor:
-    """y = R(x) w^T + bias in one kernel (GEMM-prologue fusion).
-
-    x [..., K], w [N, K] (torch Linear weight [out, in]): bf16 CUDA tensors;
-    a [ng, 6], b [ng, 4] fp32 (groups along K); bias [N] (any float dtype,
-    applied in fp32) or None.  Returns y [..., N] bf16.  R(x) never exists in
-    HBM -- what rational_forward followed by F.linear computes, in one pass.
-    """
-    if x.dtype != torch.bfloat16 or w.dtype != torch.bfloat16:
-        raise UnsupportedError("fused linear forward takes bf16 x and w")
-    if not (x.is_cuda and w.is_cuda):
-        raise UnsupportedError("fused linear forward needs CUDA tensors; there is no CPU path")
-    k = x.shape[-1]
-    if w.dim() != 2 or w.shape[1] != k:
-        raise LayoutMismatchError("layout mismatch: w must be [N, K=%d], got %s" % (k, tuple(w.shape)))
-    if a.dtype != torch.float32 or b.dtype != torch.float32 or a.shape[1] != 6 or b.shape[1] != 4:
-        raise UnsupportedError("fused linear forward: fp32 coefficients of degrees (5, 4)")
-    n_out = w.shape[0]
-    rows = x.numel() // k if k else 0
-    x, w, a, b = x.contiguous(), w.contiguous(), a.contiguous(), b.contiguous()
-    bias32 = None if bias is None else bias.to(torch.float32).contiguous()
-    y = torch.empty(tuple(x.shape[:-1]) + (n_out,), dtype=torch.bfloat16, device=x.device)
-    with torch.cuda.device(x.device):
-        rc = N.lib().grkan_linear_fwd(x.data_ptr(), w.data_ptr(), _ptr(bias32), a.data_ptr(), b.data_ptr(),
-                                      y.data_ptr(), rows, n_out, k, a.shape[0], N.FLAG_FAST, _stream(x.device))
-        _raise(rc)
-    return y

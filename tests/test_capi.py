@@ -147,18 +147,3 @@ def test_deterministic_and_fused_entry_points_validate_on_the_host():
     assert rc == N.ERR_INVALID  # null pointers
 
 
-def test_fused_forward_validates_on_the_host():
-    L = N.lib()
-    # x [M, K], w [N, K]: groups along K
-    rc = L.grkan_linear_fwd(None, None, None, None, None, None, 128, 256, 250, 8, 0, None)
-    assert rc == N.ERR_LAYOUT  # K not divisible by groups
-    rc = L.grkan_linear_fwd(None, None, None, None, None, None, 128, 100, 256, 2, 0, None)
-    assert rc == N.ERR_UNSUPPORTED and "N % 64" in N.last_error()
-    rc = L.grkan_linear_fwd(None, None, None, None, None, None, 128, 128, 96, 2, 0, None)
-    assert rc == N.ERR_UNSUPPORTED  # K % 64
-    rc = L.grkan_linear_fwd(None, None, None, None, None, None, 128, 128, 256, 64, 0, None)
-    assert rc == N.ERR_UNSUPPORTED  # group width 4 (not a multiple of 8)
-    rc = L.grkan_linear_fwd(None, None, None, None, None, None, 128, 128, 256, 2, N.FLAG_EXACT, None)
-    assert rc == N.ERR_UNSUPPORTED
-    rc = L.grkan_linear_fwd(None, None, None, None, None, None, 128, 128, 256, 2, 0, None)
-    assert rc == N.ERR_INVALID

@@ -116,38 +116,6 @@ def test_kat_training_with_fused_mlp():
     assert losses[-1] < 0.2 * losses[0]
 
 
-FWD_SHAPES = [
-    # M, K (features of X, grouped), N (out features), groups
-    (256, 256, 128, 2),
-    (200, 768, 256, 8),       # M tail; dg 96 -> 64-column K blocks straddle groups
-    (1024, 3072, 768, 8),     # KAT-B rational2 -> fc2
-    (512, 768, 3072, 8),      # KAT-B rational1 -> fc1
-]
-
-
-@pytest.mark.parametrize("M,K,N,ng", FWD_SHAPES)
-@pytest.mark.parametrize("with_bias", [False, True])
-def test_fused_forward_matches_unfused_chain(M, K, N, ng, with_bias):
-    from paper_2505_13813_b200 import ops
-    torch.backends.cuda.matmul.allow_tf32 = False
-    g = torch.Generator(device="cpu").manual_seed(M + K + N)
-    x = torch.randn(M, K, generator=g).to(torch.bfloat16).to(DEV)
-    w = (torch.randn(N, K, generator=g) / K ** 0.5).to(torch.bfloat16).to(DEV)
-    a = torch.randn(ng, 6, generator=g).to(DEV)
-    b = torch.randn(ng, 4, generator=g).to(DEV)
-    bias = torch.randn(N, generator=g).to(DEV) if with_bias else None
-    y = ops.linear_forward_fused(x, w, a, b, bias)
-    f = ops.rational_forward(x, a, b)  # bf16 R(x): the A operand the fused kernel builds in smem
-    y_ref = f.float() @ w.float().t() + (bias if with_bias else 0.0)
-    assert y.dtype == torch.bfloat16 and y.shape == (M, N)
-    assert orc.matrix_rel(y.float().cpu().numpy(), y_ref.cpu().numpy()) <= 1e-2
-    if M * K <= 300_000:  # fp64 chain (fp64 rational of the bf16 inputs, then the fp64 matmul)
-        xs = x.double().cpu().numpy()[None]
-        f64 = orc.forward(xs, a.double().cpu().numpy(), b.double().cpu().numpy())[0]
-        y64 = f64 @ w.double().cpu().numpy().T + (bias.double().cpu().numpy() if with_bias else 0.0)
-        assert orc.matrix_rel(y.double().cpu().numpy(), y64) <= 2e-2
-
-
 @pytest.mark.parametrize("M", [512, 300, 130])
 def test_cta_pair_path_matches(monkeypatch, M):
     """GRKAN_FUSED_PAIR=1: the long-K shape on CTA pairs (cluster of 2, tcgen05.mma.cta_group::2,

@@ -186,5 +186,3 @@ def test_fused_and_parallel_paths_have_no_cpu_fallback():
     with pytest.raises(errors.UnsupportedError):
         ops.linear_backward_fused(torch.randn(4, 64).to(torch.bfloat16), torch.randn(64, 256).to(torch.bfloat16),
                                   x, torch.randn(2, 6), torch.randn(2, 4))
-    with pytest.raises(errors.UnsupportedError):
-        ops.linear_forward_fused(x, torch.randn(64, 256).to(torch.bfloat16), torch.randn(2, 6), torch.randn(2, 4))

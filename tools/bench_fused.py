@@ -1,11 +1,11 @@
-"""Fused vs unfused GR-KAN layer forward and backward through the linear map.
+"""Fused vs unfused GR-KAN layer backward through the linear map.
 
     python tools/bench_fused.py [--reps 50]  -> one JSON line per KAT-B layer shape
 
 backward  fused   : ops.linear_backward_fused  (one tcgen05 kernel + the K3 fold)
           unfused : dF = dy @ w (cuBLAS bf16, bf16 output) then ops.rational_backward(x, dF)
-forward   fused   : ops.linear_forward_fused   (rational in the tcgen05 GEMM prologue)
-          unfused : ops.rational_forward(x) then F.linear (cuBLAS)
+(The prologue-fused forward, K6, measured 0.42-0.71x of the unfused chain in round 1
+and was removed; the forward is ops.rational_forward then cuBLAS.)
 Both on the same synthetic bf16 tensors; CUDA events on the current stream,
 inputs far larger than L2.  TFLOP/s counts the GEMM's 2*M*F*K only.
 """
@@ -70,19 +70,6 @@ def main():
         t_gemm = timed(lambda: torch.matmul(dy, w, out=dF), args.reps, label="bwd_gemm")
         t_rat = timed(lambda: ops.rational_backward(x, dF, a, b), args.reps)
         flops = 2.0 * M * F * K
-        # forward of the same layer: y = R(x) w^T, w = torch weight [out = K, in = F]
-        wt = w
-        t_ffused = timed(lambda: ops.linear_forward_fused(x, wt, a, b), args.reps)
-        t_frat = timed(lambda: ops.rational_forward(x, a, b), args.reps)
-        fx = ops.rational_forward(x, a, b)
-        t_fgemm = timed(lambda: torch.nn.functional.linear(fx, wt), args.reps)
-        print(json.dumps({
-            "direction": "forward", "shape": name, "M": M, "F": F, "K": K, "groups": 8,
-            "fused_us": t_ffused, "fused_tflops": flops / t_ffused / 1e6,
-            "fused_frac_of_bf16_peak": flops / t_ffused / 1e6 / tc_peak,
-            "unfused_rational_fwd_us": t_frat, "unfused_gemm_us": t_fgemm, "unfused_us": t_frat + t_fgemm,
-            "speedup": (t_frat + t_fgemm) / t_ffused, "bf16_peak_tflops": tc_peak,
-        }), flush=True)
         print(json.dumps({"direction": "backward",
             "shape": name, "M": M, "F": F, "K": K, "groups": 8,
             "fused_us": t_fused, "fused_tflops": flops / t_fused / 1e6,
