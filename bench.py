@@ -92,6 +92,10 @@ def parse_args(argv=None):
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--block-size", type=int, default=256,
                    help="row block of the CPU reference's blocked strategy (backward.py:48)")
+    p.add_argument("--fused-step", action="store_true",
+                   help="time grkan_fwd_bwd -- forward and backward of the same x in one pass (x read once, "
+                        "y from the backward's own P and 1/Q) -- as the step; the default times grkan_fwd then "
+                        "grkan_bwd and reports the fused step beside it")
     p.add_argument("--strategy", choices=("blocked", "naive", "both"), default="both",
                    help="blocked: K2+K3 timed; naive: the Alg.-1 atomic comparator (K4) timed as the "
                         "backward; both: blocked timed, the comparator reported beside it")
@@ -275,6 +279,8 @@ def config_block(args, shape, world=1):
         "degrees": [args.num_coeffs - 1, args.den_coeffs], "seed": args.seed, "mode": args.mode,
         "io_dtype": args.dtype, "strategy": args.strategy,
         "parallelism": "dp%d" % world, "collective": args.collective,
+        "step": ("fused: grkan_fwd_bwd (forward and backward of the same x in one pass)"
+                 if getattr(args, "fused_step", False) else "two passes: grkan_fwd then grkan_bwd"),
         "l2": ("inputs larger than L2 (no flush): %d MB per tensor vs 126 MB L2"
                % (batch * seq * dim * es // 2**20)) if batch * seq * dim * es > 126 * 2**20 else
               ("inputs smaller than L2: a >=256 MB buffer is written between timed steps (L2 flush)"),
@@ -549,6 +555,23 @@ def run_b200(args, rank, world, local_rank):
                                          ops._ptr(db), N.DT_F64 if args.dtype == "fp64" else N.DT_F32, st.data_ptr(), sp)
             assert rc == 0, N.last_error()
 
+    def fused():
+        join_comm()
+        rc = L.grkan_fwd_bwd(x.data_ptr(), dy.data_ptr(), a.data_ptr(), ops._ptr(b), y.data_ptr(), dx.data_ptr(),
+                             da.data_ptr(), ops._ptr(db), ws.data_ptr(), ws_bytes, rows, dim, groups, m1, nden,
+                             dt_code, flags, sp)
+        assert rc == 0, N.last_error()
+
+    fused_ok = args.strategy != "naive" and args.collective == "allreduce"
+    if args.fused_step:
+        if not fused_ok:
+            raise SystemExit("--fused-step needs the blocked strategy and --collective allreduce")
+
+        def fwd():
+            pass
+
+        bwd = fused
+
     # warm-up: at least W steps and at least 150 ms of device work (clocks and
     # memory settled on a fresh box), untimed
     t_w = time.perf_counter()
@@ -633,6 +656,24 @@ def run_b200(args, rank, world, local_rank):
     step_ms = [e[0].elapsed_time(e[3]) for e in ev]
     ci95_ms = 1.96 * statistics.stdev(step_ms) / math.sqrt(len(step_ms)) if len(step_ms) > 1 else None
     value = world * E / (ms_step / 1e3)
+
+    # ---- the fused forward + backward step beside the two-pass step (same inputs) ---------
+    fused_us = None
+    if fused_ok and not args.fused_step and world == 1:
+        for _ in range(3):
+            fused()
+        torch.cuda.synchronize()
+        fe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        for k in range(K):
+            if flush_buf is not None:  # L2 flush outside the step's events (workload < L2)
+                flush_buf.zero_()
+            fe[k][0].record(stream)
+            fused()
+            fe[k][1].record(stream)
+        torch.cuda.synchronize()
+        fused_us = statistics.fmean(e0.elapsed_time(e1) for e0, e1 in fe) * 1e3
+    elif args.fused_step:
+        fused_us = bwd_ms * 1e3
 
     if args.dump and rank == 0:  # run_bench --dump: the final dx as a GRKB tensor dump
         from paper_2505_13813_b200 import grkb
@@ -753,10 +794,16 @@ def run_b200(args, rank, world, local_rank):
     if rank != 0:
         return
     peak, peak_src = peaks()
-    bwd_bytes = 3 * es * E
+    bwd_bytes = (4 if args.fused_step else 3) * es * E  # fused step: x, dy read once; y, dx written
     fwd_bytes = 2 * es * E
     bwd_gbs = bwd_bytes / (bwd_ms / 1e3) / 1e9
-    fwd_gbs = fwd_bytes / (fwd_ms / 1e3) / 1e9
+    fwd_gbs = fwd_bytes / (fwd_ms / 1e3) / 1e9 if not args.fused_step else 0.0
+    fused_blk = None if fused_us is None else {
+        "us": fused_us, "elements_per_s": world * E / (fused_us / 1e6),
+        "algorithmic_bytes": 4 * es * E, "gbs": 4 * es * E / (fused_us / 1e6) / 1e9,
+        "frac": 4 * es * E / (fused_us / 1e6) / 1e9 / peak,
+        "gbs_fwd_plus_bwd_bytes": 5 * es * E / (fused_us / 1e6) / 1e9,
+        "api": "grkan_fwd_bwd / ops.rational_forward_backward (y, dx, da, db of the same x in one pass)"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_ci95": ci95_ms,
@@ -770,7 +817,8 @@ def run_b200(args, rank, world, local_rank):
         "config": config_block(args, shape, world),
         "hbm_gbs": (5 * es * E) / (ms_step / 1e3) / 1e9,
         "roofline": {
-            "bound": "hbm", "kernel": "grkan_bwd (K2 bwd_main + K3 reduce)",
+            "bound": "hbm", "kernel": ("grkan_fwd_bwd (K2 with the forward fused + K3 reduce)" if args.fused_step
+                                       else "grkan_bwd (K2 bwd_main + K3 reduce)"),
             "achieved": bwd_gbs, "peak": peak, "unit": "GB/s", "frac": bwd_gbs / peak,
             "peak_source": peak_src, "traffic": ncu_traffic(args, "bwd") if world_ok(args) else None,
             "algorithmic_bytes_per_launch": bwd_bytes, "launch_us": bwd_ms * 1e3,
@@ -781,6 +829,7 @@ def run_b200(args, rank, world, local_rank):
             "bwd_us": bwd_ms * 1e3, "bwd_gbs": bwd_gbs, "bwd_frac": bwd_gbs / peak,
             "collective": args.collective, "collective_us": coll_ms * 1e3,
             "collective_check": coll_check,
+            "fused_step": fused_blk,
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * es * E,
                 "d2h_bytes_per_step": 2 * es * E + ces * groups * (m1 + nden),
@@ -791,7 +840,7 @@ def run_b200(args, rank, world, local_rank):
                 "autograd_value": world * E / (e2e_auto_ms / 1e3),
                 "reference_api": shim},
         "clocks": sampler.summary(),
-        "gpu_launches": (2 if args.strategy == "naive" else 3) * K,
+        "gpu_launches": (2 if args.strategy == "naive" or args.fused_step else 3) * K,
         "dist": None if world == 1 else {
             "backend": dist.get_backend(), "world_size": dist.get_world_size(),
             "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if args.dist_backend == "nccl" else None},

@@ -103,6 +103,18 @@ GRKAN_API int grkan_bwd(const void* x, const void* dy, const void* a, const void
               void* db, void* ws, size_t ws_bytes, int64_t rows, int32_t d, int32_t n_groups,
               int32_t m1, int32_t n, int32_t dtype, uint32_t flags, void* stream);
 
+/* Fused forward + backward step: y (forward_tensor) and dx, da, db
+ * (backward_blocked) of the same x and upstream dy in ONE pass -- x is read once
+ * and y comes from the backward's own P(x) and 1/Q(x) (rational.py:218-278 share
+ * them).  Same results as grkan_fwd + grkan_bwd (EXACT: y, dx bitwise; da/db the
+ * per-CTA fold).  For plans without the fused kernel (non-(5,4) degrees,
+ * unaligned tensors, DETERMINISTIC) it runs the two passes back to back.  `ws`
+ * as for grkan_bwd (the forward's CHECK_FINITE status shares it). */
+GRKAN_API int grkan_fwd_bwd(const void* x, const void* dy, const void* a, const void* b, void* y, void* dx,
+                            void* da, void* db, void* ws, size_t ws_bytes, int64_t rows, int32_t d,
+                            int32_t n_groups, int32_t m1, int32_t n, int32_t dtype, uint32_t flags,
+                            void* stream);
+
 /* The paper's Alg. 1 (per-element global atomicAdd into da/db).  Comparator
  * for the speed and rounding claims only; not used by the product path.
  * `status` receives the overflow flag (may be NULL). */

@@ -46,7 +46,7 @@ EXPORTS = (
     "grkan_ipc_open_handle", "grkan_ipc_close_handle", "grkan_bwd_p2p", "grkan_bwd_terms",
     "grkan_host_create", "grkan_host_destroy", "grkan_host_threads", "grkan_host_last_error",
     "grkan_host_fwd", "grkan_host_bwd", "grkan_combine_partials", "grkan_bwd_instrumented",
-    "grkan_launch_ctas",
+    "grkan_launch_ctas", "grkan_fwd_bwd",
 )
 IPC_HANDLE_BYTES = 64
 
@@ -116,6 +116,8 @@ def _declare(L):
     L.grkan_bwd_terms.restype = ctypes.c_int
     L.grkan_bwd_instrumented.argtypes = [p, p, p, p, p, p, p, p, sz, p, p, i64, i32, i32, i32, i32, i32, u32, i32, p]
     L.grkan_bwd_instrumented.restype = ctypes.c_int
+    L.grkan_fwd_bwd.argtypes = [p, p, p, p, p, p, p, p, p, sz, i64, i32, i32, i32, i32, i32, u32, p]
+    L.grkan_fwd_bwd.restype = ctypes.c_int
     L.grkan_launch_ctas.argtypes = [i64, i32, i32, i32, i32, i32, i32]
     L.grkan_launch_ctas.restype = i64
     L.grkan_combine_partials.argtypes = [p, p, i64, i32, i32, i32, p, p, i32, p]

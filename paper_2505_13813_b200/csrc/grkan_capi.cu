@@ -397,6 +397,55 @@ int grkan_bwd(const void* x, const void* dy, const void* a, const void* b, void*
   return GRKAN_OK;
 }
 
+int grkan_fwd_bwd(const void* x, const void* dy, const void* a, const void* b, void* y, void* dx, void* da,
+                  void* db, void* ws, size_t ws_bytes, int64_t rows, int32_t d, int32_t n_groups, int32_t m1,
+                  int32_t n, int32_t dtype, uint32_t flags, void* stream) {
+  int rc = check_layout(rows, d, n_groups, m1, n, dtype, flags);
+  if (rc) return rc;
+  const size_t es = elem_size(dtype);
+  const bool det = (flags & GRKAN_FLAG_DETERMINISTIC) != 0;
+  const bool vec = vec_ok(d, n_groups, es, {x, dy, dx, y});
+  const Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count(), det);
+  if (rows == 0 || !p.staged || det) {
+    // no fused instantiation for this plan: the two passes back to back (same results)
+    // (grkan_bwd's CHECK_FINITE covers x, so the forward runs unchecked)
+    rc = grkan_fwd(x, y, a, b, rows, d, n_groups, m1, n, dtype,
+                   flags & ~(GRKAN_FLAG_DETERMINISTIC | GRKAN_FLAG_CHECK_FINITE), nullptr, stream);
+    if (rc) return rc;
+    return grkan_bwd(x, dy, a, b, dx, da, db, ws, ws_bytes, rows, d, n_groups, m1, n, dtype, flags, stream);
+  }
+  if (!ws || !da || (n > 0 && !db)) return fail(GRKAN_ERR_INVALID, "null workspace / gradient pointer");
+  if (!aligned16(ws)) return fail(GRKAN_ERR_INVALID, "workspace must be 16-byte aligned");
+  if (!x || !dy || !dx || !y || !a || (n > 0 && !b)) return fail(GRKAN_ERR_INVALID, "null tensor pointer");
+  if (!plan_fits(p)) return fail(GRKAN_ERR_GRID, "grid geometry invalid: %lld CTAs", (long long)p.ctas);
+  const size_t need = ws_bytes_for(p, m1, n, dtype);
+  if (ws_bytes < need) return fail(GRKAN_ERR_INVALID, "workspace too small: %zu < %zu bytes", ws_bytes, need);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(DevStatus), s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(status)");
+  LaunchArgs L{};
+  L.plan = &p;
+  L.x = x;
+  L.dy = dy;
+  L.out = dx;
+  L.y2 = y;
+  L.a = a;
+  L.b = b;
+  L.part = static_cast<char*>(ws) + 256;
+  L.da = da;
+  L.db = db;
+  L.st = reinterpret_cast<DevStatus*>(ws);
+  L.m1 = m1;
+  L.n = n;
+  L.exact = (flags & GRKAN_FLAG_EXACT) != 0;
+  L.vec = vec;
+  L.check = (flags & GRKAN_FLAG_CHECK_FINITE) != 0;
+  L.stream = s;
+  e = launch("bwd", dtype, L);
+  if (e != cudaSuccess) return cuda_fail(e, "k_bwd (fused step) launch");
+  return GRKAN_OK;
+}
+
 int grkan_bwd_p2p(const void* x, const void* dy, const void* a, const void* b, void* dx, void* da, void* db,
                   void* ws, size_t ws_bytes, int64_t rows, int32_t d, int32_t n_groups, int32_t m1, int32_t n,
                   int32_t dtype, uint32_t flags, void* const* peer_bufs, int32_t rank, int32_t world,

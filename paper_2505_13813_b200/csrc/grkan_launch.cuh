@@ -105,7 +105,7 @@ cudaError_t launch_bwd_t(const LaunchArgs& L) {
         cudaError_t ae = allow_smem<kern>(p.smem);
         if (ae != cudaSuccess) return ae;
         kern<<<static_cast<unsigned>(p.ctas), kStagedThreads, p.smem, L.stream>>>(
-            static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out),
+            static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out), nullptr,
             static_cast<const A*>(L.a), static_cast<const A*>(L.b), static_cast<A*>(L.part), p.geo, p.stages,
             L.st);
         return cudaGetLastError();
@@ -132,17 +132,19 @@ cudaError_t launch_bwd_t(const LaunchArgs& L) {
   }
   if (p.staged) {
     e0 = dispatch_staged<T>(L, [&](auto e, auto ck) -> cudaError_t {
-      auto go = [&](auto det) -> cudaError_t {
-        constexpr auto kern = k_bwd_staged<T, decltype(e)::value, decltype(ck)::value, decltype(det)::value>;
+      auto go = [&](auto det, auto fwd) -> cudaError_t {
+        constexpr auto kern = k_bwd_staged<T, decltype(e)::value, decltype(ck)::value, decltype(det)::value, false,
+                                           decltype(fwd)::value>;
         cudaError_t ae = allow_smem<kern>(p.smem);
         if (ae != cudaSuccess) return ae;
         kern<<<static_cast<unsigned>(p.ctas), kStagedThreads, p.smem, L.stream>>>(
-            static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out),
+            static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out), static_cast<T*>(L.y2),
             static_cast<const A*>(L.a), static_cast<const A*>(L.b), static_cast<A*>(L.part), p.geo,
             p.stages, L.st);
         return cudaGetLastError();
       };
-      return p.geo.det ? go(std::true_type{}) : go(std::false_type{});
+      if (L.y2) return go(std::false_type{}, std::true_type{});  // fused step: per-CTA partials only
+      return p.geo.det ? go(std::true_type{}, std::false_type{}) : go(std::false_type{}, std::false_type{});
     });
   } else e0 = dispatch<T>(L, is_fixed(L), [&](auto e, auto fx, auto wc, auto ck) -> cudaError_t {
     constexpr bool FX = decltype(fx)::value;

@@ -377,15 +377,19 @@ struct RationalX2 {
   static __device__ __forceinline__ void acc_fma(float2& a, float2 t, float2 p) { a = fma2(t, p, a); }
   static __device__ __forceinline__ void acc_fma(float& a, float2 t, float2 p) { a = fmaf(t.y, p.y, fmaf(t.x, p.x, a)); }
 
-  template <typename ACC>
+  // WY: also return the forward value y = P / Q of the pair in *yv (the fused
+  // forward + backward step): P/Q rounded once by IEEE division in EXACT mode
+  // (rational.py:224, bitwise), P * (1/Q) = pq in FAST mode (K1's FAST form).
+  template <bool WY = false, typename ACC>
   __device__ __forceinline__ float2 grad_given(float2 x, float2 u, float2 s, float2 x2, float2 x3,
-                                               ACC (&acc)[KC]) const {
+                                               ACC (&acc)[KC], float2* yv = nullptr) const {
     const float2 p = horner2<EXACT, 6>(a, x);
     const float2 q = q_of(s);
     const float2 iq = make_float2(rcp(q.x), rcp(q.y));
     const float2 dp = horner2<EXACT, 5>(da, x);
     const float2 ds = horner2<EXACT, 4>(db, x);
     const float2 pq = mul2(p, iq);
+    if constexpr (WY) *yv = EXACT ? make_float2(__fdiv_rn(p.x, q.x), __fdiv_rn(p.y, q.y)) : pq;
     float2 dx;
     if (EXACT) {
       // dx = u * (dp*iq - ((sg*ds)*pq)*iq); terms t_i = t_{i-1} * x from u*iq;
@@ -431,175 +435,6 @@ struct RationalX2 {
     return dx;
   }
 
-  // FAST with the reference-rounded A(x), register-lean: P' and h' come out of
-  // simultaneous Horner recurrences on a and b themselves (dp = dp x + p beside
-  // p = p x + a_k; dh likewise beside the separately rounded h chain), so the
-  // derivative coefficient rows da / db need no registers.  Same FMA-pipe
-  // instruction count as grad_given's FAST branch (P 5, P' 4, A' = h + x h' 3).
-  template <typename ACC>
-  __device__ __forceinline__ float2 grad_lean(float2 x, float2 u, ACC (&acc)[KC]) const {
-    // h = ((b4 x + b3) x + b2) x + b1 with the reference's rounding; dh = h'(x)
-    const float2 h2 = xmad2(bc(b[3]), x, bc(b[2]), one);
-    const float2 h1 = xmad2(h2, x, bc(b[1]), one);
-    float2 dh = fma2(bc(b[3]), x, h2);
-    const float2 h0 = xmad2(h1, x, bc(b[0]), one);
-    dh = fma2(dh, x, h1);
-    const float2 s = mul2(h0, x);              // A(x), the reference's bits
-    const float2 ds = fma2(dh, x, h0);         // A'(x) = h + x h'
-    const float2 q = q_of(s);
-    const float2 iq = make_float2(rcp(q.x), rcp(q.y));
-    float2 p = fma2(bc(a[5]), x, bc(a[4]));
-    float2 dp = fma2(bc(a[5]), x, p);
-    p = fma2(p, x, bc(a[3]));
-    dp = fma2(dp, x, p);
-    p = fma2(p, x, bc(a[2]));
-    dp = fma2(dp, x, p);
-    p = fma2(p, x, bc(a[1]));
-    dp = fma2(dp, x, p);
-    p = fma2(p, x, bc(a[0]));
-    const float2 pq = mul2(p, iq);
-    const float2 t0 = mul2(u, iq);
-    const float2 z = make_float2(neg_sign_times(s.x, pq.x), neg_sign_times(s.y, pq.y));
-    const float2 dx = mul2(t0, fma2(ds, z, dp));
-    const float2 w = mul2(t0, z);
-    const float2 x2 = mul2(x, x);
-    const float2 x3 = mul2(x2, x);
-    const float2 x4 = mul2(x2, x2);
-    const float2 x5 = mul2(x4, x);
-    acc_add(acc[0], t0);
-    acc_fma(acc[1], t0, x);
-    acc_fma(acc[2], t0, x2);
-    acc_fma(acc[3], t0, x3);
-    acc_fma(acc[4], t0, x4);
-    acc_fma(acc[5], t0, x5);
-    acc_fma(acc[6], w, x);
-    acc_fma(acc[7], w, x2);
-    acc_fma(acc[8], w, x3);
-    acc_fma(acc[9], w, x4);
-    return dx;
-  }
-
-  // grad_lean over P pairs in lock step: every statement is issued for all P pairs
-  // before the next, so each dependent step has P independent instructions between
-  // it and its producer (explicit ILP for the FMA-latency-bound bf16 backward).
-  template <int P, typename ACC>
-  __device__ __forceinline__ void grad_lean_n(const float2 (&x)[P], const float2 (&u)[P], float2 (&out)[P],
-                                              ACC (&acc)[KC]) const {
-    float2 h[P], dh[P], s[P], ds[P], iq[P], p[P], dp[P];
-#pragma unroll
-    for (int i = 0; i < P; ++i) h[i] = xmad2(bc(b[3]), x[i], bc(b[2]), one);
-#pragma unroll
-    for (int i = 0; i < P; ++i) dh[i] = fma2(bc(b[3]), x[i], h[i]);
-#pragma unroll
-    for (int i = 0; i < P; ++i) s[i] = xmad2(h[i], x[i], bc(b[1]), one);  // h1
-#pragma unroll
-    for (int i = 0; i < P; ++i) dh[i] = fma2(dh[i], x[i], s[i]);
-#pragma unroll
-    for (int i = 0; i < P; ++i) h[i] = xmad2(s[i], x[i], bc(b[0]), one);  // h0
-#pragma unroll
-    for (int i = 0; i < P; ++i) {
-      s[i] = mul2(h[i], x[i]);
-      ds[i] = fma2(dh[i], x[i], h[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < P; ++i) {
-      const float2 q = q_of(s[i]);
-      iq[i] = make_float2(rcp(q.x), rcp(q.y));
-    }
-#pragma unroll
-    for (int i = 0; i < P; ++i) p[i] = fma2(bc(a[5]), x[i], bc(a[4]));
-#pragma unroll
-    for (int i = 0; i < P; ++i) dp[i] = fma2(bc(a[5]), x[i], p[i]);
-#pragma unroll
-    for (int k = 3; k >= 1; --k) {
-#pragma unroll
-      for (int i = 0; i < P; ++i) p[i] = fma2(p[i], x[i], bc(a[k]));
-#pragma unroll
-      for (int i = 0; i < P; ++i) dp[i] = fma2(dp[i], x[i], p[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < P; ++i) p[i] = fma2(p[i], x[i], bc(a[0]));
-#pragma unroll
-    for (int i = 0; i < P; ++i) {
-      const float2 pq = mul2(p[i], iq[i]);
-      const float2 t0 = mul2(u[i], iq[i]);
-      const float2 z = make_float2(neg_sign_times(s[i].x, pq.x), neg_sign_times(s[i].y, pq.y));
-      out[i] = mul2(t0, fma2(ds[i], z, dp[i]));
-      const float2 w = mul2(t0, z);
-      const float2 x2 = mul2(x[i], x[i]);
-      const float2 x3 = mul2(x2, x[i]);
-      const float2 x4 = mul2(x2, x2);
-      const float2 x5 = mul2(x4, x[i]);
-      acc_add(acc[0], t0);
-      acc_fma(acc[1], t0, x[i]);
-      acc_fma(acc[2], t0, x2);
-      acc_fma(acc[3], t0, x3);
-      acc_fma(acc[4], t0, x4);
-      acc_fma(acc[5], t0, x5);
-      acc_fma(acc[6], w, x[i]);
-      acc_fma(acc[7], w, x2);
-      acc_fma(acc[8], w, x3);
-      acc_fma(acc[9], w, x4);
-    }
-  }
-
-  // FAST, shallow: every polynomial by Estrin's scheme on the powers x^2, x^4 the
-  // coefficient terms need anyway (P: 5 FMAs, depth 3; P': 4; h: 3; A': 3), and A(x)
-  // = h x with h in FMA form under the sign guard (one rarely taken branch per
-  // vector re-evaluates A with the reference's rounding).  36 FMA-pipe
-  // instructions per pair against grad_given's 39, and a critical path of ~2/3.
-  // Error of the FMA h: <= 3 u H(|x|) (u = 2^-24, H = sum |b_k| |x|^(k-1)),
-  // under the guard threshold 2^-17 bsum max(1, |x|^3) with >= 10x margin
-  // (see sign_unsafe).
-  template <int NP, typename ACC>
-  __device__ __forceinline__ void grad_estrin_n(const float (&vx)[2 * NP], const float (&vu)[2 * NP],
-                                                float (&o)[2 * NP], ACC (&acc)[KC]) const {
-    float2 x[NP], x2[NP], x3[NP], x4[NP], s[NP];
-    bool bad = false;
-#pragma unroll
-    for (int i = 0; i < NP; ++i) {
-      x[i] = make_float2(vx[2 * i], vx[2 * i + 1]);
-      x2[i] = mul2(x[i], x[i]);
-      x3[i] = mul2(x2[i], x[i]);
-      x4[i] = mul2(x2[i], x2[i]);
-      const float2 h = fma2(x2[i], fma2(bc(b[3]), x[i], bc(b[2])), fma2(bc(b[1]), x[i], bc(b[0])));
-      bad |= sign_unsafe(h.x, x3[i].x) | sign_unsafe(h.y, x3[i].y);
-      s[i] = mul2(h, x[i]);
-    }
-    if (bad) {
-#pragma unroll
-      for (int i = 0; i < NP; ++i) s[i] = series_ref(x[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < NP; ++i) {
-      const float2 q = q_of(s[i]);
-      const float2 iq = make_float2(rcp(q.x), rcp(q.y));
-      const float2 p = fma2(x4[i], fma2(bc(a[5]), x[i], bc(a[4])),
-                            fma2(x2[i], fma2(bc(a[3]), x[i], bc(a[2])), fma2(bc(a[1]), x[i], bc(a[0]))));
-      const float2 dp = fma2(x4[i], bc(da[4]), fma2(x2[i], fma2(bc(da[3]), x[i], bc(da[2])),
-                                                     fma2(bc(da[1]), x[i], bc(da[0]))));
-      const float2 ds = fma2(x2[i], fma2(bc(db[3]), x[i], bc(db[2])), fma2(bc(db[1]), x[i], bc(db[0])));
-      const float2 pq = mul2(p, iq);
-      const float2 t0 = mul2(make_float2(vu[2 * i], vu[2 * i + 1]), iq);
-      const float2 z = make_float2(neg_sign_times(s[i].x, pq.x), neg_sign_times(s[i].y, pq.y));
-      const float2 r = mul2(t0, fma2(ds, z, dp));
-      o[2 * i] = r.x;
-      o[2 * i + 1] = r.y;
-      const float2 w = mul2(t0, z);
-      const float2 x5 = mul2(x4[i], x[i]);
-      acc_add(acc[0], t0);
-      acc_fma(acc[1], t0, x[i]);
-      acc_fma(acc[2], t0, x2[i]);
-      acc_fma(acc[3], t0, x3[i]);
-      acc_fma(acc[4], t0, x4[i]);
-      acc_fma(acc[5], t0, x5);
-      acc_fma(acc[6], w, x[i]);
-      acc_fma(acc[7], w, x2[i]);
-      acc_fma(acc[8], w, x3[i]);
-      acc_fma(acc[9], w, x4[i]);
-    }
-  }
-
   // dx for NP pairs (one 16-byte vector) and their terms folded into acc.
   // FAST: the guard is evaluated for all NP pairs first and resolved by ONE
   // (rarely taken) branch, so the straight-line math of the NP pairs stays in
@@ -610,13 +445,10 @@ struct RationalX2 {
   // backward is latency-bound and loses more to the guard's branches than it
   // gains from 3 fewer FMUL2 per pair (fp32: 323 -> 307 us with the guard,
   // bf16: 260 -> 273 us at KAT-B; 283 us with a warp-uniform __any_sync branch).
-  template <int NP, bool GUARD = true, typename ACC = float2>
+  template <int NP, bool GUARD = true, typename ACC = float2, bool WY = false>
   __device__ __forceinline__ void grad_n(const float (&vx)[2 * NP], const float (&vu)[2 * NP],
-                                         float (&o)[2 * NP], ACC (&acc)[KC]) const {
-    if constexpr (!EXACT && GRKAN_ESTRIN) {
-      grad_estrin_n<NP>(vx, vu, o, acc);
-      return;
-    }
+                                         float (&o)[2 * NP], ACC (&acc)[KC],
+                                         float (*yo)[2 * NP] = nullptr) const {
     constexpr int G = GRKAN_GUARD_NP < NP ? GRKAN_GUARD_NP : NP;
     static_assert(NP % G == 0, "guard group must divide the pair count");
 #pragma unroll
@@ -624,33 +456,6 @@ struct RationalX2 {
       float2 x[G], s[G], x2[G], x3[G];
 #pragma unroll
       for (int i = 0; i < G; ++i) x[i] = make_float2(vx[2 * (i0 + i)], vx[2 * (i0 + i) + 1]);
-      if (!EXACT && GRKAN_LEAN_FAST && (!GUARD || !GRKAN_SIGN_GUARD)) {
-        if constexpr (GRKAN_LEAN_ILP > 1) {
-          if (i0 == 0) {  // every pair of the vector in one lock-step pass
-            float2 xx[NP], uu[NP], rr[NP];
-#pragma unroll
-            for (int i = 0; i < NP; ++i) {
-              xx[i] = make_float2(vx[2 * i], vx[2 * i + 1]);
-              uu[i] = make_float2(vu[2 * i], vu[2 * i + 1]);
-            }
-            grad_lean_n<NP>(xx, uu, rr, acc);
-#pragma unroll
-            for (int i = 0; i < NP; ++i) {
-              o[2 * i] = rr[i].x;
-              o[2 * i + 1] = rr[i].y;
-            }
-          }
-          continue;
-        }
-#pragma unroll
-        for (int i = 0; i < G; ++i) {
-          const int e = 2 * (i0 + i);
-          const float2 r = grad_lean(x[i], make_float2(vu[e], vu[e + 1]), acc);
-          o[e] = r.x;
-          o[e + 1] = r.y;
-        }
-        continue;
-      }
       if (EXACT || !GUARD || !GRKAN_SIGN_GUARD) {
 #pragma unroll
         for (int i = 0; i < G; ++i) {
@@ -676,9 +481,14 @@ struct RationalX2 {
 #pragma unroll
       for (int i = 0; i < G; ++i) {
         const int e = 2 * (i0 + i);
-        const float2 r = grad_given(x[i], make_float2(vu[e], vu[e + 1]), s[i], x2[i], x3[i], acc);
+        float2 yv;
+        const float2 r = grad_given<WY>(x[i], make_float2(vu[e], vu[e + 1]), s[i], x2[i], x3[i], acc, &yv);
         o[e] = r.x;
         o[e + 1] = r.y;
+        if constexpr (WY) {
+          (*yo)[e] = yv.x;
+          (*yo)[e + 1] = yv.y;
+        }
       }
     }
   }

@@ -254,10 +254,13 @@ __device__ __forceinline__ void produce(const T* const (&src)[NT], T* const (&ri
 
 // ---------------------------------------------------------------------------
 // K2 staged: backward main pass, degrees (5, 4).
+// FWD: the fused forward + backward step -- the forward value y = P/Q of every
+// element falls out of the backward's own P and 1/Q (pq), so y is written beside
+// dx from the same shared-memory x (x read once for both passes).
 // ---------------------------------------------------------------------------
-template <typename T, bool EXACT, bool CHECK, bool DET, bool INSTR = false>
+template <typename T, bool EXACT, bool CHECK, bool DET, bool INSTR = false, bool FWD = false>
 __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
-    k_bwd_staged(const T* __restrict__ x, const T* __restrict__ dy, T* __restrict__ dx,
+    k_bwd_staged(const T* __restrict__ x, const T* __restrict__ dy, T* __restrict__ dx, T* __restrict__ y,
                  const typename VecIO<T, 1>::A* __restrict__ ca,
                  const typename VecIO<T, 1>::A* __restrict__ cb,
                  typename VecIO<T, 1>::A* __restrict__ part, Geom geo, int stages,
@@ -343,15 +346,22 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
       const T* xs = sx + slot * slot_elems;
       const T* us = su + slot * slot_elems;
       auto vec = [&](int j) {
-        A vx[W], vu[W], o[W];
+        A vx[W], vu[W], o[W], yo[W];
         RW::unpack(*reinterpret_cast<const uint4*>(xs + so[j]), vx);
         RW::unpack(*reinterpret_cast<const uint4*>(us + so[j]), vu);
         if constexpr (PK) {
-          rp.template grad_n<W / 2, kGuard<T>>(vx, vu, o, acc2);
+          if constexpr (FWD)
+            rp.template grad_n<W / 2, kGuard<T>, float2, true>(vx, vu, o, acc2, &yo);
+          else
+            rp.template grad_n<W / 2, kGuard<T>>(vx, vu, o, acc2);
         } else {
 #pragma unroll
-          for (int e = 0; e < W; ++e) o[e] = rs.grad(vx[e], vu[e], acc);
+          for (int e = 0; e < W; ++e) {
+            o[e] = rs.grad(vx[e], vu[e], acc);
+            if constexpr (FWD) yo[e] = rs.value(vx[e]);
+          }
         }
+        if constexpr (FWD) __stcs(reinterpret_cast<uint4*>(y + (gp[j] - dx)), RW::pack(yo));
         if constexpr (CHECK) {
 #pragma unroll
           for (int e = 0; e < W; ++e) {

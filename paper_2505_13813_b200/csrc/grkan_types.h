@@ -95,15 +95,6 @@ struct Plan {
 #ifndef GRKAN_PROBE_NOMEM
 #define GRKAN_PROBE_NOMEM 0       // diagnostic only: staged backward computes on unfilled shared memory
 #endif
-#ifndef GRKAN_LEAN_FAST
-#define GRKAN_LEAN_FAST 0         // FAST, reference-rounded A(x): P' / h' by simultaneous Horner (no da/db registers)
-#endif
-#ifndef GRKAN_LEAN_ILP
-#define GRKAN_LEAN_ILP 1          // with GRKAN_LEAN_FAST: >1 = all pairs of a vector in lock step
-#endif
-#ifndef GRKAN_ESTRIN
-#define GRKAN_ESTRIN 0            // FAST backward: Estrin polynomials + guarded FMA A(x) (grad_estrin_n)
-#endif
 #ifndef GRKAN_FWD_CTAS
 #define GRKAN_FWD_CTAS 8
 #endif
@@ -135,6 +126,7 @@ struct LaunchArgs {
   bool exact, vec, check;
   bool partials_only;  // backward: K2 only (deterministic multi-GPU path)
   bool instr;          // backward: the instrumented instantiations (coverage + access counts)
+  void* y2;            // backward: also write the forward value here (fused step; staged plans only)
   cudaStream_t stream;
 };
 

@@ -10,6 +10,7 @@ Public functions
   rational_backward(x, dy, a, b)       -> dx, da, db (grkan_bwd: K2 + K3)
   rational_backward_atomic(x, dy, a, b)-> dx, da, db (grkan_bwd_atomic, Alg. 1 comparator)
   rational_backward(..., deterministic=True)   row-sharding-invariant da/db
+  rational_forward_backward(x, dy, a, b) -> y, dx, da, db in one pass (grkan_fwd_bwd)
   backward_partials(x, dy, a, b)       -> dx, per-block partials (grkan_bwd_partials)
   reduce_partials(part, ...)           -> da, db (grkan_reduce_partials)
   linear_backward_fused(dy, w, x, a, b)-> dx, da, db (grkan_linear_bwd: tcgen05 dY.W + rational
@@ -165,6 +166,36 @@ def rational_backward(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor, b: tor
         if check_finite or check_overflow:
             read_status(workspace[:STATUS_BYTES])
     return dx, da, db
+
+
+def rational_forward_backward(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor, b: torch.Tensor,
+                              exact: bool = False, check_finite: bool = False, check_overflow: bool = False,
+                              workspace: torch.Tensor | None = None):
+    """(y, dx, da, db): forward_tensor and backward_blocked of the same x in one pass
+    (grkan_fwd_bwd: x read once, y from the backward's own P and 1/Q).  Same results as
+    rational_forward + rational_backward -- EXACT y / dx bitwise the reference's."""
+    rows, d, ng, m1, n = _validate(x, a, b)
+    if dy.shape != x.shape:
+        from .errors import GridGeometryError
+        raise GridGeometryError("grid geometry invalid: x and upstream shapes differ")
+    if dy.dtype != x.dtype or dy.device != x.device:
+        raise UnsupportedError("upstream must match x in dtype and device")
+    x, dy, a, b = x.contiguous(), dy.contiguous(), a.contiguous(), b.contiguous()
+    y = torch.empty_like(x)
+    dx = torch.empty_like(x)
+    da = torch.empty((ng, m1), dtype=a.dtype, device=x.device)
+    db = torch.empty((ng, n), dtype=a.dtype, device=x.device)
+    nbytes = workspace_bytes(rows, d, ng, m1, n, x.dtype)
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+    with torch.cuda.device(x.device):
+        rc = N.lib().grkan_fwd_bwd(x.data_ptr(), dy.data_ptr(), a.data_ptr(), _ptr(b), y.data_ptr(), dx.data_ptr(),
+                                   da.data_ptr(), _ptr(db), workspace.data_ptr(), workspace.numel(), rows, d, ng,
+                                   m1, n, _DT[x.dtype], _flags(exact, check_finite, False), _stream(x.device))
+        _raise(rc)
+        if check_finite or check_overflow:
+            read_status(workspace[:STATUS_BYTES])
+    return y, dx, da, db
 
 
 def det_block_rows(d: int, ng: int, dtype: torch.dtype) -> int:

@@ -12,14 +12,18 @@ __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b
 // MODE 2: acc = acc * kernelParam + pairC     (.F32 broadcast from a uniform register)
 // MODE 3: acc = acc * pairB                   (FMUL2, two F32x2 operands)
 // MODE 4: acc = pairB * acc + acc2            (both multiplicands pairs, addend another chain)
+// MODE 5: acc_i = shared * pairB_i + acc_i     (the coefficient-term accumulation: one pair
+//                                              operand common to consecutive FFMA2s -> .reuse)
 template <int MODE, int CH>
-__global__ void k(float* out, float s, float t, int iters) {
+__global__ void k(float* out, const float* __restrict__ init, float s, float t, int iters) {
+  // operands loaded at run time, so the loop holds real register operands (no
+  // rematerialised constants)
   float2 acc[CH], b[CH], c[CH];
 #pragma unroll
   for (int i = 0; i < CH; ++i) {
-    acc[i] = f2(threadIdx.x * 1e-3f + i, i * 0.5f);
-    b[i] = f2(0.999f - i * 1e-4f, 0.998f + threadIdx.x * 1e-7f);
-    c[i] = f2(1e-3f * i, 2e-3f);
+    acc[i] = f2(init[(threadIdx.x + 3 * i) & 63], init[(threadIdx.x + 3 * i + 1) & 63]);
+    b[i] = f2(init[64 + ((threadIdx.x + i) & 63)], init[64 + ((threadIdx.x + i + 7) & 63)]);
+    c[i] = f2(init[128 + ((threadIdx.x + 5 * i) & 63)], init[128 + ((threadIdx.x + i + 9) & 63)]);
   }
   const float sr = s * (threadIdx.x & 1 ? 1.0f : 0.9999f);  // a per-thread (vector) register
   for (int it = 0; it < iters; ++it) {
@@ -30,6 +34,7 @@ __global__ void k(float* out, float s, float t, int iters) {
       if (MODE == 2) acc[i] = __ffma2_rn(acc[i], f2(t, t), c[i]);
       if (MODE == 3) acc[i] = __fmul2_rn(acc[i], b[i]);
       if (MODE == 4) acc[i] = __ffma2_rn(b[i], acc[i], acc[(i + 1) % CH]);
+      if (MODE == 5) acc[i] = __ffma2_rn(c[0], b[i], acc[i]);
     }
   }
   float r = 0;
@@ -47,7 +52,7 @@ void run(const char* name, float* dbuf, int sms, int warps_per_sm) {
   float ms = 0;
   for (int rep = 0; rep < 3; ++rep) {
     cudaEventRecord(e0);
-    k<MODE, CH><<<blocks, threads>>>(dbuf, 0.999f, 0.9995f, iters);
+    k<MODE, CH><<<blocks, threads>>>(dbuf, dbuf + 8, 0.999f, 0.9995f, iters);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
@@ -61,15 +66,19 @@ void run(const char* name, float* dbuf, int sms, int warps_per_sm) {
 
 int main() {
   float* d;
-  cudaMalloc(&d, 8);
+  cudaMalloc(&d, 256 * sizeof(float));
+  float h[256];
+  for (int i = 0; i < 256; ++i) h[i] = i < 8 ? 0.f : (i < 72 ? 0.5f + i * 1e-3f : (i < 136 ? 0.9999f - (i % 64) * 1e-6f : 1e-4f * (i % 64)));
+  cudaMemcpy(d, h, sizeof h, cudaMemcpyHostToDevice);
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  for (int w : {16, 32, 64}) {
+  for (int w : {16, 32}) {
     run<0, 8>("FFMA2 pair*pair+pair", d, sms, w);
     run<1, 8>("FFMA2 pair*vreg.F32+pair", d, sms, w);
     run<2, 8>("FFMA2 pair*ureg.F32+pair", d, sms, w);
     run<3, 8>("FMUL2 pair*pair", d, sms, w);
     run<4, 8>("FFMA2 pair*pair+pair(other chain)", d, sms, w);
+    run<5, 8>("FFMA2 shared*pair+acc (reuse)", d, sms, w);
   }
   for (int w : {16, 32}) {
     run<0, 1>("FFMA2 pair*pair+pair", d, sms, w);
