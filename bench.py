@@ -925,6 +925,10 @@ def run_train(args, rank, world, local_rank):
         }), flush=True)
 
 
+# a rank that never arrives fails the collective (and the run) instead of hanging it
+PG_TIMEOUT = __import__("datetime").timedelta(seconds=float(os.environ.get("GRKAN_PG_TIMEOUT_S", "600")))
+
+
 def free_port():
     import socket
     with socket.socket() as sk:
@@ -941,6 +945,10 @@ def spawn_ranks(args, argv):
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)]
     cmd += list(sys.argv[1:] if argv is None else argv)
     env = dict(os.environ, GRKAN_BENCH_SPAWNED="1")
+    if args.dist_backend == "gloo":
+        # single node: gloo's transport on loopback (its default device follows the
+        # hostname, which need not resolve to this box inside a container)
+        env.setdefault("GLOO_SOCKET_IFNAME", "lo")
     return subprocess.run(cmd, env=env).returncode
 
 
@@ -978,9 +986,9 @@ def main(argv=None):
             os.environ.setdefault("NCCL_DEBUG", "INFO")
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank), timeout=PG_TIMEOUT)
         else:
-            dist.init_process_group(args.dist_backend)
+            dist.init_process_group(args.dist_backend, timeout=PG_TIMEOUT)
         assert dist.get_world_size() == args.gpus, (dist.get_world_size(), args.gpus)
     try:
         if args.config in TRAIN_CONFIGS:

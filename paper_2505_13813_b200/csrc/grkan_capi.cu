@@ -96,10 +96,23 @@ int64_t det_rows(int32_t d, int32_t ng, size_t es) {
   return static_cast<int64_t>(RS) * ((GRKAN_DET_ROWS + RS - 1) / RS);
 }
 
+// bf16 FAST backward: the x-factor table (grkan_staged.cuh LUT); results agree
+// with the table-free kernel within the FAST tolerance.  GRKAN_LUT=1 in the
+// environment forces it wherever it fits (tests), =0 disables it (A/B); unset:
+// the build default over row runs of at least kLutMinStagesPerCta stages.
+constexpr int64_t kLutMinStagesPerCta = 64;
+
+bool lut_enabled(int64_t stages_per_cta) {
+  const char* v = getenv("GRKAN_LUT");
+  if (v && (v[0] == '0' || v[0] == '1')) return v[0] == '1';
+  return GRKAN_LUT != 0 && stages_per_cta >= kLutMinStagesPerCta;
+}
+
 // nt = tensors streamed in (1 forward, 2 backward).  det: one partial per
 // global RB-row block (slot-major), independent of the launch geometry.
+// lut: the caller runs the bf16 FAST backward (grkan_bwd / grkan_bwd_partials).
 Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_t es, bool vec, int nt,
-               int sms, bool det = false) {
+               int sms, bool det = false, bool lut = false) {
   Plan p;
   const int dg = d / ng;
   const int64_t RB = det ? det_rows(d, ng, es) : 0;
@@ -118,6 +131,25 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
     p.smem = static_cast<size_t>(p.stages) * nt * RS * dg * es;
     if (nt == 2)  // + per-lane accumulator totals [10][256] in the accumulation type
       p.smem += static_cast<size_t>(m1 + n) * 32 * grkan::kConsumerWarpsHost * (es == 8 ? 8 : 4);
+    // the table build (~2 us per CTA) and the shallower ring pay off only over
+    // long row runs: measured +3% at KAT-B (85 stages per CTA), -10% at KAT-S (21)
+    const int64_t stages_per_cta = nsu * RU / RS / (static_cast<int64_t>(sms) * grkan::kBwdCtasPerSmHost / ng + 1);
+    if (nt == 2 && es == 2 && lut && lut_enabled(stages_per_cta)) {
+      // the table takes a ring stage's place; the widest exponent window that
+      // keeps kBwdCtasPerSm CTAs resident (<= 16 exponents: kLutSignStride slots)
+      const size_t ring = static_cast<size_t>(GRKAN_LUT_STAGES) * nt * RS * dg * es;
+      const size_t acc = static_cast<size_t>(m1 + n) * 32 * grkan::kConsumerWarpsHost * 4;
+      for (int ne = 16; ne >= 8; --ne) {
+        const size_t sm = ring + acc + static_cast<size_t>(grkan::kLutSignStride + ne * 128) * sizeof(float2);
+        if (kSmemPerSm / (sm + 2048) >= static_cast<size_t>(grkan::kBwdCtasPerSmHost)) {
+          p.stages = GRKAN_LUT_STAGES;
+          p.smem = sm;
+          p.geo.lut_ne = ne;
+          p.geo.lut_e0 = GRKAN_LUT_TOP - ne + 1;
+          break;
+        }
+      }
+    }
     const int occ_regs = nt == 2 ? grkan::kBwdCtasPerSmHost : grkan::kFwdCtasPerSmHost;
     int occ = static_cast<int>(kSmemPerSm / (p.smem + 2048));
     occ = occ < 1 ? 1 : (occ > occ_regs ? occ_regs : occ);
@@ -370,7 +402,8 @@ int grkan_bwd(const void* x, const void* dy, const void* a, const void* b, void*
   const size_t es = elem_size(dtype);
   const bool vec = vec_ok(d, n_groups, es, {x, dy, dx});
   const bool det = (flags & GRKAN_FLAG_DETERMINISTIC) != 0;
-  const Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count(), det);
+  const Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count(), det,
+                           (flags & GRKAN_FLAG_EXACT) == 0);
   if (!plan_fits(p)) return fail(GRKAN_ERR_GRID, "grid geometry invalid: %lld CTAs", (long long)p.ctas);
   const size_t need = ws_bytes_for(p, m1, n, dtype);
   if (ws_bytes < need)
@@ -531,7 +564,8 @@ int grkan_bwd_partials(const void* x, const void* dy, const void* a, const void*
   if (!x || !dy || !dx || !a || (n > 0 && !b)) return fail(GRKAN_ERR_INVALID, "null tensor pointer");
   const size_t es = elem_size(dtype);
   const bool vec = vec_ok(d, n_groups, es, {x, dy, dx});
-  const Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count(), true);
+  const Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count(), true,
+                           (flags & GRKAN_FLAG_EXACT) == 0);
   if (!plan_fits(p)) return fail(GRKAN_ERR_GRID, "grid geometry invalid: %lld CTAs", (long long)p.ctas);
   LaunchArgs L{};
   L.plan = &p;

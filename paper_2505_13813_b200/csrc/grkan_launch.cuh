@@ -132,9 +132,9 @@ cudaError_t launch_bwd_t(const LaunchArgs& L) {
   }
   if (p.staged) {
     e0 = dispatch_staged<T>(L, [&](auto e, auto ck) -> cudaError_t {
-      auto go = [&](auto det, auto fwd) -> cudaError_t {
+      auto go = [&](auto det, auto fwd, auto lut) -> cudaError_t {
         constexpr auto kern = k_bwd_staged<T, decltype(e)::value, decltype(ck)::value, decltype(det)::value, false,
-                                           decltype(fwd)::value>;
+                                           decltype(fwd)::value, decltype(lut)::value>;
         cudaError_t ae = allow_smem<kern>(p.smem);
         if (ae != cudaSuccess) return ae;
         kern<<<static_cast<unsigned>(p.ctas), kStagedThreads, p.smem, L.stream>>>(
@@ -143,8 +143,13 @@ cudaError_t launch_bwd_t(const LaunchArgs& L) {
             p.stages, L.st);
         return cudaGetLastError();
       };
-      if (L.y2) return go(std::false_type{}, std::true_type{});  // fused step: per-CTA partials only
-      return p.geo.det ? go(std::true_type{}, std::false_type{}) : go(std::false_type{}, std::false_type{});
+      const std::false_type no;
+      if (L.y2) return go(no, std::true_type{}, no);  // fused step: per-CTA partials only
+      if constexpr (std::is_same<T, __nv_bfloat16>::value && !decltype(e)::value) {
+        if (p.geo.lut_ne > 0)  // the x-factor table (make_plan decides; sizes its shared memory)
+          return p.geo.det ? go(std::true_type{}, no, std::true_type{}) : go(no, no, std::true_type{});
+      }
+      return p.geo.det ? go(std::true_type{}, no, no) : go(no, no, no);
     });
   } else e0 = dispatch<T>(L, is_fixed(L), [&](auto e, auto fx, auto wc, auto ck) -> cudaError_t {
     constexpr bool FX = decltype(fx)::value;

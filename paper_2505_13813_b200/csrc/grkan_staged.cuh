@@ -59,7 +59,22 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// With a suspend-time hint the waiting warp is parked until the phase flips (or
+// the hint expires) instead of re-issuing try_wait: a spinning producer or an
+// early consumer otherwise takes issue slots from the consumer warps that share
+// its scheduler (ncu: ~7% of the bf16 backward's instructions were retry loops).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if GRKAN_WAIT_HINT_NS > 0
+  asm volatile(
+      "{\n"
+      "  .reg .pred p;\n"
+      "WAIT_%=:\n"
+      "  mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "  @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "n"(GRKAN_WAIT_HINT_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n"
       "  .reg .pred p;\n"
@@ -69,6 +84,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 // global -> shared bulk copy (TMA engine), completion counted on `bar`;
 // L2 evict-first: every byte is read exactly once.
@@ -258,7 +274,24 @@ __device__ __forceinline__ void produce(const T* const (&src)[NT], T* const (&ri
 // element falls out of the backward's own P and 1/Q (pq), so y is written beside
 // dx from the same shared-memory x (x read once for both passes).
 // ---------------------------------------------------------------------------
-template <typename T, bool EXACT, bool CHECK, bool DET, bool INSTR = false, bool FWD = false>
+// LUT (bf16 I/O, FAST): the x-only factors {1/Q, -sign(A) P/Q^2} of every x in
+// the exponent window come from a per-CTA shared-memory table built at start
+// (RationalX2::lut_entry); elements outside the window evaluate the same
+// function inline, so results do not depend on the window.
+//
+// Table slot of the two bf16 values packed in one 32-bit word: the magnitude's
+// offset from the window base, plus kLutSignStride for negative x.  Returns
+// false if either value is outside the window (slots then unusable).
+__device__ __forceinline__ bool lut_slots(uint32_t w, uint32_t base, uint32_t span, uint32_t& s0,
+                                          uint32_t& s1) {
+  const uint32_t t0 = (w & 0x7fffu) - base;
+  const uint32_t t1 = ((w >> 16) & 0x7fffu) - base;
+  s0 = t0 + ((w >> 4) & static_cast<uint32_t>(kLutSignStride));
+  s1 = t1 + ((w >> 20) & static_cast<uint32_t>(kLutSignStride));
+  return (t0 < span) & (t1 < span);
+}
+
+template <typename T, bool EXACT, bool CHECK, bool DET, bool INSTR = false, bool FWD = false, bool LUT = false>
 __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
     k_bwd_staged(const T* __restrict__ x, const T* __restrict__ dy, T* __restrict__ dx, T* __restrict__ y,
                  const typename VecIO<T, 1>::A* __restrict__ ca,
@@ -270,6 +303,8 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
   constexpr int W = RW::W;
   constexpr bool PK = std::is_same<A, float>::value;
   constexpr int KC = 10;
+  static_assert(!LUT || (std::is_same<T, __nv_bfloat16>::value && !EXACT && !INSTR && !FWD),
+                "the x-factor table is the bf16 FAST backward only");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ A red[DET ? 2 : 1][DET ? kConsumerWarps : 1][DET ? KC : 1];
@@ -322,6 +357,20 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
     } else {
       rs.load(ca, cb, g, 6, 4);
     }
+    // the x-factor table after the accumulator totals: built once by the
+    // consumer warps (the producer is already streaming the first stages)
+    float2* const tbl = reinterpret_cast<float2*>(sacc + KC * 32 * kConsumerWarps);
+    const uint32_t lut_base = static_cast<uint32_t>(geo.lut_e0) << 7;
+    const uint32_t lut_span = static_cast<uint32_t>(geo.lut_ne) << 7;
+    if constexpr (LUT) {
+      for (uint32_t i = threadIdx.x; i < 2 * lut_span; i += 32 * kConsumerWarps) {
+        const uint32_t neg = i >= lut_span ? 1u : 0u;
+        const uint32_t t = i - neg * lut_span;
+        const float xv = __uint_as_float(((lut_base + t) | (neg << 15)) << 16);
+        tbl[t + neg * kLutSignStride] = rp.lut_entry(xv);
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps) : "memory");
+    }
     // this thread's fixed (row, vector) slots in every stage
     int sr[kVPT], so[kVPT];
     T* gp[kVPT];  // running global pointers: advance by RS rows per stage
@@ -347,9 +396,37 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
       const T* us = su + slot * slot_elems;
       auto vec = [&](int j) {
         A vx[W], vu[W], o[W], yo[W];
-        RW::unpack(*reinterpret_cast<const uint4*>(xs + so[j]), vx);
+        const uint4 rx = *reinterpret_cast<const uint4*>(xs + so[j]);
+        RW::unpack(rx, vx);
         RW::unpack(*reinterpret_cast<const uint4*>(us + so[j]), vu);
-        if constexpr (PK) {
+        if constexpr (LUT) {
+          const uint32_t wx[4] = {rx.x, rx.y, rx.z, rx.w};
+          uint32_t sl[W];
+          bool in = true;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) in &= lut_slots(wx[i], lut_base, lut_span, sl[2 * i], sl[2 * i + 1]);
+          float2 ent[W];
+          if (__builtin_expect(in, 1)) {
+#pragma unroll
+            for (int e = 0; e < W; ++e) ent[e] = tbl[sl[e]];
+          } else {  // an x outside the window: that element evaluates the table function itself
+#pragma unroll
+            for (int e = 0; e < W; ++e) {
+              const uint32_t t = ((e & 1) ? (wx[e >> 1] >> 16) : wx[e >> 1]) & 0x7fffu;
+              if (t - lut_base < lut_span)
+                ent[e] = tbl[sl[e]];
+              else
+                ent[e] = rp.lut_entry(vx[e]);
+            }
+          }
+#pragma unroll
+          for (int p = 0; p < W / 2; ++p) {
+            const float2 r = rp.grad_lut(make_float2(vx[2 * p], vx[2 * p + 1]), make_float2(vu[2 * p], vu[2 * p + 1]),
+                                         ent[2 * p], ent[2 * p + 1], acc2);
+            o[2 * p] = r.x;
+            o[2 * p + 1] = r.y;
+          }
+        } else if constexpr (PK) {
           if constexpr (FWD)
             rp.template grad_n<W / 2, kGuard<T>, float2, true>(vx, vu, o, acc2, &yo);
           else

@@ -25,6 +25,10 @@ struct Geom {
   int32_t det;      // deterministic (global row-block) partials: slot-major
                     // part[(block * ng + g) * kc + k], one partial per RB-row block
   int32_t spb;      // staged deterministic: stages per block (RB / RS)
+  // staged bf16 FAST backward: per-CTA table of the x-only factors over the x
+  // exponent window [lut_e0, lut_e0 + lut_ne) (biased fp32/bf16 exponents)
+  int32_t lut_e0;
+  int32_t lut_ne;   // 0: no table
   // instrumented launches only (grkan_bwd_instrumented; null otherwise): per-element
   // visit counts [rows * d] and element-access tallies {reads, writes, rmw}
   int32_t* cov;
@@ -98,6 +102,19 @@ struct Plan {
 #ifndef GRKAN_FWD_CTAS
 #define GRKAN_FWD_CTAS 8
 #endif
+#ifndef GRKAN_LUT
+#define GRKAN_LUT 1               // bf16 FAST backward: per-CTA table of the x-only factors
+#endif
+#ifndef GRKAN_WAIT_HINT_NS
+#define GRKAN_WAIT_HINT_NS 1000000  // staged ring waits: mbarrier.try_wait suspend-time hint (0: none)
+#endif
+#ifndef GRKAN_LUT_STAGES
+#define GRKAN_LUT_STAGES 3        // ring depth when the table shares shared memory
+#endif
+#ifndef GRKAN_LUT_TOP
+#define GRKAN_LUT_TOP 129         // highest tabulated biased exponent: |x| < 2^3
+#endif
+constexpr int kLutSignStride = 2048;  // table slots: [t] for x >= 0, [2048 + t] for x < 0
 constexpr int kConsumerWarpsHost = GRKAN_CONSUMER_WARPS;
 constexpr int kStagedThreadsHost = 32 * (GRKAN_CONSUMER_WARPS + 1);
 constexpr int kStageVecsHost = GRKAN_STAGE_VECS;

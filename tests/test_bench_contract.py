@@ -105,7 +105,8 @@ def test_gpus_2_without_launcher_runs_two_ranks():
                           "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1",
                           "--dist-backend", "gloo"],
                          capture_output=True, text=True, timeout=900, cwd=ROOT,
-                         env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+                         env=dict({k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")},
+                                  GRKAN_BENCH_TRACE_AFTER="600", GRKAN_PG_TIMEOUT_S="300"))
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1

@@ -1,0 +1,100 @@
+"""bf16 FAST backward with the per-CTA x-factor table (grkan_staged.cuh LUT).
+
+The table holds {1/Q, -sign(A) P/Q^2} for every bf16 x in an exponent window;
+x outside the window (zeros, tiny, large, non-finite) evaluates the same
+function inline.  These tests put many elements on both sides of the window
+edges and check the result against the oracle exactly as the other bf16 FAST
+tests do (dx within 1e-2 max-scaled per scale band, da/db within 1e-5 of the
+fp64 oracle), and against the direct (table-free) kernel, GRKAN_LUT=0.
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import c_oracle
+from oracle import grkan_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda", 0) if torch.cuda.is_available() else None
+SCALES = (1e-6, 3e-4, 1.0, 4.0, 30.0, 1e3)  # window is [2^-11, 2^3) at KAT shapes
+
+
+def ops():
+    from paper_2505_13813_b200 import ops as _ops
+    return _ops
+
+
+def _inputs(batch, seq, dim, groups, seed):
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((batch, seq, dim)).astype(np.float32)
+    for bi in range(batch):  # one scale band per batch entry
+        x[bi] *= np.float32(SCALES[bi % len(SCALES)])
+    # the window edges, exact zeros of both signs
+    edge = np.array([2.0 ** -11, np.nextafter(np.float32(2.0 ** -11), 0), 8.0, 7.96875, 0.0, -0.0,
+                     -(2.0 ** -11), -8.0], dtype=np.float32)
+    x[0, 0, : edge.size] = edge
+    x[1, 3, 5 : 5 + edge.size] = edge[::-1]
+    u = rng.standard_normal((batch, seq, dim)).astype(np.float32)
+    num = rng.standard_normal((groups, 6))
+    den = rng.standard_normal((groups, 4))
+    xb = torch.from_numpy(x).bfloat16()
+    ub = torch.from_numpy(u).bfloat16()
+    return xb, ub, num, den
+
+
+def _run(xb, ub, num, den, lut):
+    old = os.environ.get("GRKAN_LUT")
+    os.environ["GRKAN_LUT"] = "1" if lut else "0"
+    try:
+        a = torch.from_numpy(num.astype(np.float32)).to(DEV)
+        b = torch.from_numpy(den.astype(np.float32)).to(DEV)
+        dx, da, db = ops().rational_backward(xb.to(DEV), ub.to(DEV), a, b, check_overflow=True)
+        torch.cuda.synchronize()
+        return dx.float().cpu().numpy(), da.cpu().numpy(), db.cpu().numpy()
+    finally:
+        if old is None:
+            del os.environ["GRKAN_LUT"]
+        else:
+            os.environ["GRKAN_LUT"] = old
+
+
+@pytest.mark.parametrize("shape,groups", [((12, 197, 3072), 8), ((12, 197, 1536), 8), ((6, 33, 192), 8),
+                                          ((6, 17, 64), 1)])
+def test_table_path_matches_oracle_across_scales(shape, groups):
+    xb, ub, num, den = _inputs(*shape, groups, seed=11)
+    xr, ur = xb.float().numpy(), ub.float().numpy()
+    r = c_oracle.backward(xr, ur, num, den, 256)
+    dx, da, db = _run(xb, ub, num, den, lut=True)
+    for bi in range(shape[0]):  # max-scaled within each scale band
+        assert orc.matrix_rel(dx[bi], r["dx"][bi]) <= 1e-2, (bi, SCALES[bi % len(SCALES)])
+    assert orc.matrix_rel(da, r["true64_da"]) <= 1e-5
+    assert orc.matrix_rel(db, r["true64_db"]) <= 1e-5
+    assert orc.mae(da, r["true64_da"]) <= orc.mae(r["blocked_da"], r["true64_da"])
+    assert orc.mae(db, r["true64_db"]) <= orc.mae(r["blocked_db"], r["true64_db"])
+
+
+def test_table_path_agrees_with_direct_kernel():
+    xb, ub, num, den = _inputs(12, 197, 3072, 8, seed=12)
+    dx1, da1, db1 = _run(xb, ub, num, den, lut=True)
+    dx0, da0, db0 = _run(xb, ub, num, den, lut=False)
+    for bi in range(xb.shape[0]):
+        assert orc.matrix_rel(dx1[bi], dx0[bi]) <= 1e-2, bi
+    assert orc.matrix_rel(da1, da0) <= 1e-5 and orc.matrix_rel(db1, db0) <= 1e-5
+
+
+def test_table_path_nonfinite_inputs_propagate_and_are_flagged():
+    from paper_2505_13813_b200.errors import NonFiniteInputError
+    xb, ub, num, den = _inputs(2, 9, 3072, 8, seed=13)
+    xb[0, 1, 7] = float("nan")
+    xb[1, 2, 9] = float("inf")
+    a = torch.from_numpy(num.astype(np.float32)).to(DEV)
+    b = torch.from_numpy(den.astype(np.float32)).to(DEV)
+    dx, _, _ = ops().rational_backward(xb.to(DEV), ub.to(DEV), a, b)
+    assert torch.isnan(dx[0, 1, 7]) and not torch.isfinite(dx[1, 2, 9])
+    assert torch.isfinite(dx[0, 0]).all()
+    with pytest.raises(NonFiniteInputError):
+        ops().rational_backward(xb.to(DEV), ub.to(DEV), a, b, check_finite=True)

@@ -1,13 +1,18 @@
-# Round 2 check c: bf16 backward variants (lean FAST math, 1-CTA geometry, compute-only probes) + spawn test under pytest.
+# A/B: mbarrier suspend-time hint (default build) vs none (tools/variants/nohint), and the
+# bf16 x-factor table on/off.  usage: bash tools/gpu_r2c.sh TAG
 TAG=${1:-r2c}
 mkdir -p gpurun_out
-for v in default lean cw16 leancw16 lean3 probe leanprobe; do
-  if [ "$v" = default ]; then L=""; else L="GRKAN_LIB=tools/variants/$v/libgrkan_b200.so"; fi
+one() {  # lib lut cfg dtype
+  if [ "$1" = default ]; then L=""; else L="GRKAN_LIB=tools/variants/$1/libgrkan_b200.so"; fi
+  env $L GRKAN_LUT=$2 timeout 300 python bench.py --config $3 --dtype $4 --steps 50 --no-cpu-baseline --e2e-steps 1 > /tmp/ab.json 2>/tmp/ab.err
+  python -c "import json; d=json.load(open('/tmp/ab.json')); k=d['kernels']; print('$1 lut=$2 $3 $4 fwd %.1f bwd %.1f (%.3f) value %.3e' % (k['fwd_us'], k['bwd_us'], k['bwd_frac'], d['value']), d['clocks']['sm_mhz'], d['clocks']['reasons'])" || tail -3 /tmp/ab.err
+}
+for rep in 1 2; do
+for lib in default nohint; do
   for cfg in kat-b kat-s; do
-    env $L timeout 300 python bench.py --config $cfg --steps 30 --warmup 5 --dtype bf16 --no-cpu-baseline --e2e-steps 1 > /tmp/vb.json 2>/tmp/vb.err
-    python -c "import json; d=json.load(open('/tmp/vb.json')); k=d['kernels']; print('$v $cfg bf16', 'bwd=%.1fus(%.3f)'%(k['bwd_us'],k['bwd_frac']), 'fwd=%.1fus(%.3f)'%(k['fwd_us'],k['fwd_frac']), d['clocks']['sm_mhz'], d['clocks']['reasons'])" || tail -3 /tmp/vb.err
+    one $lib 1 $cfg bf16
+    one $lib 0 $cfg bf16
+    one $lib 0 $cfg fp32
   done
-  env $L timeout 300 python bench.py --config kat-b --steps 30 --warmup 5 --dtype fp32 --no-cpu-baseline --e2e-steps 1 > /tmp/vb.json 2>/tmp/vb.err
-  python -c "import json; d=json.load(open('/tmp/vb.json')); k=d['kernels']; print('$v kat-b fp32', 'bwd=%.1fus(%.3f)'%(k['bwd_us'],k['bwd_frac']), 'fwd=%.1fus(%.3f)'%(k['fwd_us'],k['fwd_frac']))" || tail -3 /tmp/vb.err
 done
-GRKAN_BENCH_TRACE_AFTER=100 timeout 600 python -m pytest -q -m gpu tests/test_bench_contract.py > gpurun_out/pytest_${TAG}_contract.txt 2>&1; tail -30 gpurun_out/pytest_${TAG}_contract.txt
+done 2>&1 | tee gpurun_out/ab_${TAG}.txt
