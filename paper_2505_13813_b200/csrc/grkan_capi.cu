@@ -135,19 +135,17 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
     // long row runs: measured +3% at KAT-B (85 stages per CTA), -10% at KAT-S (21)
     const int64_t stages_per_cta = nsu * RU / RS / (static_cast<int64_t>(sms) * grkan::kBwdCtasPerSmHost / ng + 1);
     if (nt == 2 && es == 2 && lut && lut_enabled(stages_per_cta)) {
-      // the table takes a ring stage's place; the widest exponent window that
-      // keeps kBwdCtasPerSm CTAs resident (<= 16 exponents: kLutSignStride slots)
+      // the table (two float arrays over a 16-exponent window) takes a ring
+      // stage's place and the accumulator totals go one slot per lane pair, so
+      // kBwdCtasPerSm CTAs stay resident
       const size_t ring = static_cast<size_t>(GRKAN_LUT_STAGES) * nt * RS * dg * es;
-      const size_t acc = static_cast<size_t>(m1 + n) * 32 * grkan::kConsumerWarpsHost * 4;
-      for (int ne = 16; ne >= 8; --ne) {
-        const size_t sm = ring + acc + static_cast<size_t>(grkan::kLutSignStride + ne * 128) * sizeof(float2);
-        if (kSmemPerSm / (sm + 2048) >= static_cast<size_t>(grkan::kBwdCtasPerSmHost)) {
-          p.stages = GRKAN_LUT_STAGES;
-          p.smem = sm;
-          p.geo.lut_ne = ne;
-          p.geo.lut_e0 = GRKAN_LUT_TOP - ne + 1;
-          break;
-        }
+      const size_t acc = static_cast<size_t>(m1 + n) * 16 * grkan::kConsumerWarpsHost * 4;
+      const size_t sm = ring + acc + 2 * 2 * grkan::kLutSignStride * sizeof(float);
+      if (kSmemPerSm / (sm + 2048) >= static_cast<size_t>(grkan::kBwdCtasPerSmHost)) {
+        p.stages = GRKAN_LUT_STAGES;
+        p.smem = sm;
+        p.geo.lut_ne = 16;
+        p.geo.lut_e0 = GRKAN_LUT_TOP - 15;  // <= 128: the slot arithmetic needs base <= 0x4000
       }
     }
     const int occ_regs = nt == 2 ? grkan::kBwdCtasPerSmHost : grkan::kFwdCtasPerSmHost;

@@ -457,12 +457,12 @@ struct RationalX2 {
     return make_float2(iq, iq * z);
   }
 
-  // dx and the ten terms of one pair given its table entries {1/Q, -sign(A)P/Q^2}:
-  // 25 packed FP32 ops per pair instead of grad_given's 39, no MUFU.
+  // dx and the ten terms of one pair given its table entries iq = 1/Q and
+  // wq = -sign(A)P/Q^2: 25 packed FP32 ops per pair instead of grad_given's 39, no MUFU.
   template <typename ACC>
-  __device__ __forceinline__ float2 grad_lut(float2 x, float2 u, float2 e0, float2 e1, ACC (&acc)[KC]) const {
-    const float2 t0 = mul2(u, make_float2(e0.x, e1.x));  // u/Q
-    const float2 w = mul2(u, make_float2(e0.y, e1.y));   // -sign(A) u P/Q^2
+  __device__ __forceinline__ float2 grad_lut(float2 x, float2 u, float2 iq, float2 wq, ACC (&acc)[KC]) const {
+    const float2 t0 = mul2(u, iq);  // u/Q
+    const float2 w = mul2(u, wq);   // -sign(A) u P/Q^2
     const float2 dp = horner2<false, 5>(da, x);
     const float2 ds = horner2<false, 4>(db, x);
     const float2 dx = fma2(w, ds, mul2(t0, dp));         // u (P'/Q - sign(A) A' P/Q^2)

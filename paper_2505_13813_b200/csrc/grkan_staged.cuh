@@ -157,8 +157,15 @@ struct Raw16<double> {
 // Accumulator flush: every geo.flush stages each lane folds its register
 // accumulators into a private fp32 slot in shared memory ([k][thread], bank-
 // conflict free) and restarts them, so per-lane fp32 chains stay short
-// (<= 6 * flush terms) at ~40 instructions per flush.
-template <typename A, int KC, bool PK>
+// (<= 6 * flush terms) at ~40 instructions per flush.  SH = 1: one slot per
+// lane pair (the pair's totals meet by one shuffle first) -- half the shared
+// memory, for the bf16 table kernel.
+template <int SH>
+__device__ __forceinline__ int acc_slot(int k) {
+  return k * ((32 * kConsumerWarps) >> SH) + (static_cast<int>(threadIdx.x) >> SH);
+}
+
+template <typename A, int KC, bool PK, int SH = 0>
 __device__ __forceinline__ void lane_flush(A (&acc)[KC], float2 (&acc2)[KC], A* __restrict__ sacc) {
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
@@ -170,21 +177,36 @@ __device__ __forceinline__ void lane_flush(A (&acc)[KC], float2 (&acc2)[KC], A* 
       v = acc[k];
       acc[k] = A(0);
     }
-    sacc[k * (32 * kConsumerWarps) + threadIdx.x] += v;
+    if constexpr (SH == 1) {
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      if ((threadIdx.x & 1) == 0) sacc[acc_slot<SH>(k)] += v;
+    } else {
+      sacc[acc_slot<SH>(k)] += v;
+    }
   }
+}
+
+// This warp's lanes' slot values for coefficient k (SH = 1: 16 slots, lanes >= 16 add 0).
+template <typename A, int SH>
+__device__ __forceinline__ A warp_slot_value(const A* __restrict__ sacc, int k) {
+  const int lane = threadIdx.x & 31;
+  if constexpr (SH == 1)
+    return lane < 16 ? sacc[k * (16 * kConsumerWarps) + (threadIdx.x >> 5) * 16 + lane] : A(0);
+  else
+    return sacc[acc_slot<0>(k)];
 }
 
 // End of CTA: each consumer warp folds its lanes' shared-memory totals with a
 // fixed butterfly into partial slot (CTA j, warp w):
 // part[((g * KC + k) * pg + j) * 8 + w]  ->  n_tiles = pg * 8 per (group, coefficient).
-template <typename A, int KC>
+template <typename A, int KC, int SH = 0>
 __device__ __forceinline__ void warp_store(const A* __restrict__ sacc, A* __restrict__ part, int g, int64_t j,
                                            int warp, const Geom& geo) {
   const int lane = threadIdx.x & 31;
   const int64_t n_tiles = (int64_t)geo.pg * kConsumerWarps;
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
-    A v = sacc[k * (32 * kConsumerWarps) + threadIdx.x];
+    A v = warp_slot_value<A, SH>(sacc, k);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) part[((int64_t)g * KC + k) * n_tiles + j * kConsumerWarps + warp] = v;
@@ -212,15 +234,16 @@ __device__ __forceinline__ void staged_range(const Geom& geo, int& g, int64_t& j
 // re-zeroed for the next block.  The partial depends only on the block's
 // data (the thread -> element map is fixed per stage), never on which CTA
 // processed it: bitwise identical for any row sharding aligned to RB.
-template <typename A, int KC>
+template <typename A, int KC, int SH = 0>
 __device__ __forceinline__ void block_store(A* __restrict__ sacc, A (&red)[2][kConsumerWarps][KC], int buf,
                                             A* __restrict__ part, int g, int64_t blk, int warp,
                                             const Geom& geo) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
-    A v = sacc[k * (32 * kConsumerWarps) + threadIdx.x];
-    sacc[k * (32 * kConsumerWarps) + threadIdx.x] = A(0);
+    A v = warp_slot_value<A, SH>(sacc, k);
+    __syncwarp();
+    if (SH == 0 || lane < 16) sacc[SH == 1 ? k * (16 * kConsumerWarps) + warp * 16 + lane : acc_slot<0>(k)] = A(0);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) red[buf][warp][k] = v;
@@ -275,20 +298,23 @@ __device__ __forceinline__ void produce(const T* const (&src)[NT], T* const (&ri
 // dx from the same shared-memory x (x read once for both passes).
 // ---------------------------------------------------------------------------
 // LUT (bf16 I/O, FAST): the x-only factors {1/Q, -sign(A) P/Q^2} of every x in
-// the exponent window come from a per-CTA shared-memory table built at start
+// a 16-exponent window come from a per-CTA shared-memory table built at start
 // (RationalX2::lut_entry); elements outside the window evaluate the same
-// function inline, so results do not depend on the window.
-//
-// Table slot of the two bf16 values packed in one 32-bit word: the magnitude's
-// offset from the window base, plus kLutSignStride for negative x.  Returns
-// false if either value is outside the window (slots then unusable).
-__device__ __forceinline__ bool lut_slots(uint32_t w, uint32_t base, uint32_t span, uint32_t& s0,
-                                          uint32_t& s1) {
-  const uint32_t t0 = (w & 0x7fffu) - base;
-  const uint32_t t1 = ((w >> 16) & 0x7fffu) - base;
-  s0 = t0 + ((w >> 4) & static_cast<uint32_t>(kLutSignStride));
-  s1 = t1 + ((w >> 20) & static_cast<uint32_t>(kLutSignStride));
-  return (t0 < span) & (t1 < span);
+// function inline, so results do not depend on the window.  Table: two float
+// arrays (1/Q, then -sign(A)P/Q^2) of kLutSlots, slot = t | sign << 11 with
+// t = bf16 magnitude bits - window base (0 <= t < 2048).
+constexpr int kLutSlots = 2 * kLutSignStride;
+
+// The two bf16 values of one 32-bit word at once: d = w + C puts each half at
+// sign * 0x8000 + 0x4000 + (magnitude - base), so a half is inside the window
+// iff its bits 11-14 read 1000b, and its slot is its low 11 bits plus its sign
+// moved to bit 11 (carries between the halves only occur for |x| >= 2^115 or
+// non-finite x, which are outside the window and make the check fail).
+// Returns the packed slots (lo | hi << 16); `bad` collects window misses.
+__device__ __forceinline__ uint32_t lut_slots2(uint32_t w, uint32_t c, uint32_t& bad) {
+  const uint32_t d = w + c;
+  bad |= (d ^ 0x40004000u) & 0x78007800u;
+  return (d & 0x07ff07ffu) | ((d & 0x80008000u) >> 4);
 }
 
 template <typename T, bool EXACT, bool CHECK, bool DET, bool INSTR = false, bool FWD = false, bool LUT = false>
@@ -330,7 +356,8 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
   }
   if (threadIdx.x < 32 * kConsumerWarps) {
 #pragma unroll
-    for (int k = 0; k < 10; ++k) sacc[k * (32 * kConsumerWarps) + threadIdx.x] = 0;
+    for (int k = 0; k < 10; ++k)
+      if (!LUT || (threadIdx.x & 1) == 0) sacc[acc_slot<LUT ? 1 : 0>(k)] = 0;
   }
   __syncthreads();
 
@@ -359,15 +386,15 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
     }
     // the x-factor table after the accumulator totals: built once by the
     // consumer warps (the producer is already streaming the first stages)
-    float2* const tbl = reinterpret_cast<float2*>(sacc + KC * 32 * kConsumerWarps);
+    float* const tiq = reinterpret_cast<float*>(sacc + KC * ((32 * kConsumerWarps) >> (LUT ? 1 : 0)));
     const uint32_t lut_base = static_cast<uint32_t>(geo.lut_e0) << 7;
-    const uint32_t lut_span = static_cast<uint32_t>(geo.lut_ne) << 7;
+    const uint32_t lut_c = (0x4000u - lut_base) * 0x10001u;
     if constexpr (LUT) {
-      for (uint32_t i = threadIdx.x; i < 2 * lut_span; i += 32 * kConsumerWarps) {
-        const uint32_t neg = i >= lut_span ? 1u : 0u;
-        const uint32_t t = i - neg * lut_span;
-        const float xv = __uint_as_float(((lut_base + t) | (neg << 15)) << 16);
-        tbl[t + neg * kLutSignStride] = rp.lut_entry(xv);
+      for (int i = threadIdx.x; i < kLutSlots; i += 32 * kConsumerWarps) {
+        const uint32_t t = i & (kLutSignStride - 1), neg = static_cast<uint32_t>(i) >> 11;
+        const float2 e = rp.lut_entry(__uint_as_float(((lut_base + t) | (neg << 15)) << 16));
+        tiq[i] = e.x;
+        tiq[kLutSlots + i] = e.y;
       }
       asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps) : "memory");
     }
@@ -401,28 +428,40 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
         RW::unpack(*reinterpret_cast<const uint4*>(us + so[j]), vu);
         if constexpr (LUT) {
           const uint32_t wx[4] = {rx.x, rx.y, rx.z, rx.w};
-          uint32_t sl[W];
-          bool in = true;
+          uint32_t sl[4], bad = 0;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) in &= lut_slots(wx[i], lut_base, lut_span, sl[2 * i], sl[2 * i + 1]);
-          float2 ent[W];
-          if (__builtin_expect(in, 1)) {
+          for (int i = 0; i < 4; ++i) sl[i] = lut_slots2(wx[i], lut_c, bad);
+          float iq[W], wf[W];
+          if (__builtin_expect(bad == 0, 1)) {
 #pragma unroll
-            for (int e = 0; e < W; ++e) ent[e] = tbl[sl[e]];
+            for (int i = 0; i < 4; ++i) {
+              const uint32_t s0 = sl[i] & 0xffffu, s1 = sl[i] >> 16;
+              iq[2 * i] = tiq[s0];
+              iq[2 * i + 1] = tiq[s1];
+              wf[2 * i] = tiq[kLutSlots + s0];
+              wf[2 * i + 1] = tiq[kLutSlots + s1];
+            }
           } else {  // an x outside the window: that element evaluates the table function itself
 #pragma unroll
             for (int e = 0; e < W; ++e) {
-              const uint32_t t = ((e & 1) ? (wx[e >> 1] >> 16) : wx[e >> 1]) & 0x7fffu;
-              if (t - lut_base < lut_span)
-                ent[e] = tbl[sl[e]];
-              else
-                ent[e] = rp.lut_entry(vx[e]);
+              const uint32_t h = (e & 1) ? (wx[e >> 1] >> 16) : (wx[e >> 1] & 0xffffu);
+              const uint32_t t = (h & 0x7fffu) - lut_base;
+              float2 en;
+              if (t < static_cast<uint32_t>(kLutSignStride)) {
+                const uint32_t sidx = t | ((h >> 4) & 0x800u);
+                en = make_float2(tiq[sidx], tiq[kLutSlots + sidx]);
+              } else {
+                en = rp.lut_entry(vx[e]);
+              }
+              iq[e] = en.x;
+              wf[e] = en.y;
             }
           }
 #pragma unroll
           for (int p = 0; p < W / 2; ++p) {
             const float2 r = rp.grad_lut(make_float2(vx[2 * p], vx[2 * p + 1]), make_float2(vu[2 * p], vu[2 * p + 1]),
-                                         ent[2 * p], ent[2 * p + 1], acc2);
+                                         make_float2(iq[2 * p], iq[2 * p + 1]), make_float2(wf[2 * p], wf[2 * p + 1]),
+                                         acc2);
             o[2 * p] = r.x;
             o[2 * p + 1] = r.y;
           }
@@ -471,13 +510,13 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
       // term-evaluation floor (see lane_flush).
       const bool block_end = DET && ((s + 1) % geo.spb == 0 || s + 1 == nst);
       if (++since_flush == geo.flush || s + 1 == nst || block_end) {
-        lane_flush<A, KC, PK>(acc, acc2, sacc);
+        lane_flush<A, KC, PK, LUT ? 1 : 0>(acc, acc2, sacc);
         since_flush = 0;
       }
       if constexpr (DET) {
         if (block_end) {
           __syncwarp();
-          block_store<A, KC>(sacc, red, (s / geo.spb) & 1, part, g, tile + s / geo.spb, warp, geo);
+          block_store<A, KC, LUT ? 1 : 0>(sacc, red, (s / geo.spb) & 1, part, g, tile + s / geo.spb, warp, geo);
         }
       }
       if (++slot == stages) {
@@ -487,7 +526,7 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
     }
     if constexpr (!DET) {
       __syncwarp();
-      warp_store<A, KC>(sacc, part, g, tile, warp, geo);
+      warp_store<A, KC, LUT ? 1 : 0>(sacc, part, g, tile, warp, geo);
     }
     if constexpr (INSTR) {
       if (lane == 0) {
