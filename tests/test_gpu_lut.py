@@ -20,7 +20,7 @@ from oracle import grkan_oracle as orc
 pytestmark = pytest.mark.gpu
 
 DEV = torch.device("cuda", 0) if torch.cuda.is_available() else None
-SCALES = (1e-6, 3e-4, 1.0, 4.0, 30.0, 1e3)  # window is [2^-11, 2^3) at KAT shapes
+SCALES = (1e-6, 3e-5, 1.0, 4.0, 30.0, 1e3)  # the table window is |x| in [2^-13, 2^3)
 
 
 def ops():
@@ -34,8 +34,8 @@ def _inputs(batch, seq, dim, groups, seed):
     for bi in range(batch):  # one scale band per batch entry
         x[bi] *= np.float32(SCALES[bi % len(SCALES)])
     # the window edges, exact zeros of both signs
-    edge = np.array([2.0 ** -11, np.nextafter(np.float32(2.0 ** -11), 0), 8.0, 7.96875, 0.0, -0.0,
-                     -(2.0 ** -11), -8.0], dtype=np.float32)
+    edge = np.array([2.0 ** -13, np.nextafter(np.float32(2.0 ** -13), 0), 8.0, 7.96875, 0.0, -0.0,
+                     -(2.0 ** -13), -8.0], dtype=np.float32)
     x[0, 0, : edge.size] = edge
     x[1, 3, 5 : 5 + edge.size] = edge[::-1]
     u = rng.standard_normal((batch, seq, dim)).astype(np.float32)
