@@ -108,6 +108,14 @@ bool lut_enabled(int64_t stages_per_cta) {
   return GRKAN_LUT != 0 && stages_per_cta >= kLutMinStagesPerCta;
 }
 
+// bf16 forward from the y table (k_fwd_lut, both policies: the table holds the
+// EXACT values).  GRKAN_FWD_LUT=0 selects the FP32-math staged forward (A/B).
+bool fwd_lut_enabled() {
+  const char* v = getenv("GRKAN_FWD_LUT");
+  if (v && (v[0] == '0' || v[0] == '1')) return v[0] == '1';
+  return GRKAN_FWD_LUT != 0;
+}
+
 // nt = tensors streamed in (1 forward, 2 backward).  det: one partial per
 // global RB-row block (slot-major), independent of the launch geometry.
 // lut: the caller runs the bf16 FAST backward (grkan_bwd / grkan_bwd_partials).
@@ -119,8 +127,11 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
   p.geo.det = det ? 1 : 0;
   p.geo.one = 1.0f;
   p.W = vec ? static_cast<int>(16 / es) : 1;
-  const int stage_vecs = nt == 2 ? grkan::kStageVecsHost : grkan::kFwdStageVecsHost;
-  if (vec && m1 == 6 && n == 4 && dg / p.W <= stage_vecs && staged_enabled(nt, es)) {
+  // bf16 forward: the y table kernel (k_fwd_lut) on the backward's staged geometry
+  const bool fwd_lut = nt == 1 && es == 2 && vec && m1 == 6 && n == 4 && fwd_lut_enabled() &&
+                       dg / p.W <= grkan::kStageVecsHost;
+  const int stage_vecs = (nt == 2 || fwd_lut) ? grkan::kStageVecsHost : grkan::kFwdStageVecsHost;
+  if (vec && m1 == 6 && n == 4 && dg / p.W <= stage_vecs && (fwd_lut || staged_enabled(nt, es))) {
     // TMA-staged persistent kernels (grkan_staged.cuh)
     const int V = dg / p.W;
     const int RS = stage_vecs / V;
@@ -148,14 +159,20 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
         p.geo.lut_e0 = GRKAN_LUT_TOP - 15;  // <= 128: the slot arithmetic needs base <= 0x4000
       }
     }
-    const int occ_regs = nt == 2 ? grkan::kBwdCtasPerSmHost : grkan::kFwdCtasPerSmHost;
+    if (fwd_lut) {
+      p.stages = GRKAN_FWD_LUT_STAGES;
+      p.smem = static_cast<size_t>(p.stages) * RS * dg * es + 2 * grkan::kLutSignStride * sizeof(uint16_t);
+      p.geo.lut_ne = 16;
+      p.geo.lut_e0 = GRKAN_LUT_TOP - 15;
+    }
+    const int occ_regs = nt == 2 ? grkan::kBwdCtasPerSmHost : (fwd_lut ? GRKAN_FWD_LUT_CTAS : grkan::kFwdCtasPerSmHost);
     int occ = static_cast<int>(kSmemPerSm / (p.smem + 2048));
     occ = occ < 1 ? 1 : (occ > occ_regs ? occ_regs : occ);
     const int64_t slots = static_cast<int64_t>(sms) * occ;
     int64_t pg = slots / ng;
     if (pg > nsu) pg = nsu;
     if (pg < 1) pg = 1;
-    p.threads = nt == 2 ? grkan::kStagedThreadsHost : grkan::kFwdThreadsHost;
+    p.threads = (nt == 2 || fwd_lut) ? grkan::kStagedThreadsHost : grkan::kFwdThreadsHost;
     p.geo.rows = rows;
     p.geo.d = d;
     p.geo.ng = ng;

@@ -639,4 +639,126 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdCtasPerSm)
   if (CHECK && chk.bad()) st->nonfinite_input = 1;
 }
 
+// ---------------------------------------------------------------------------
+// K1 table (bf16 I/O, both policies): y of every x in the 16-exponent window
+// from a per-CTA table of bf16 values built at start with the reference's
+// rounding (separately rounded Horner, IEEE division: rational.py:218-224), so
+// y is bitwise the EXACT result in FAST mode too; x outside the window
+// evaluates the same function inline.  Per element: the packed slot
+// arithmetic of the backward's table (lut_slots2) and one 2-byte shared load,
+// no FP32 math -- the pass streams at the HBM rate.  Geometry of the staged
+// backward (kConsumerWarps consumers + 1 producer, kStageVecs-vector stages).
+// ---------------------------------------------------------------------------
+template <bool CHECK>
+__global__ void __launch_bounds__(kStagedThreads, GRKAN_FWD_LUT_CTAS)
+    k_fwd_lut(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y, const float* __restrict__ ca,
+              const float* __restrict__ cb, Geom geo, int stages, DevStatus* __restrict__ st) {
+  using T = __nv_bfloat16;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
+  int g;
+  int64_t tile, row0;
+  int nr;
+  staged_range(geo, g, tile, row0, nr);
+  T* const sx = reinterpret_cast<T*>(smem_raw);
+  uint16_t* const ty = reinterpret_cast<uint16_t*>(sx + (size_t)stages * geo.RS * geo.dg);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      const T* const src[1] = {x};
+      T* const ring[1] = {sx};
+      produce<T, 1>(src, ring, geo, row0, nr, stages, full, empty, g);
+    }
+    return;
+  }
+  Rational<float, true, 6, 4, true> rs;  // the reference's rounding
+  rs.load(ca, cb, g, 6, 4);
+  const uint32_t lut_base = static_cast<uint32_t>(geo.lut_e0) << 7;
+  const uint32_t lut_c = (0x4000u - lut_base) * 0x10001u;
+  auto yval = [&](uint32_t h) -> uint32_t {  // bf16 bits of y for the bf16 bits h of x
+    const __nv_bfloat16 v = __float2bfloat16_rn(rs.value(__uint_as_float(h << 16)));
+    return static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(&v));
+  };
+  for (int i = threadIdx.x; i < kLutSlots; i += 32 * kConsumerWarps) {
+    const uint32_t t = i & (kLutSignStride - 1), neg = static_cast<uint32_t>(i) >> 11;
+    ty[i] = static_cast<uint16_t>(yval((lut_base + t) | (neg << 15)));
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps) : "memory");
+  int sr[kVPT], so[kVPT];
+  int64_t goff[kVPT];
+  const int svecs = geo.RS * geo.V;
+#pragma unroll
+  for (int j = 0; j < kVPT; ++j) {
+    const int k = threadIdx.x + j * 32 * kConsumerWarps;
+    const int r = k / geo.V, c = k - (k / geo.V) * geo.V;
+    sr[j] = k < svecs ? r : 0x7fffffff;
+    so[j] = r * geo.dg + c * 8;
+    goff[j] = (int64_t)r * geo.d + (int64_t)g * geo.dg + c * 8;
+  }
+  Checker<float> chk;
+  const int nst = (nr + geo.RS - 1) / geo.RS;
+  int slot = 0;
+  uint32_t phase = 0;
+  for (int s = 0; s < nst; ++s) {
+    mbar_wait(&full[slot], phase);
+    const int rows_here = min(geo.RS, nr - s * geo.RS);
+    const T* xs = sx + (size_t)slot * geo.RS * geo.dg;
+    T* ys = y + (row0 + (int64_t)s * geo.RS) * geo.d;
+    uint4 rx[kVPT];
+#pragma unroll
+    for (int j = 0; j < kVPT; ++j)
+      if (sr[j] < rows_here) rx[j] = *reinterpret_cast<const uint4*>(xs + so[j]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+#pragma unroll
+    for (int j = 0; j < kVPT; ++j) {
+      if (sr[j] < rows_here) {
+        const uint32_t wx[4] = {rx[j].x, rx[j].y, rx[j].z, rx[j].w};
+        uint32_t sl[4], bad = 0, wy[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sl[i] = lut_slots2(wx[i], lut_c, bad);
+        if (__builtin_expect(bad == 0, 1)) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            wy[i] = static_cast<uint32_t>(ty[sl[i] & 0xffffu]) | (static_cast<uint32_t>(ty[sl[i] >> 16]) << 16);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            uint32_t o[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const uint32_t h = e ? (wx[i] >> 16) : (wx[i] & 0xffffu);
+              const uint32_t t = (h & 0x7fffu) - lut_base;
+              o[e] = t < static_cast<uint32_t>(kLutSignStride) ? static_cast<uint32_t>(ty[t | ((h >> 4) & 0x800u)])
+                                                              : yval(h);
+            }
+            wy[i] = o[0] | (o[1] << 16);
+          }
+        }
+        if constexpr (CHECK) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            chk.add(__uint_as_float(wx[i] << 16));
+            chk.add(__uint_as_float(wx[i] & 0xffff0000u));
+          }
+        }
+        __stcs(reinterpret_cast<uint4*>(ys + goff[j]), make_uint4(wy[0], wy[1], wy[2], wy[3]));
+      }
+    }
+    if (++slot == stages) {
+      slot = 0;
+      phase ^= 1;
+    }
+  }
+  if (CHECK && chk.bad()) st->nonfinite_input = 1;
+}
+
 }  // namespace grkan

@@ -105,6 +105,15 @@ struct Plan {
 #ifndef GRKAN_LUT
 #define GRKAN_LUT 1               // bf16 FAST backward: per-CTA table of the x-only factors
 #endif
+#ifndef GRKAN_FWD_LUT
+#define GRKAN_FWD_LUT 1           // bf16 forward from a per-CTA table of y (k_fwd_lut)
+#endif
+#ifndef GRKAN_FWD_LUT_CTAS
+#define GRKAN_FWD_LUT_CTAS 2      // k_fwd_lut CTAs per SM
+#endif
+#ifndef GRKAN_FWD_LUT_STAGES
+#define GRKAN_FWD_LUT_STAGES 8    // k_fwd_lut ring depth (kStageVecs vectors per stage)
+#endif
 #ifndef GRKAN_WAIT_HINT_NS
 #define GRKAN_WAIT_HINT_NS 1000000  // staged ring waits: mbarrier.try_wait suspend-time hint (0: none)
 #endif

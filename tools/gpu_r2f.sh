@@ -1,10 +1,18 @@
+# Full GPU suite on the current build; KAT-S bf16 with the table forced on/off; bench lines
+# across run_bench's workload surface at KAT-B E (groups 1/16/64, degrees (3,2)).
 TAG=${1:-r2f}
 mkdir -p gpurun_out
-for v in default estrin estrinprobe probe; do
-  if [ "$v" = default ]; then L=""; else L="GRKAN_LIB=tools/variants/$v/libgrkan_b200.so"; fi
-  for cfg in kat-b kat-s; do for dt in bf16 fp32; do
-    env $L timeout 300 python bench.py --config $cfg --steps 30 --warmup 5 --dtype $dt --no-cpu-baseline --e2e-steps 1 > /tmp/vb.json 2>/tmp/vb.err
-    python -c "import json; d=json.load(open('/tmp/vb.json')); k=d['kernels']; print('$v $cfg $dt', 'bwd=%.1fus(%.3f)'%(k['bwd_us'],k['bwd_frac']), 'fwd=%.1fus(%.3f)'%(k['fwd_us'],k['fwd_frac']), d['clocks']['sm_mhz'], d['clocks']['reasons'])" || tail -3 /tmp/vb.err
-  done; done
+timeout 2400 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu_${TAG}.txt 2>&1; tail -3 gpurun_out/pytest_gpu_${TAG}.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_${TAG}.txt 2>&1; tail -1 gpurun_out/smoke_${TAG}.txt
+for lut in 1 0; do
+  GRKAN_LUT=$lut timeout 300 python bench.py --config kat-s --dtype bf16 --steps 50 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_${TAG}_kat-s_bf16_lut${lut}.json 2>/dev/null
+  python -c "import json; d=json.load(open('gpurun_out/bench_${TAG}_kat-s_bf16_lut${lut}.json')); k=d['kernels']; print('kat-s bf16 lut=$lut fwd %.1f bwd %.1f (%.3f) value %.3e' % (k['fwd_us'], k['bwd_us'], k['bwd_frac'], d['value']))"
 done
-GRKAN_LIB=tools/variants/estrin/libgrkan_b200.so timeout 900 python -m pytest -q -m gpu tests/test_gpu_parity.py -x > gpurun_out/pytest_${TAG}_estrin_parity.txt 2>&1; tail -3 gpurun_out/pytest_${TAG}_estrin_parity.txt
+for dt in fp32 bf16; do
+  for g in 1 16 64; do
+    timeout 300 python bench.py --config kat-b --groups $g --dtype $dt --steps 30 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_${TAG}_g${g}_${dt}.json 2>/dev/null
+    python -c "import json; d=json.load(open('gpurun_out/bench_${TAG}_g${g}_${dt}.json')); k=d['kernels']; print('g$g $dt', 'bwd=%.1fus(%.3f)'%(k['bwd_us'],k['bwd_frac']), 'fwd=%.1fus(%.3f)'%(k['fwd_us'],k['fwd_frac']), 'value %.3e frac %.3f'%(d['value'], d['roofline']['frac']), d['clocks']['sm_mhz'])"
+  done
+  timeout 300 python bench.py --config kat-b --num-coeffs 4 --den-coeffs 2 --dtype $dt --steps 30 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_${TAG}_deg32_${dt}.json 2>/dev/null
+  python -c "import json; d=json.load(open('gpurun_out/bench_${TAG}_deg32_${dt}.json')); k=d['kernels']; print('deg(3,2) $dt', 'bwd=%.1fus(%.3f)'%(k['bwd_us'],k['bwd_frac']), 'fwd=%.1fus(%.3f)'%(k['fwd_us'],k['fwd_frac']), 'value %.3e'%d['value'], d['clocks']['sm_mhz'])"
+done
