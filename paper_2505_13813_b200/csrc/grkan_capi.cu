@@ -14,6 +14,7 @@
 #include <cstdlib>
 
 #include "../../include/grkan_b200.h"
+#include "grkan_tmap.h"
 #include "grkan_types.h"
 
 #define GRKAN_VERSION_STRING "grkan_b200 0.1.0 (sm_100a)"
@@ -100,7 +101,7 @@ int64_t det_rows(int32_t d, int32_t ng, size_t es) {
 // with the table-free kernel within the FAST tolerance.  GRKAN_LUT=1 in the
 // environment forces it wherever it fits (tests), =0 disables it (A/B); unset:
 // the build default over row runs of at least kLutMinStagesPerCta stages.
-constexpr int64_t kLutMinStagesPerCta = 64;
+constexpr int64_t kLutMinStagesPerCta = 16;
 
 bool lut_enabled(int64_t stages_per_cta) {
   const char* v = getenv("GRKAN_LUT");
@@ -108,12 +109,11 @@ bool lut_enabled(int64_t stages_per_cta) {
   return GRKAN_LUT != 0 && stages_per_cta >= kLutMinStagesPerCta;
 }
 
-// bf16 forward from the y table (k_fwd_lut, both policies: the table holds the
-// EXACT values).  GRKAN_FWD_LUT=0 selects the FP32-math staged forward (A/B).
-bool fwd_lut_enabled() {
-  const char* v = getenv("GRKAN_FWD_LUT");
-  if (v && (v[0] == '0' || v[0] == '1')) return v[0] == '1';
-  return GRKAN_FWD_LUT != 0;
+// Short row segments: the staged producers copy whole stages as 2-D tensor-map
+// boxes instead of one bulk copy per row (GRKAN_TMA2D=0: per-row copies, A/B).
+bool tma2d_enabled() {
+  const char* v = getenv("GRKAN_TMA2D");
+  return !(v && v[0] == '0');
 }
 
 // nt = tensors streamed in (1 forward, 2 backward).  det: one partial per
@@ -127,11 +127,8 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
   p.geo.det = det ? 1 : 0;
   p.geo.one = 1.0f;
   p.W = vec ? static_cast<int>(16 / es) : 1;
-  // bf16 forward: the y table kernel (k_fwd_lut) on the backward's staged geometry
-  const bool fwd_lut = nt == 1 && es == 2 && vec && m1 == 6 && n == 4 && fwd_lut_enabled() &&
-                       dg / p.W <= grkan::kStageVecsHost;
-  const int stage_vecs = (nt == 2 || fwd_lut) ? grkan::kStageVecsHost : grkan::kFwdStageVecsHost;
-  if (vec && m1 == 6 && n == 4 && dg / p.W <= stage_vecs && (fwd_lut || staged_enabled(nt, es))) {
+  const int stage_vecs = nt == 2 ? grkan::kStageVecsHost : grkan::kFwdStageVecsHost;
+  if (vec && m1 == 6 && n == 4 && dg / p.W <= stage_vecs && staged_enabled(nt, es)) {
     // TMA-staged persistent kernels (grkan_staged.cuh)
     const int V = dg / p.W;
     const int RS = stage_vecs / V;
@@ -143,7 +140,7 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
     if (nt == 2)  // + per-lane accumulator totals [10][256] in the accumulation type
       p.smem += static_cast<size_t>(m1 + n) * 32 * grkan::kConsumerWarpsHost * (es == 8 ? 8 : 4);
     // the table build (~2 us per CTA) and the shallower ring pay off only over
-    // long row runs: measured +3% at KAT-B (85 stages per CTA), -10% at KAT-S (21)
+    // long row runs (table v2: faster at KAT-B, 85 stages per CTA, and KAT-S, 21)
     const int64_t stages_per_cta = nsu * RU / RS / (static_cast<int64_t>(sms) * grkan::kBwdCtasPerSmHost / ng + 1);
     if (nt == 2 && es == 2 && lut && lut_enabled(stages_per_cta)) {
       // the table (two float arrays over a 16-exponent window) takes a ring
@@ -159,20 +156,22 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
         p.geo.lut_e0 = GRKAN_LUT_TOP - 15;  // <= 128: the slot arithmetic needs base <= 0x4000
       }
     }
-    if (fwd_lut) {
-      p.stages = GRKAN_FWD_LUT_STAGES;
-      p.smem = static_cast<size_t>(p.stages) * RS * dg * es + 2 * grkan::kLutSignStride * sizeof(uint16_t);
-      p.geo.lut_ne = 16;
-      p.geo.lut_e0 = GRKAN_LUT_TOP - 15;
+    // (measured: the backward gains from boxes up to 384-byte rows and loses at
+    // 768; the forward's smaller stages only below ~100-byte rows)
+    if (tma2d_enabled() && dg <= 256 &&
+        static_cast<size_t>(dg) * es <= (nt == 2 ? GRKAN_TMA2D_MAX_ROW_BYTES : GRKAN_TMA2D_MAX_ROW_BYTES_FWD) &&
+        (static_cast<size_t>(RS) * dg * es) % 128 == 0 && rows < (int64_t{1} << 31)) {
+      const int nbox = (RS + 255) / 256;  // box dimensions are <= 256
+      if (RS % nbox == 0) p.geo.tma_rows = RS / nbox;
     }
-    const int occ_regs = nt == 2 ? grkan::kBwdCtasPerSmHost : (fwd_lut ? GRKAN_FWD_LUT_CTAS : grkan::kFwdCtasPerSmHost);
+    const int occ_regs = nt == 2 ? grkan::kBwdCtasPerSmHost : grkan::kFwdCtasPerSmHost;
     int occ = static_cast<int>(kSmemPerSm / (p.smem + 2048));
     occ = occ < 1 ? 1 : (occ > occ_regs ? occ_regs : occ);
     const int64_t slots = static_cast<int64_t>(sms) * occ;
     int64_t pg = slots / ng;
     if (pg > nsu) pg = nsu;
     if (pg < 1) pg = 1;
-    p.threads = (nt == 2 || fwd_lut) ? grkan::kStagedThreadsHost : grkan::kFwdThreadsHost;
+    p.threads = nt == 2 ? grkan::kStagedThreadsHost : grkan::kFwdThreadsHost;
     p.geo.rows = rows;
     p.geo.d = d;
     p.geo.ng = ng;
@@ -226,6 +225,29 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
   p.geo.dc = grkan::kBlock % V;
   p.ctas = n_tiles * ng;
   return p;
+}
+
+// The [rows, d] tiled maps of x and dy for a plan with geo.tma_rows > 0 (boxes of
+// tma_rows rows x one group's columns); on any encode failure the plan falls
+// back to per-row copies.
+void attach_maps(Plan& p, grkan::LaunchArgs& L, const void* x, const void* u, int32_t dtype) {
+  if (p.geo.tma_rows <= 0) return;
+  auto fn = grkan::encode_fn();
+  const size_t es = elem_size(dtype);
+  const CUtensorMapDataType ty = dtype == GRKAN_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : dtype == GRKAN_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                       : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.geo.d), static_cast<cuuint64_t>(p.geo.rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.geo.d) * es};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(p.geo.dg), static_cast<cuuint32_t>(p.geo.tma_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  auto enc = [&](CUtensorMap* m, const void* base) {
+    return fn && base &&
+           fn(m, ty, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  if (!enc(&L.tmx, x) || (u && !enc(&L.tmu, u))) p.geo.tma_rows = 0;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -376,7 +398,7 @@ int grkan_fwd(const void* x, void* y, const void* a, const void* b, int64_t rows
   if (!x || !y || !a || (n > 0 && !b)) return fail(GRKAN_ERR_INVALID, "null tensor pointer");
   const size_t es = elem_size(dtype);
   const bool vec = vec_ok(d, n_groups, es, {x, y});
-  const Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 1, sm_count());
+  Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 1, sm_count());
   if (!plan_fits(p)) return fail(GRKAN_ERR_GRID, "grid geometry invalid: %lld CTAs", (long long)p.ctas);
   LaunchArgs L{};
   L.plan = &p;
@@ -391,6 +413,7 @@ int grkan_fwd(const void* x, void* y, const void* a, const void* b, int64_t rows
   L.vec = vec;
   L.check = check;
   L.stream = s;
+  attach_maps(p, L, x, nullptr, dtype);
   cudaError_t e = launch("fwd", dtype, L);
   if (e != cudaSuccess) return cuda_fail(e, "k_fwd launch");
   return GRKAN_OK;
@@ -417,7 +440,7 @@ int grkan_bwd(const void* x, const void* dy, const void* a, const void* b, void*
   const size_t es = elem_size(dtype);
   const bool vec = vec_ok(d, n_groups, es, {x, dy, dx});
   const bool det = (flags & GRKAN_FLAG_DETERMINISTIC) != 0;
-  const Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count(), det,
+  Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count(), det,
                            (flags & GRKAN_FLAG_EXACT) == 0);
   if (!plan_fits(p)) return fail(GRKAN_ERR_GRID, "grid geometry invalid: %lld CTAs", (long long)p.ctas);
   const size_t need = ws_bytes_for(p, m1, n, dtype);
@@ -440,6 +463,7 @@ int grkan_bwd(const void* x, const void* dy, const void* a, const void* b, void*
   L.vec = vec;
   L.check = (flags & GRKAN_FLAG_CHECK_FINITE) != 0;
   L.stream = s;
+  attach_maps(p, L, x, dy, dtype);
   e = launch("bwd", dtype, L);
   if (e != cudaSuccess) return cuda_fail(e, "k_bwd launch");
   return GRKAN_OK;
@@ -453,7 +477,7 @@ int grkan_fwd_bwd(const void* x, const void* dy, const void* a, const void* b, v
   const size_t es = elem_size(dtype);
   const bool det = (flags & GRKAN_FLAG_DETERMINISTIC) != 0;
   const bool vec = vec_ok(d, n_groups, es, {x, dy, dx, y});
-  const Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count(), det);
+  Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count(), det);
   if (rows == 0 || !p.staged || det) {
     // no fused instantiation for this plan: the two passes back to back (same results)
     // (grkan_bwd's CHECK_FINITE covers x, so the forward runs unchecked)
@@ -489,6 +513,7 @@ int grkan_fwd_bwd(const void* x, const void* dy, const void* a, const void* b, v
   L.vec = vec;
   L.check = (flags & GRKAN_FLAG_CHECK_FINITE) != 0;
   L.stream = s;
+  attach_maps(p, L, x, dy, dtype);
   e = launch("bwd", dtype, L);
   if (e != cudaSuccess) return cuda_fail(e, "k_bwd (fused step) launch");
   return GRKAN_OK;
@@ -515,7 +540,7 @@ int grkan_bwd_p2p(const void* x, const void* dy, const void* a, const void* b, v
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(status)");
   const size_t es = elem_size(dtype);
   const bool vec = rows > 0 && vec_ok(d, n_groups, es, {x, dy, dx});
-  const Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count());
+  Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count());
   if (!plan_fits(p)) return fail(GRKAN_ERR_GRID, "grid geometry invalid: %lld CTAs", (long long)p.ctas);
   const size_t need = ws_bytes_for(p, m1, n, dtype);
   if (ws_bytes < need) return fail(GRKAN_ERR_INVALID, "workspace too small: %zu < %zu bytes", ws_bytes, need);
@@ -536,6 +561,7 @@ int grkan_bwd_p2p(const void* x, const void* dy, const void* a, const void* b, v
     L.check = (flags & GRKAN_FLAG_CHECK_FINITE) != 0;
     L.partials_only = true;
     L.stream = s;
+    attach_maps(p, L, x, dy, dtype);
     e = launch("bwd", dtype, L);
     if (e != cudaSuccess) return cuda_fail(e, "k_bwd (partials) launch");
   }
@@ -579,7 +605,7 @@ int grkan_bwd_partials(const void* x, const void* dy, const void* a, const void*
   if (!x || !dy || !dx || !a || (n > 0 && !b)) return fail(GRKAN_ERR_INVALID, "null tensor pointer");
   const size_t es = elem_size(dtype);
   const bool vec = vec_ok(d, n_groups, es, {x, dy, dx});
-  const Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count(), true,
+  Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count(), true,
                            (flags & GRKAN_FLAG_EXACT) == 0);
   if (!plan_fits(p)) return fail(GRKAN_ERR_GRID, "grid geometry invalid: %lld CTAs", (long long)p.ctas);
   LaunchArgs L{};
@@ -598,6 +624,7 @@ int grkan_bwd_partials(const void* x, const void* dy, const void* a, const void*
   L.check = check;
   L.partials_only = true;
   L.stream = s;
+  attach_maps(p, L, x, dy, dtype);
   cudaError_t e = launch("bwd", dtype, L);
   if (e != cudaSuccess) return cuda_fail(e, "k_bwd (partials) launch");
   return GRKAN_OK;
@@ -675,6 +702,7 @@ int grkan_bwd_instrumented(const void* x, const void* dy, const void* a, const v
   L.check = false;
   L.instr = true;
   L.stream = s;
+  if (!naive) attach_maps(p, L, x, dy, dtype);
   e = launch(naive ? "atomic" : "bwd", dtype, L);
   if (e != cudaSuccess) return cuda_fail(e, "instrumented backward launch");
   return GRKAN_OK;

@@ -40,6 +40,7 @@
 
 #include "../../include/grkan_b200.h"
 #include "grkan_staged.cuh"
+#include "grkan_tmap.h"
 #include "grkan_types.h"
 
 namespace grkan {
@@ -541,19 +542,7 @@ __global__ void __launch_bounds__(64 + 128 * ES, 1)
 
 // ---- host -------------------------------------------------------------------
 
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  // resolved once; a function-local static is initialised thread-safely, so
-  // concurrent first callers (the C ABI is reentrant) do not race
-  static const PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    return nullptr;
-  }();
-  return fn;
-}
+using grkan::encode_fn;
 
 bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_in, uint32_t box_out,
               CUtensorMapSwizzle sw) {

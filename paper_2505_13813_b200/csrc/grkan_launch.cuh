@@ -67,20 +67,6 @@ template <typename T>
 cudaError_t launch_fwd_t(const LaunchArgs& L) {
   using A = typename VecIO<T, 1>::A;
   const Plan& p = *L.plan;
-  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-    if (p.staged && p.geo.lut_ne > 0) {  // the y table (both policies: it holds the EXACT values)
-      auto go = [&](auto ck) -> cudaError_t {
-        constexpr auto kern = k_fwd_lut<decltype(ck)::value>;
-        cudaError_t ae = allow_smem<kern>(p.smem);
-        if (ae != cudaSuccess) return ae;
-        kern<<<static_cast<unsigned>(p.ctas), kStagedThreads, p.smem, L.stream>>>(
-            static_cast<const T*>(L.x), static_cast<T*>(L.out), static_cast<const float*>(L.a),
-            static_cast<const float*>(L.b), p.geo, p.stages, L.st);
-        return cudaGetLastError();
-      };
-      return L.check ? go(std::true_type{}) : go(std::false_type{});
-    }
-  }
   if (p.staged) {
     return dispatch_staged<T>(L, [&](auto e, auto ck) -> cudaError_t {
       constexpr auto kern = k_fwd_staged<T, decltype(e)::value, decltype(ck)::value>;
@@ -88,7 +74,7 @@ cudaError_t launch_fwd_t(const LaunchArgs& L) {
       if (ae != cudaSuccess) return ae;
       kern<<<static_cast<unsigned>(p.ctas), kFwdThreads, p.smem, L.stream>>>(
           static_cast<const T*>(L.x), static_cast<T*>(L.out), static_cast<const A*>(L.a),
-          static_cast<const A*>(L.b), p.geo, p.stages, L.st);
+          static_cast<const A*>(L.b), p.geo, p.stages, L.st, L.tmx);
       return cudaGetLastError();
     });
   }
@@ -121,7 +107,7 @@ cudaError_t launch_bwd_t(const LaunchArgs& L) {
         kern<<<static_cast<unsigned>(p.ctas), kStagedThreads, p.smem, L.stream>>>(
             static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out), nullptr,
             static_cast<const A*>(L.a), static_cast<const A*>(L.b), static_cast<A*>(L.part), p.geo, p.stages,
-            L.st);
+            L.st, L.tmx, L.tmu);
         return cudaGetLastError();
       }
       auto fw = [&](auto fx, auto wc) -> cudaError_t {
@@ -154,7 +140,7 @@ cudaError_t launch_bwd_t(const LaunchArgs& L) {
         kern<<<static_cast<unsigned>(p.ctas), kStagedThreads, p.smem, L.stream>>>(
             static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out), static_cast<T*>(L.y2),
             static_cast<const A*>(L.a), static_cast<const A*>(L.b), static_cast<A*>(L.part), p.geo,
-            p.stages, L.st);
+            p.stages, L.st, L.tmx, L.tmu);
         return cudaGetLastError();
       };
       const std::false_type no;

@@ -96,6 +96,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// 2-D tiled tensor copy (TMA): box at (c0 = column, c1 = row) of a [rows, d] map.
+__device__ __forceinline__ void tma2d_g2s(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                          uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -262,27 +271,41 @@ __device__ __forceinline__ void block_store(A* __restrict__ sacc, A (&red)[2][kC
 
 // ---------------------------------------------------------------------------
 // Producer: lane 0 of the last warp fills the ring, one bulk copy per row
-// segment per tensor.  `nt` tensors (1 forward, 2 backward).
+// segment per tensor -- or, with geo.tma_rows > 0 (short row segments, where
+// per-row copies cost more than they move), RS / tma_rows 2-D tensor-map boxes
+// per tensor (full boxes: rows past the tensor end arrive zero-filled, rows past
+// the CTA's run are read and ignored).  `nt` tensors (1 forward, 2 backward).
 // ---------------------------------------------------------------------------
 template <typename T, int NT>
 __device__ __forceinline__ void produce(const T* const (&src)[NT], T* const (&ring)[NT], const Geom& geo,
                                         int64_t row0, int nr, int stages, uint64_t* full,
-                                        uint64_t* empty, int g) {
+                                        uint64_t* empty, int g, const CUtensorMap* const (&maps)[NT]) {
   const uint64_t policy = evict_first_policy();
   const int RS = geo.RS;
   const int nst = (nr + RS - 1) / RS;
   const uint32_t seg = static_cast<uint32_t>(geo.dg * sizeof(T));
+  const int tr = geo.tma_rows;
   int slot = 0;
   uint32_t phase = 0;  // parity of the current pass over the ring
   for (int s = 0; s < nst; ++s) {
     if (s >= stages) mbar_wait(&empty[slot], phase ^ 1);  // released by the previous pass
-    const int rows_here = min(RS, nr - s * RS);
-    mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(rows_here) * seg * NT);
-    for (int r = 0; r < rows_here; ++r) {
-      const int64_t goff = (row0 + s * RS + r) * geo.d + (int64_t)g * geo.dg;
+    if (tr > 0) {
+      mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(RS) * seg * NT);
+      for (int r = 0; r < RS; r += tr) {
 #pragma unroll
-      for (int t = 0; t < NT; ++t)
-        bulk_g2s(ring[t] + ((size_t)slot * RS + r) * geo.dg, src[t] + goff, seg, &full[slot], policy);
+        for (int t = 0; t < NT; ++t)
+          tma2d_g2s(ring[t] + ((size_t)slot * RS + r) * geo.dg, maps[t], g * geo.dg,
+                    static_cast<int>(row0 + (int64_t)s * RS + r), &full[slot], policy);
+      }
+    } else {
+      const int rows_here = min(RS, nr - s * RS);
+      mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(rows_here) * seg * NT);
+      for (int r = 0; r < rows_here; ++r) {
+        const int64_t goff = (row0 + s * RS + r) * geo.d + (int64_t)g * geo.dg;
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+          bulk_g2s(ring[t] + ((size_t)slot * RS + r) * geo.dg, src[t] + goff, seg, &full[slot], policy);
+      }
     }
     if (++slot == stages) {
       slot = 0;
@@ -323,7 +346,8 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
                  const typename VecIO<T, 1>::A* __restrict__ ca,
                  const typename VecIO<T, 1>::A* __restrict__ cb,
                  typename VecIO<T, 1>::A* __restrict__ part, Geom geo, int stages,
-                 DevStatus* __restrict__ st) {
+                 DevStatus* __restrict__ st, const __grid_constant__ CUtensorMap tmx,
+                 const __grid_constant__ CUtensorMap tmu) {
   using A = typename VecIO<T, 1>::A;
   using RW = Raw16<T>;
   constexpr int W = RW::W;
@@ -371,7 +395,8 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
     if (lane == 0) {
       const T* const src[2] = {x, dy};
       T* const ring[2] = {sx, su};
-      if (!GRKAN_PROBE_NOMEM) produce<T, 2>(src, ring, geo, row0, nr, stages, full, empty, g);
+      const CUtensorMap* const maps[2] = {&tmx, &tmu};
+      if (!GRKAN_PROBE_NOMEM) produce<T, 2>(src, ring, geo, row0, nr, stages, full, empty, g, maps);
     }
   } else {
     RationalX2<EXACT> rp;
@@ -546,7 +571,7 @@ template <typename T, bool EXACT, bool CHECK>
 __global__ void __launch_bounds__(kFwdThreads, kFwdCtasPerSm)
     k_fwd_staged(const T* __restrict__ x, T* __restrict__ y, const typename VecIO<T, 1>::A* __restrict__ ca,
                  const typename VecIO<T, 1>::A* __restrict__ cb, Geom geo, int stages,
-                 DevStatus* __restrict__ st) {
+                 DevStatus* __restrict__ st, const __grid_constant__ CUtensorMap tmx) {
   using A = typename VecIO<T, 1>::A;
   using RW = Raw16<T>;
   constexpr int W = RW::W;
@@ -572,7 +597,8 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdCtasPerSm)
     if (lane == 0) {
       const T* const src[1] = {x};
       T* const ring[1] = {sx};
-      produce<T, 1>(src, ring, geo, row0, nr, stages, full, empty, g);
+      const CUtensorMap* const maps[1] = {&tmx};
+      produce<T, 1>(src, ring, geo, row0, nr, stages, full, empty, g, maps);
     }
     return;
   }
@@ -629,128 +655,6 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdCtasPerSm)
           for (int e = 0; e < W; ++e) chk.add(v[e]);
         }
         __stcs(reinterpret_cast<uint4*>(ys + goff[j]), RW::pack(o));
-      }
-    }
-    if (++slot == stages) {
-      slot = 0;
-      phase ^= 1;
-    }
-  }
-  if (CHECK && chk.bad()) st->nonfinite_input = 1;
-}
-
-// ---------------------------------------------------------------------------
-// K1 table (bf16 I/O, both policies): y of every x in the 16-exponent window
-// from a per-CTA table of bf16 values built at start with the reference's
-// rounding (separately rounded Horner, IEEE division: rational.py:218-224), so
-// y is bitwise the EXACT result in FAST mode too; x outside the window
-// evaluates the same function inline.  Per element: the packed slot
-// arithmetic of the backward's table (lut_slots2) and one 2-byte shared load,
-// no FP32 math -- the pass streams at the HBM rate.  Geometry of the staged
-// backward (kConsumerWarps consumers + 1 producer, kStageVecs-vector stages).
-// ---------------------------------------------------------------------------
-template <bool CHECK>
-__global__ void __launch_bounds__(kStagedThreads, GRKAN_FWD_LUT_CTAS)
-    k_fwd_lut(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y, const float* __restrict__ ca,
-              const float* __restrict__ cb, Geom geo, int stages, DevStatus* __restrict__ st) {
-  using T = __nv_bfloat16;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
-  int g;
-  int64_t tile, row0;
-  int nr;
-  staged_range(geo, g, tile, row0, nr);
-  T* const sx = reinterpret_cast<T*>(smem_raw);
-  uint16_t* const ty = reinterpret_cast<uint16_t*>(sx + (size_t)stages * geo.RS * geo.dg);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (warp == kConsumerWarps) {
-    if (lane == 0) {
-      const T* const src[1] = {x};
-      T* const ring[1] = {sx};
-      produce<T, 1>(src, ring, geo, row0, nr, stages, full, empty, g);
-    }
-    return;
-  }
-  Rational<float, true, 6, 4, true> rs;  // the reference's rounding
-  rs.load(ca, cb, g, 6, 4);
-  const uint32_t lut_base = static_cast<uint32_t>(geo.lut_e0) << 7;
-  const uint32_t lut_c = (0x4000u - lut_base) * 0x10001u;
-  auto yval = [&](uint32_t h) -> uint32_t {  // bf16 bits of y for the bf16 bits h of x
-    const __nv_bfloat16 v = __float2bfloat16_rn(rs.value(__uint_as_float(h << 16)));
-    return static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(&v));
-  };
-  for (int i = threadIdx.x; i < kLutSlots; i += 32 * kConsumerWarps) {
-    const uint32_t t = i & (kLutSignStride - 1), neg = static_cast<uint32_t>(i) >> 11;
-    ty[i] = static_cast<uint16_t>(yval((lut_base + t) | (neg << 15)));
-  }
-  asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps) : "memory");
-  int sr[kVPT], so[kVPT];
-  int64_t goff[kVPT];
-  const int svecs = geo.RS * geo.V;
-#pragma unroll
-  for (int j = 0; j < kVPT; ++j) {
-    const int k = threadIdx.x + j * 32 * kConsumerWarps;
-    const int r = k / geo.V, c = k - (k / geo.V) * geo.V;
-    sr[j] = k < svecs ? r : 0x7fffffff;
-    so[j] = r * geo.dg + c * 8;
-    goff[j] = (int64_t)r * geo.d + (int64_t)g * geo.dg + c * 8;
-  }
-  Checker<float> chk;
-  const int nst = (nr + geo.RS - 1) / geo.RS;
-  int slot = 0;
-  uint32_t phase = 0;
-  for (int s = 0; s < nst; ++s) {
-    mbar_wait(&full[slot], phase);
-    const int rows_here = min(geo.RS, nr - s * geo.RS);
-    const T* xs = sx + (size_t)slot * geo.RS * geo.dg;
-    T* ys = y + (row0 + (int64_t)s * geo.RS) * geo.d;
-    uint4 rx[kVPT];
-#pragma unroll
-    for (int j = 0; j < kVPT; ++j)
-      if (sr[j] < rows_here) rx[j] = *reinterpret_cast<const uint4*>(xs + so[j]);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);
-#pragma unroll
-    for (int j = 0; j < kVPT; ++j) {
-      if (sr[j] < rows_here) {
-        const uint32_t wx[4] = {rx[j].x, rx[j].y, rx[j].z, rx[j].w};
-        uint32_t sl[4], bad = 0, wy[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) sl[i] = lut_slots2(wx[i], lut_c, bad);
-        if (__builtin_expect(bad == 0, 1)) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            wy[i] = static_cast<uint32_t>(ty[sl[i] & 0xffffu]) | (static_cast<uint32_t>(ty[sl[i] >> 16]) << 16);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            uint32_t o[2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const uint32_t h = e ? (wx[i] >> 16) : (wx[i] & 0xffffu);
-              const uint32_t t = (h & 0x7fffu) - lut_base;
-              o[e] = t < static_cast<uint32_t>(kLutSignStride) ? static_cast<uint32_t>(ty[t | ((h >> 4) & 0x800u)])
-                                                              : yval(h);
-            }
-            wy[i] = o[0] | (o[1] << 16);
-          }
-        }
-        if constexpr (CHECK) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            chk.add(__uint_as_float(wx[i] << 16));
-            chk.add(__uint_as_float(wx[i] & 0xffff0000u));
-          }
-        }
-        __stcs(reinterpret_cast<uint4*>(ys + goff[j]), make_uint4(wy[0], wy[1], wy[2], wy[3]));
       }
     }
     if (++slot == stages) {

@@ -1,6 +1,7 @@
 // grkan_types.h -- plain types shared by the host launch code and the kernels.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -29,6 +30,9 @@ struct Geom {
   // exponent window [lut_e0, lut_e0 + lut_ne) (biased fp32/bf16 exponents)
   int32_t lut_e0;
   int32_t lut_ne;   // 0: no table
+  // staged kernels: rows per 2-D TMA box (tensor-map copies of RS-row stages,
+  // RS / tma_rows boxes per tensor); 0: one bulk copy per row segment
+  int32_t tma_rows;
   // instrumented launches only (grkan_bwd_instrumented; null otherwise): per-element
   // visit counts [rows * d] and element-access tallies {reads, writes, rmw}
   int32_t* cov;
@@ -105,14 +109,11 @@ struct Plan {
 #ifndef GRKAN_LUT
 #define GRKAN_LUT 1               // bf16 FAST backward: per-CTA table of the x-only factors
 #endif
-#ifndef GRKAN_FWD_LUT
-#define GRKAN_FWD_LUT 1           // bf16 forward from a per-CTA table of y (k_fwd_lut)
+#ifndef GRKAN_TMA2D_MAX_ROW_BYTES
+#define GRKAN_TMA2D_MAX_ROW_BYTES 512  // staged backward: tensor-map stage copies for row segments up to this size
 #endif
-#ifndef GRKAN_FWD_LUT_CTAS
-#define GRKAN_FWD_LUT_CTAS 2      // k_fwd_lut CTAs per SM
-#endif
-#ifndef GRKAN_FWD_LUT_STAGES
-#define GRKAN_FWD_LUT_STAGES 8    // k_fwd_lut ring depth (kStageVecs vectors per stage)
+#ifndef GRKAN_TMA2D_MAX_ROW_BYTES_FWD
+#define GRKAN_TMA2D_MAX_ROW_BYTES_FWD 128  // staged forward: the same, smaller stages
 #endif
 #ifndef GRKAN_WAIT_HINT_NS
 #define GRKAN_WAIT_HINT_NS 1000000  // staged ring waits: mbarrier.try_wait suspend-time hint (0: none)
@@ -153,6 +154,7 @@ struct LaunchArgs {
   bool partials_only;  // backward: K2 only (deterministic multi-GPU path)
   bool instr;          // backward: the instrumented instantiations (coverage + access counts)
   void* y2;            // backward: also write the forward value here (fused step; staged plans only)
+  CUtensorMap tmx, tmu;  // staged plans with geo.tma_rows > 0: x and dy as [rows, d] tiled maps
   cudaStream_t stream;
 };
 

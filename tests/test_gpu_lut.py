@@ -103,43 +103,3 @@ def test_table_path_nonfinite_inputs_propagate_and_are_flagged():
     with pytest.raises(NonFiniteInputError):
         ops().rational_backward(xb.to(DEV), ub.to(DEV), a, b, check_finite=True)
 
-
-def _fwd(xb, num, den, exact, fwd_lut):
-    old = os.environ.get("GRKAN_FWD_LUT")
-    os.environ["GRKAN_FWD_LUT"] = "1" if fwd_lut else "0"
-    try:
-        a = torch.from_numpy(num.astype(np.float32)).to(DEV)
-        b = torch.from_numpy(den.astype(np.float32)).to(DEV)
-        y = ops().rational_forward(xb.to(DEV), a, b, exact=exact)
-        torch.cuda.synchronize()
-        return y.cpu()
-    finally:
-        if old is None:
-            del os.environ["GRKAN_FWD_LUT"]
-        else:
-            os.environ["GRKAN_FWD_LUT"] = old
-
-
-@pytest.mark.parametrize("shape,groups", [((12, 197, 3072), 8), ((6, 33, 192), 8), ((6, 17, 64), 1)])
-def test_forward_table_is_bitwise_the_reference_in_both_policies(shape, groups):
-    """The y table holds bf16_rn of the reference's fp32 value (rational.py:218-224) for every
-    x in the window, the inline fallback the same outside it: FAST and EXACT forward are both
-    bitwise the reference's, at every scale band, and equal the FP32-math EXACT kernel."""
-    xb, _, num, den = _inputs(*shape, groups, seed=14)
-    y_ref = torch.from_numpy(c_oracle.forward(xb.float().numpy(), num, den)).bfloat16()
-    for exact in (False, True):
-        assert torch.equal(_fwd(xb, num, den, exact, fwd_lut=True), y_ref), exact
-    assert torch.equal(_fwd(xb, num, den, True, fwd_lut=False), y_ref)
-
-
-def test_forward_table_nonfinite_and_checked_mode():
-    from paper_2505_13813_b200.errors import NonFiniteInputError
-    xb, _, num, den = _inputs(2, 9, 3072, 8, seed=15)
-    xb[0, 1, 7] = float("nan")
-    xb[1, 2, 9] = float("-inf")
-    a = torch.from_numpy(num.astype(np.float32)).to(DEV)
-    b = torch.from_numpy(den.astype(np.float32)).to(DEV)
-    y = ops().rational_forward(xb.to(DEV), a, b)
-    assert torch.isnan(y[0, 1, 7]) and torch.isfinite(y[0, 0]).all()
-    with pytest.raises(NonFiniteInputError):
-        ops().rational_forward(xb.to(DEV), a, b, check_finite=True)

@@ -1,10 +1,20 @@
+# Tensor-map stage copies (short row segments) and the bf16 y table: tests + A/B lines.
 TAG=${1:-r2g}
 mkdir -p gpurun_out
-./tools/micro/ffma2_ops > gpurun_out/ffma2_ops_${TAG}.txt 2>&1; cat gpurun_out/ffma2_ops_${TAG}.txt
-for v in default v6s2 v6s2probe w12v1 w24v1; do
-  if [ "$v" = default ]; then L=""; else L="GRKAN_LIB=tools/variants/$v/libgrkan_b200.so"; fi
-  for cfg in kat-b kat-s; do for dt in bf16 fp32; do
-    env $L timeout 300 python bench.py --config $cfg --steps 30 --warmup 5 --dtype $dt --no-cpu-baseline --e2e-steps 1 > /tmp/vb.json 2>/tmp/vb.err
-    python -c "import json; d=json.load(open('/tmp/vb.json')); k=d['kernels']; print('$v $cfg $dt', 'bwd=%.1fus(%.3f)'%(k['bwd_us'],k['bwd_frac']), 'fwd=%.1fus(%.3f)'%(k['fwd_us'],k['fwd_frac']), d['clocks']['sm_mhz'], d['clocks']['reasons'])" || tail -3 /tmp/vb.err
-  done; done
-done
+timeout 1200 python -m pytest -q -m gpu tests/test_gpu_tma.py tests/test_gpu_lut.py tests/test_gpu_parity.py tests/test_gpu_deterministic.py tests/test_gpu_api.py > gpurun_out/pytest_${TAG}.txt 2>&1; tail -3 gpurun_out/pytest_${TAG}.txt
+one() {  # env cfg dtype extra
+  env $1 timeout 300 python bench.py --config $2 --dtype $3 --steps 50 --no-cpu-baseline --e2e-steps 1 $4 > /tmp/ab.json 2>/tmp/ab.err
+  python -c "import json; d=json.load(open('/tmp/ab.json')); k=d['kernels']; print('$1 $2 $3 $4 fwd %.1f (%.3f) bwd %.1f (%.3f) value %.3e step %.3f' % (k['fwd_us'], k['fwd_frac'], k['bwd_us'], k['bwd_frac'], d['value'], d['hbm_gbs']/d['roofline']['peak']), d['clocks']['sm_mhz'], d['clocks']['reasons'])" || tail -3 /tmp/ab.err
+}
+for t in 1 0; do
+  one GRKAN_TMA2D=$t kat-s fp32
+  one GRKAN_TMA2D=$t kat-s bf16
+  one GRKAN_TMA2D=$t kat-b fp32 "--groups 16"
+  one GRKAN_TMA2D=$t kat-b bf16 "--groups 16"
+  one GRKAN_TMA2D=$t kat-b fp32 "--groups 64"
+  one GRKAN_TMA2D=$t kat-b bf16 "--groups 64"
+done 2>&1 | tee gpurun_out/ab_${TAG}_tma.txt
+for f in 1 0; do
+  one GRKAN_FWD_LUT=$f kat-b bf16
+  one GRKAN_FWD_LUT=$f kat-s bf16
+done 2>&1 | tee gpurun_out/ab_${TAG}_fwdlut.txt
