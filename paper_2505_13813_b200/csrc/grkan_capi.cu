@@ -156,13 +156,28 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
         p.geo.lut_e0 = GRKAN_LUT_TOP - 15;  // <= 128: the slot arithmetic needs base <= 0x4000
       }
     }
-    // (measured: the backward gains from boxes up to 384-byte rows and loses at
-    // 768; the forward's smaller stages only below ~100-byte rows)
-    if (tma2d_enabled() && dg <= 256 &&
-        static_cast<size_t>(dg) * es <= (nt == 2 ? GRKAN_TMA2D_MAX_ROW_BYTES : GRKAN_TMA2D_MAX_ROW_BYTES_FWD) &&
-        (static_cast<size_t>(RS) * dg * es) % 128 == 0 && rows < (int64_t{1} << 31)) {
-      const int nbox = (RS + 255) / 256;  // box dimensions are <= 256
-      if (RS % nbox == 0) p.geo.tma_rows = RS / nbox;
+    // Tensor-map stage copies (measured: the backward gains from boxes up to
+    // 384-byte rows and, fp32, loses at 768; the bf16 backward is issue-bound and
+    // gains at any length; the forward's small stages only below ~100-byte rows).
+    // Box inner extent: the largest 16-byte-multiple divisor of dg that is <= 256.
+    {
+      int ci = 0;
+      for (int c = dg < 256 ? dg : 256; c >= 1; --c)
+        if (dg % c == 0 && (static_cast<size_t>(c) * es) % 16 == 0) {
+          ci = c;
+          break;
+        }
+      const size_t row_bytes = static_cast<size_t>(dg) * es;
+      const bool want = nt == 2 ? (row_bytes <= GRKAN_TMA2D_MAX_ROW_BYTES || (es == 2 && GRKAN_TMA_BF16_BWD))
+                                : row_bytes <= GRKAN_TMA2D_MAX_ROW_BYTES_FWD;
+      if (tma2d_enabled() && want && ci > 0 && (static_cast<size_t>(RS) * dg * es) % 128 == 0 &&
+          rows < (int64_t{1} << 31)) {
+        const int nbox = (RS + 255) / 256;  // box dimensions are <= 256
+        if (RS % nbox == 0) {
+          p.geo.tma_rows = RS / nbox;
+          p.geo.tma_ci = ci;
+        }
+      }
     }
     const int occ_regs = nt == 2 ? grkan::kBwdCtasPerSmHost : grkan::kFwdCtasPerSmHost;
     int occ = static_cast<int>(kSmemPerSm / (p.smem + 2048));
@@ -227,9 +242,9 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
   return p;
 }
 
-// The [rows, d] tiled maps of x and dy for a plan with geo.tma_rows > 0 (boxes of
-// tma_rows rows x one group's columns); on any encode failure the plan falls
-// back to per-row copies.
+// The tiled maps of x and dy for a plan with geo.tma_rows > 0: [rows, d] viewed
+// as [rows, d / ci, ci], boxes of tma_rows rows x one group's dg / ci chunks; on
+// any encode failure the plan falls back to per-row copies.
 void attach_maps(Plan& p, grkan::LaunchArgs& L, const void* x, const void* u, int32_t dtype) {
   if (p.geo.tma_rows <= 0) return;
   auto fn = grkan::encode_fn();
@@ -237,13 +252,16 @@ void attach_maps(Plan& p, grkan::LaunchArgs& L, const void* x, const void* u, in
   const CUtensorMapDataType ty = dtype == GRKAN_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                  : dtype == GRKAN_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                                        : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.geo.d), static_cast<cuuint64_t>(p.geo.rows)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.geo.d) * es};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(p.geo.dg), static_cast<cuuint32_t>(p.geo.tma_rows)};
-  const cuuint32_t estr[2] = {1, 1};
+  const int ci = p.geo.tma_ci;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(ci), static_cast<cuuint64_t>(p.geo.d / ci),
+                              static_cast<cuuint64_t>(p.geo.rows)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ci) * es, static_cast<cuuint64_t>(p.geo.d) * es};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(ci), static_cast<cuuint32_t>(p.geo.dg / ci),
+                             static_cast<cuuint32_t>(p.geo.tma_rows)};
+  const cuuint32_t estr[3] = {1, 1, 1};
   auto enc = [&](CUtensorMap* m, const void* base) {
     return fn && base &&
-           fn(m, ty, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           fn(m, ty, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   };

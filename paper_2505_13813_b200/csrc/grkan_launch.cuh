@@ -17,23 +17,48 @@ constexpr int kGenM1 = 12, kGenN = 12; // GRKAN_MAX_M1 / GRKAN_MAX_N
 template <typename T>
 constexpr int vec_width() { return static_cast<int>(16 / sizeof(T)); }
 
-// Calls f(bool_constant<EXACT>, bool_constant<FIXED>, int_constant<W>, bool_constant<CHECK>).
+// Degree shapes of the register-direct kernels: 0 = the paper's (5, 4) at
+// compile time; C = 4, 8, 12 = run-time degrees up to capacity C for both
+// polynomials (the generic Horner evaluates all C steps with uniform selects,
+// so a small capacity is several times cheaper than the 12/12 maximum).
+template <int S>
+struct Deg {
+  static constexpr bool FX = S == 0;
+  static constexpr int M1 = S == 0 ? kFixM1 : S;
+  static constexpr int N = S == 0 ? kFixN : S;
+};
+
+inline int deg_shape(const LaunchArgs& L) {
+  if (L.m1 == kFixM1 && L.n == kFixN) return 0;
+  const int c = L.m1 > L.n ? L.m1 : L.n;
+  return c <= 4 ? 4 : (c <= 8 ? 8 : kGenM1);
+}
+
+template <typename F>
+cudaError_t with_shape(int s, F&& f) {
+  switch (s) {
+    case 0: return f(std::integral_constant<int, 0>{});
+    case 4: return f(std::integral_constant<int, 4>{});
+    case 8: return f(std::integral_constant<int, 8>{});
+    default: return f(std::integral_constant<int, kGenM1>{});
+  }
+}
+
+// Calls f(bool_constant<EXACT>, int_constant<degree shape>, int_constant<W>, bool_constant<CHECK>).
 template <typename T, typename F>
-cudaError_t dispatch(const LaunchArgs& L, bool fixed, F&& f) {
-  auto w = [&](auto e, auto fx, auto ck) -> cudaError_t {
-    if (L.vec) return f(e, fx, std::integral_constant<int, vec_width<T>()>{}, ck);
-    return f(e, fx, std::integral_constant<int, 1>{}, ck);
+cudaError_t dispatch(const LaunchArgs& L, F&& f) {
+  auto w = [&](auto e, auto sh, auto ck) -> cudaError_t {
+    if (L.vec) return f(e, sh, std::integral_constant<int, vec_width<T>()>{}, ck);
+    return f(e, sh, std::integral_constant<int, 1>{}, ck);
   };
-  auto c = [&](auto e, auto fx) -> cudaError_t {
-    return L.check ? w(e, fx, std::true_type{}) : w(e, fx, std::false_type{});
+  auto c = [&](auto e, auto sh) -> cudaError_t {
+    return L.check ? w(e, sh, std::true_type{}) : w(e, sh, std::false_type{});
   };
   auto x = [&](auto e) -> cudaError_t {
-    return fixed ? c(e, std::true_type{}) : c(e, std::false_type{});
+    return with_shape(deg_shape(L), [&](auto sh) { return c(e, sh); });
   };
   return L.exact ? x(std::true_type{}) : x(std::false_type{});
 }
-
-inline bool is_fixed(const LaunchArgs& L) { return L.m1 == kFixM1 && L.n == kFixN; }
 
 // Opt a kernel into its dynamic shared memory size (static + dynamic > 48 KB
 // needs the attribute).  The attribute is per device: one cache per kernel
@@ -78,9 +103,9 @@ cudaError_t launch_fwd_t(const LaunchArgs& L) {
       return cudaGetLastError();
     });
   }
-  return dispatch<T>(L, is_fixed(L), [&](auto e, auto fx, auto wc, auto ck) -> cudaError_t {
-    constexpr bool FX = decltype(fx)::value;
-    k_fwd<T, decltype(e)::value, FX ? kFixM1 : kGenM1, FX ? kFixN : kGenN, FX, decltype(wc)::value,
+  return dispatch<T>(L, [&](auto e, auto sh, auto wc, auto ck) -> cudaError_t {
+    using DG = Deg<decltype(sh)::value>;
+    k_fwd<T, decltype(e)::value, DG::M1, DG::N, DG::FX, decltype(wc)::value,
           decltype(ck)::value><<<static_cast<unsigned>(p.ctas), kBlock, 0, L.stream>>>(
         static_cast<const T*>(L.x), static_cast<T*>(L.out), static_cast<const A*>(L.a),
         static_cast<const A*>(L.b), p.geo, L.m1, L.n, L.st);
@@ -110,20 +135,20 @@ cudaError_t launch_bwd_t(const LaunchArgs& L) {
             L.st, L.tmx, L.tmu);
         return cudaGetLastError();
       }
-      auto fw = [&](auto fx, auto wc) -> cudaError_t {
-        constexpr bool FX = decltype(fx)::value;
-        k_bwd_main<T, decltype(e)::value, FX ? kFixM1 : kGenM1, FX ? kFixN : kGenN, FX, decltype(wc)::value,
+      auto fw = [&](auto sh, auto wc) -> cudaError_t {
+        using DG = Deg<decltype(sh)::value>;
+        k_bwd_main<T, decltype(e)::value, DG::M1, DG::N, DG::FX, decltype(wc)::value,
                    false, true><<<static_cast<unsigned>(p.ctas), kBlock, 0, L.stream>>>(
             static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out),
             static_cast<const A*>(L.a), static_cast<const A*>(L.b), static_cast<A*>(L.part), p.geo, L.m1, L.n,
             L.st);
         return cudaGetLastError();
       };
-      auto w = [&](auto fx) -> cudaError_t {
-        if (L.vec) return fw(fx, std::integral_constant<int, vec_width<T>()>{});
-        return fw(fx, std::integral_constant<int, 1>{});
+      auto w = [&](auto sh) -> cudaError_t {
+        if (L.vec) return fw(sh, std::integral_constant<int, vec_width<T>()>{});
+        return fw(sh, std::integral_constant<int, 1>{});
       };
-      return is_fixed(L) ? w(std::true_type{}) : w(std::false_type{});
+      return with_shape(deg_shape(L), w);
     };
     e0 = L.exact ? ex(std::true_type{}) : ex(std::false_type{});
     if (e0 != cudaSuccess) return e0;
@@ -151,9 +176,9 @@ cudaError_t launch_bwd_t(const LaunchArgs& L) {
       }
       return p.geo.det ? go(std::true_type{}, no, no) : go(no, no, no);
     });
-  } else e0 = dispatch<T>(L, is_fixed(L), [&](auto e, auto fx, auto wc, auto ck) -> cudaError_t {
-    constexpr bool FX = decltype(fx)::value;
-    k_bwd_main<T, decltype(e)::value, FX ? kFixM1 : kGenM1, FX ? kFixN : kGenN, FX,
+  } else e0 = dispatch<T>(L, [&](auto e, auto sh, auto wc, auto ck) -> cudaError_t {
+    using DG = Deg<decltype(sh)::value>;
+    k_bwd_main<T, decltype(e)::value, DG::M1, DG::N, DG::FX,
                decltype(wc)::value, decltype(ck)::value>
         <<<static_cast<unsigned>(p.ctas), kBlock, 0, L.stream>>>(
             static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out),
@@ -192,10 +217,10 @@ cudaError_t launch_atomic_t(const LaunchArgs& L) {
   const Plan& p = *L.plan;
   LaunchArgs L2 = L;
   L2.check = false;
-  cudaError_t e0 = dispatch<T>(L2, is_fixed(L), [&](auto e, auto fx, auto wc, auto) -> cudaError_t {
-    constexpr bool FX = decltype(fx)::value;
+  cudaError_t e0 = dispatch<T>(L2, [&](auto e, auto sh, auto wc, auto) -> cudaError_t {
+    using DG = Deg<decltype(sh)::value>;
     auto go = [&](auto ins) -> cudaError_t {
-      k_bwd_atomic<T, decltype(e)::value, FX ? kFixM1 : kGenM1, FX ? kFixN : kGenN, FX, decltype(wc)::value,
+      k_bwd_atomic<T, decltype(e)::value, DG::M1, DG::N, DG::FX, decltype(wc)::value,
                    decltype(ins)::value><<<static_cast<unsigned>(p.ctas), kBlock, 0, L.stream>>>(
           static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out),
           static_cast<const A*>(L.a), static_cast<const A*>(L.b), static_cast<A*>(L.da),

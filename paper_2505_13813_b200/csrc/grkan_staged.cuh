@@ -96,13 +96,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
-// 2-D tiled tensor copy (TMA): box at (c0 = column, c1 = row) of a [rows, d] map.
-__device__ __forceinline__ void tma2d_g2s(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+// 3-D tiled tensor copy (TMA): box at (c0, c1 = column chunk, c2 = row) of a
+// [rows, d / ci, ci] map.
+__device__ __forceinline__ void tma3d_g2s(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
                                           uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(
           smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
 __device__ __forceinline__ uint64_t evict_first_policy() {
@@ -272,7 +273,7 @@ __device__ __forceinline__ void block_store(A* __restrict__ sacc, A (&red)[2][kC
 // ---------------------------------------------------------------------------
 // Producer: lane 0 of the last warp fills the ring, one bulk copy per row
 // segment per tensor -- or, with geo.tma_rows > 0 (short row segments, where
-// per-row copies cost more than they move), RS / tma_rows 2-D tensor-map boxes
+// per-row copies cost more than they move), RS / tma_rows tensor-map boxes
 // per tensor (full boxes: rows past the tensor end arrive zero-filled, rows past
 // the CTA's run are read and ignored).  `nt` tensors (1 forward, 2 backward).
 // ---------------------------------------------------------------------------
@@ -294,7 +295,7 @@ __device__ __forceinline__ void produce(const T* const (&src)[NT], T* const (&ri
       for (int r = 0; r < RS; r += tr) {
 #pragma unroll
         for (int t = 0; t < NT; ++t)
-          tma2d_g2s(ring[t] + ((size_t)slot * RS + r) * geo.dg, maps[t], g * geo.dg,
+          tma3d_g2s(ring[t] + ((size_t)slot * RS + r) * geo.dg, maps[t], 0, g * (geo.dg / geo.tma_ci),
                     static_cast<int>(row0 + (int64_t)s * RS + r), &full[slot], policy);
       }
     } else {

@@ -30,9 +30,11 @@ struct Geom {
   // exponent window [lut_e0, lut_e0 + lut_ne) (biased fp32/bf16 exponents)
   int32_t lut_e0;
   int32_t lut_ne;   // 0: no table
-  // staged kernels: rows per 2-D TMA box (tensor-map copies of RS-row stages,
-  // RS / tma_rows boxes per tensor); 0: one bulk copy per row segment
+  // staged kernels: rows per TMA box (tensor-map copies of RS-row stages,
+  // RS / tma_rows boxes per tensor); 0: one bulk copy per row segment.  The map
+  // views [rows, d] as [rows, d / tma_ci, tma_ci] (box inner extent <= 256).
   int32_t tma_rows;
+  int32_t tma_ci;
   // instrumented launches only (grkan_bwd_instrumented; null otherwise): per-element
   // visit counts [rows * d] and element-access tallies {reads, writes, rmw}
   int32_t* cov;
@@ -112,6 +114,9 @@ struct Plan {
 #ifndef GRKAN_TMA2D_MAX_ROW_BYTES
 #define GRKAN_TMA2D_MAX_ROW_BYTES 512  // staged backward: tensor-map stage copies for row segments up to this size
 #endif
+#ifndef GRKAN_TMA_BF16_BWD
+#define GRKAN_TMA_BF16_BWD 1      // bf16 backward (issue-bound): tensor-map stage copies at any row length
+#endif
 #ifndef GRKAN_TMA2D_MAX_ROW_BYTES_FWD
 #define GRKAN_TMA2D_MAX_ROW_BYTES_FWD 128  // staged forward: the same, smaller stages
 #endif
@@ -154,7 +159,7 @@ struct LaunchArgs {
   bool partials_only;  // backward: K2 only (deterministic multi-GPU path)
   bool instr;          // backward: the instrumented instantiations (coverage + access counts)
   void* y2;            // backward: also write the forward value here (fused step; staged plans only)
-  CUtensorMap tmx, tmu;  // staged plans with geo.tma_rows > 0: x and dy as [rows, d] tiled maps
+  CUtensorMap tmx, tmu;  // staged plans with geo.tma_rows > 0: x and dy as tiled maps
   cudaStream_t stream;
 };
 

@@ -1,4 +1,5 @@
-"""Staged kernels with tensor-map stage copies (short row segments, geo.tma_rows > 0).
+"""Staged kernels with tensor-map stage copies (geo.tma_rows > 0: short row segments,
+and the bf16 backward at any row length, boxes of up to 256-column chunks).
 
 How a stage reaches shared memory must not change a single bit: every output
 of the forward, backward, fused step and deterministic partials path is
@@ -41,7 +42,7 @@ def _with_env(name, value, fn):
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("rows,d,groups", [(3001, 768, 16), (777, 3072, 64), (1000, 192, 8), (513, 1536, 8),
-                                           (4099, 256, 1), (37, 128, 8)])
+                                           (4099, 256, 1), (37, 128, 8), (1003, 3072, 8), (300, 1536, 1)])
 def test_tensor_map_copies_are_bitwise_the_row_copies(dtype, rows, d, groups):
     g = torch.Generator(device="cpu").manual_seed(rows + d)
     x = torch.randn(rows, d, generator=g).to(dtype).to(DEV)

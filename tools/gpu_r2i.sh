@@ -1,9 +1,18 @@
+# Generic degrees by capacity bucket; KAT-S lines on the current build.
 TAG=${1:-r2i}
 mkdir -p gpurun_out
-timeout 900 python -m pytest -q -m gpu tests/test_gpu_fused_step.py tests/test_gpu_parity.py tests/test_gpu_api.py > gpurun_out/pytest_${TAG}.txt 2>&1; tail -5 gpurun_out/pytest_${TAG}.txt
-for cfg in kat-b kat-s; do for dt in fp32 bf16; do
-  timeout 300 python bench.py --config $cfg --dtype $dt --steps 30 --warmup 5 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_${TAG}_${cfg}_${dt}.json 2>/dev/null
-  python -c "import json; d=json.load(open('gpurun_out/bench_${TAG}_${cfg}_${dt}.json')); k=d['kernels']; f=k['fused_step']; print('$cfg $dt two-pass %.1f Gel/s (%.3f of HBM, fwd %.1f bwd %.1f us) | fused %.1f us %.1f Gel/s frac(4sE) %.3f frac(5sE) %.3f' % (d['value']/1e9, d['hbm_gbs']/d['roofline']['peak'], k['fwd_us'], k['bwd_us'], f['us'], f['elements_per_s']/1e9, f['frac'], f['gbs_fwd_plus_bwd_bytes']/d['roofline']['peak']), d['clocks']['sm_mhz'], d['clocks']['reasons'])"
-  timeout 300 python bench.py --config $cfg --dtype $dt --fused-step --steps 30 --warmup 5 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_${TAG}_${cfg}_${dt}_fused.json 2>gpurun_out/bench_${TAG}_fused.err
-  python -c "import json; d=json.load(open('gpurun_out/bench_${TAG}_${cfg}_${dt}_fused.json')); print('$cfg $dt --fused-step value %.1f Gel/s ms %.4f roofline %.3f' % (d['value']/1e9, d['ms_per_step'], d['roofline']['frac']))" || tail -3 gpurun_out/bench_${TAG}_fused.err
-done; done
+timeout 1200 python -m pytest -q -m gpu tests/test_gpu_parity.py tests/test_gpu_api.py tests/test_gpu_lut.py tests/test_gpu_tma.py > gpurun_out/pytest_${TAG}.txt 2>&1; tail -3 gpurun_out/pytest_${TAG}.txt
+one() {  # env cfg dtype extra
+  env $1 timeout 300 python bench.py --config $2 --dtype $3 --steps 50 --no-cpu-baseline --e2e-steps 1 $4 > /tmp/ab.json 2>/tmp/ab.err
+  python -c "import json; d=json.load(open('/tmp/ab.json')); k=d['kernels']; print('$1 $2 $3 $4 fwd %.1f (%.3f) bwd %.1f (%.3f) value %.3e step %.3f' % (k['fwd_us'], k['fwd_frac'], k['bwd_us'], k['bwd_frac'], d['value'], d['hbm_gbs']/d['roofline']['peak']), d['clocks']['sm_mhz'], d['clocks']['reasons'])" || tail -3 /tmp/ab.err
+  cp /tmp/ab.json gpurun_out/bench_${TAG}_$2_$3$(echo $4 | tr -d ' -').json 2>/dev/null
+}
+{
+one X=1 kat-b fp32 "--num-coeffs 4 --den-coeffs 2"
+one X=1 kat-b bf16 "--num-coeffs 4 --den-coeffs 2"
+one X=1 kat-b fp32 "--num-coeffs 8 --den-coeffs 7"
+one X=1 kat-s fp32
+one X=1 kat-s bf16
+one GRKAN_LUT=0 kat-s bf16
+one X=1 kat-b bf16
+} 2>&1 | tee gpurun_out/ab_${TAG}.txt
