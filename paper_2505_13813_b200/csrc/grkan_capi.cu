@@ -154,6 +154,7 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
         p.smem = sm;
         p.geo.lut_ne = 16;
         p.geo.lut_e0 = GRKAN_LUT_TOP - 15;  // <= 128: the slot arithmetic needs base <= 0x4000
+        p.geo.lut_c = (0x4000u - (static_cast<uint32_t>(p.geo.lut_e0) << 7)) * 0x10001u;
       }
     }
     // Tensor-map stage copies (measured: the backward gains from boxes up to

@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
     // consumer warps (the producer is already streaming the first stages)
     float* const tiq = reinterpret_cast<float*>(sacc + KC * ((32 * kConsumerWarps) >> (LUT ? 1 : 0)));
     const uint32_t lut_base = static_cast<uint32_t>(geo.lut_e0) << 7;
-    const uint32_t lut_c = (0x4000u - lut_base) * 0x10001u;
+    const uint32_t lut_c = geo.lut_c;  // a kernel parameter: one IADD3 per pair, not an IMAD
     if constexpr (LUT) {
       for (int i = threadIdx.x; i < kLutSlots; i += 32 * kConsumerWarps) {
         const uint32_t t = i & (kLutSignStride - 1), neg = static_cast<uint32_t>(i) >> 11;

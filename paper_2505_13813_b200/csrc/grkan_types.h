@@ -30,6 +30,7 @@ struct Geom {
   // exponent window [lut_e0, lut_e0 + lut_ne) (biased fp32/bf16 exponents)
   int32_t lut_e0;
   int32_t lut_ne;   // 0: no table
+  uint32_t lut_c;   // (0x4000 - (lut_e0 << 7)) * 0x10001: the slot offset of both halves of a bf16 pair
   // staged kernels: rows per TMA box (tensor-map copies of RS-row stages,
   // RS / tma_rows boxes per tensor); 0: one bulk copy per row segment.  The map
   // views [rows, d] as [rows, d / tma_ci, tma_ci] (box inner extent <= 256).
