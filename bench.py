@@ -573,16 +573,27 @@ def run_b200(args, rank, world, local_rank):
         bwd = fused
 
     # warm-up: at least W steps and at least 150 ms of device work (clocks and
-    # memory settled on a fresh box), untimed
+    # memory settled on a fresh box), untimed.  Every step carries a collective,
+    # so every rank must run the same number: the time-based extension is
+    # agreed across ranks (the slowest rank's count) before it runs.
+    def warm(n):
+        for i in range(n):
+            fwd(); bwd(); allreduce()
+            if (i + 1) % 20 == 0:
+                torch.cuda.synchronize()
+        join_comm()
+        torch.cuda.synchronize()
+
+    n_min = max(3, args.warmup)
     t_w = time.perf_counter()
-    n_w = 0
-    while n_w < max(3, args.warmup) or time.perf_counter() - t_w < 0.15:
-        fwd(); bwd(); allreduce()
-        n_w += 1
-        if n_w % 20 == 0:
-            torch.cuda.synchronize()
-    join_comm()
-    torch.cuda.synchronize()
+    warm(n_min)
+    el = time.perf_counter() - t_w
+    extra = 0 if el >= 0.15 else int(math.ceil((0.15 - el) / max(el / n_min, 1e-6)))
+    if world > 1:
+        t_extra = torch.tensor([extra], dtype=torch.int64, device=dev)
+        dist.all_reduce(t_extra, op=dist.ReduceOp.MAX)
+        extra = int(t_extra.item())
+    warm(extra)
     # host cost of enqueueing one step (events included), to size the hold below
     t_h = time.perf_counter()
     for _ in range(4):

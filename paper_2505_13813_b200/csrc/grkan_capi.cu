@@ -128,7 +128,9 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
   p.geo.one = 1.0f;
   p.W = vec ? static_cast<int>(16 / es) : 1;
   const int stage_vecs = nt == 2 ? grkan::kStageVecsHost : grkan::kFwdStageVecsHost;
-  if (vec && m1 == 6 && n == 4 && dg / p.W <= stage_vecs && staged_enabled(nt, es)) {
+  // staged kernels: compile-time degrees (5, 4) (the paper) and (3, 2)
+  const bool staged_deg = (m1 == 6 && n == 4) || (m1 == 4 && n == 2);
+  if (vec && staged_deg && dg / p.W <= stage_vecs && staged_enabled(nt, es)) {
     // TMA-staged persistent kernels (grkan_staged.cuh)
     const int V = dg / p.W;
     const int RS = stage_vecs / V;
@@ -142,7 +144,7 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
     // the table build (~2 us per CTA) and the shallower ring pay off only over
     // long row runs (table v2: faster at KAT-B, 85 stages per CTA, and KAT-S, 21)
     const int64_t stages_per_cta = nsu * RU / RS / (static_cast<int64_t>(sms) * grkan::kBwdCtasPerSmHost / ng + 1);
-    if (nt == 2 && es == 2 && lut && lut_enabled(stages_per_cta)) {
+    if (nt == 2 && es == 2 && lut && m1 == 6 && n == 4 && lut_enabled(stages_per_cta)) {
       // the table (two float arrays over a 16-exponent window) takes a ring
       // stage's place and the accumulator totals go one slot per lane pair, so
       // kBwdCtasPerSm CTAs stay resident

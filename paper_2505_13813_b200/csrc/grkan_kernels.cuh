@@ -136,9 +136,10 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 template <typename T, bool EXACT, int MM1, int MN, bool FIXED, int W>
 struct Engine {
   using A = typename VecIO<T, W>::A;
-  static constexpr bool kPacked =
-      std::is_same<A, float>::value && FIXED && MM1 == 6 && MN == 4 && (W % 2 == 0);
+  static constexpr bool kPacked = std::is_same<A, float>::value && FIXED &&
+                                  ((MM1 == 6 && MN == 4) || (MM1 == 4 && MN == 2)) && (W % 2 == 0);
   using Scalar = Rational<A, EXACT, MM1, MN, FIXED>;
+  using Packed = RationalX2<EXACT, kPacked ? MM1 : 6, kPacked ? MN : 4>;
   static constexpr int KC = MM1 + MN;
   // vectors per tensor per thread per step (backward; = unroll_for_width(W))
   static constexpr int U = W >= 2 ? 2 : 4;
@@ -217,7 +218,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
   const int g = static_cast<int>(bid % geo.ng);
   const int64_t tile = bid / geo.ng;
   typename E::Scalar rs;
-  RationalX2<EXACT> rp;
+  typename E::Packed rp;
   if constexpr (E::kPacked) rp.load(ca, cb, g, geo.one); else rs.load(ca, cb, g, m1, n);
   const int64_t row0 = tile * geo.R;
   const int nr = static_cast<int>(geo.rows - row0 < geo.R ? geo.rows - row0 : geo.R);
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
   const int g = static_cast<int>(bid % geo.ng);
   const int64_t tile = bid / geo.ng;
   typename E::Scalar rs;
-  RationalX2<EXACT> rp;
+  typename E::Packed rp;
   A acc[KC];
   float2 acc2[E::kPacked ? KC : 1];
   if constexpr (E::kPacked) {

@@ -17,19 +17,22 @@ constexpr int kGenM1 = 12, kGenN = 12; // GRKAN_MAX_M1 / GRKAN_MAX_N
 template <typename T>
 constexpr int vec_width() { return static_cast<int>(16 / sizeof(T)); }
 
-// Degree shapes of the register-direct kernels: 0 = the paper's (5, 4) at
-// compile time; C = 4, 8, 12 = run-time degrees up to capacity C for both
-// polynomials (the generic Horner evaluates all C steps with uniform selects,
-// so a small capacity is several times cheaper than the 12/12 maximum).
+// Degree shapes of the register-direct kernels: 0 = the paper's (5, 4) and
+// -1 = (3, 2) (the reference's small test degrees, run_bench --num-coeffs 4
+// --den-coeffs 2) at compile time; C = 4, 8, 12 = run-time degrees up to
+// capacity C for both polynomials (the generic Horner evaluates all C steps
+// with uniform selects, so a small capacity is several times cheaper than the
+// 12/12 maximum).
 template <int S>
 struct Deg {
-  static constexpr bool FX = S == 0;
-  static constexpr int M1 = S == 0 ? kFixM1 : S;
-  static constexpr int N = S == 0 ? kFixN : S;
+  static constexpr bool FX = S <= 0;
+  static constexpr int M1 = S == 0 ? kFixM1 : (S < 0 ? 4 : S);
+  static constexpr int N = S == 0 ? kFixN : (S < 0 ? 2 : S);
 };
 
 inline int deg_shape(const LaunchArgs& L) {
   if (L.m1 == kFixM1 && L.n == kFixN) return 0;
+  if (L.m1 == 4 && L.n == 2) return -1;
   const int c = L.m1 > L.n ? L.m1 : L.n;
   return c <= 4 ? 4 : (c <= 8 ? 8 : kGenM1);
 }
@@ -38,6 +41,7 @@ template <typename F>
 cudaError_t with_shape(int s, F&& f) {
   switch (s) {
     case 0: return f(std::integral_constant<int, 0>{});
+    case -1: return f(std::integral_constant<int, -1>{});
     case 4: return f(std::integral_constant<int, 4>{});
     case 8: return f(std::integral_constant<int, 8>{});
     default: return f(std::integral_constant<int, kGenM1>{});
@@ -80,10 +84,17 @@ cudaError_t allow_smem(size_t bytes) {
   return e;
 }
 
+// Staged kernels: f(bool_constant<EXACT>, bool_constant<CHECK>, int_constant<M1>,
+// int_constant<N>) for the two compile-time degree pairs make_plan stages:
+// the paper's (5, 4) and (3, 2).
 template <typename T, typename F>
 cudaError_t dispatch_staged(const LaunchArgs& L, F&& f) {
+  auto d = [&](auto e, auto ck) -> cudaError_t {
+    if (L.m1 == 4 && L.n == 2) return f(e, ck, std::integral_constant<int, 4>{}, std::integral_constant<int, 2>{});
+    return f(e, ck, std::integral_constant<int, kFixM1>{}, std::integral_constant<int, kFixN>{});
+  };
   auto c = [&](auto e) -> cudaError_t {
-    return L.check ? f(e, std::true_type{}) : f(e, std::false_type{});
+    return L.check ? d(e, std::true_type{}) : d(e, std::false_type{});
   };
   return L.exact ? c(std::true_type{}) : c(std::false_type{});
 }
@@ -93,8 +104,9 @@ cudaError_t launch_fwd_t(const LaunchArgs& L) {
   using A = typename VecIO<T, 1>::A;
   const Plan& p = *L.plan;
   if (p.staged) {
-    return dispatch_staged<T>(L, [&](auto e, auto ck) -> cudaError_t {
-      constexpr auto kern = k_fwd_staged<T, decltype(e)::value, decltype(ck)::value>;
+    return dispatch_staged<T>(L, [&](auto e, auto ck, auto m1, auto n) -> cudaError_t {
+      constexpr auto kern = k_fwd_staged<T, decltype(e)::value, decltype(ck)::value, decltype(m1)::value,
+                                         decltype(n)::value>;
       cudaError_t ae = allow_smem<kern>(p.smem);
       if (ae != cudaSuccess) return ae;
       kern<<<static_cast<unsigned>(p.ctas), kFwdThreads, p.smem, L.stream>>>(
@@ -125,6 +137,16 @@ cudaError_t launch_bwd_t(const LaunchArgs& L) {
   if (L.instr) {
     // the instrumented instantiations: same kernels, counting (unchecked, per-CTA partials)
     auto ex = [&](auto e) -> cudaError_t {
+      if (p.staged && L.m1 == 4) {
+        constexpr auto kern = k_bwd_staged<T, decltype(e)::value, false, false, true, false, false, 4, 2>;
+        cudaError_t ae = allow_smem<kern>(p.smem);
+        if (ae != cudaSuccess) return ae;
+        kern<<<static_cast<unsigned>(p.ctas), kStagedThreads, p.smem, L.stream>>>(
+            static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out), nullptr,
+            static_cast<const A*>(L.a), static_cast<const A*>(L.b), static_cast<A*>(L.part), p.geo, p.stages,
+            L.st, L.tmx, L.tmu);
+        return cudaGetLastError();
+      }
       if (p.staged) {
         constexpr auto kern = k_bwd_staged<T, decltype(e)::value, false, false, true>;
         cudaError_t ae = allow_smem<kern>(p.smem);
@@ -156,10 +178,11 @@ cudaError_t launch_bwd_t(const LaunchArgs& L) {
                               static_cast<A*>(L.da), static_cast<A*>(L.db), L.st, L.stream, p.geo.cnt);
   }
   if (p.staged) {
-    e0 = dispatch_staged<T>(L, [&](auto e, auto ck) -> cudaError_t {
+    e0 = dispatch_staged<T>(L, [&](auto e, auto ck, auto m1, auto n) -> cudaError_t {
       auto go = [&](auto det, auto fwd, auto lut) -> cudaError_t {
         constexpr auto kern = k_bwd_staged<T, decltype(e)::value, decltype(ck)::value, decltype(det)::value, false,
-                                           decltype(fwd)::value, decltype(lut)::value>;
+                                           decltype(fwd)::value, decltype(lut)::value, decltype(m1)::value,
+                                           decltype(n)::value>;
         cudaError_t ae = allow_smem<kern>(p.smem);
         if (ae != cudaSuccess) return ae;
         kern<<<static_cast<unsigned>(p.ctas), kStagedThreads, p.smem, L.stream>>>(
@@ -170,7 +193,8 @@ cudaError_t launch_bwd_t(const LaunchArgs& L) {
       };
       const std::false_type no;
       if (L.y2) return go(no, std::true_type{}, no);  // fused step: per-CTA partials only
-      if constexpr (std::is_same<T, __nv_bfloat16>::value && !decltype(e)::value) {
+      if constexpr (std::is_same<T, __nv_bfloat16>::value && !decltype(e)::value && decltype(m1)::value == kFixM1 &&
+                    decltype(n)::value == kFixN) {
         if (p.geo.lut_ne > 0)  // the x-factor table (make_plan decides; sizes its shared memory)
           return p.geo.det ? go(std::true_type{}, no, std::true_type{}) : go(no, no, std::true_type{});
       }

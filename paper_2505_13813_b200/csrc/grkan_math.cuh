@@ -250,44 +250,53 @@ __device__ __forceinline__ float2 xmad2(float2 a, float2 b, float2 c, float one)
 __device__ __forceinline__ float2 xadd2(float2 a, float2 b, float one) { return fma2(a, bc(one), b); }
 __device__ __forceinline__ float2 xsub2(float2 a, float2 b, float one) { return fma2(b, bc(-one), a); }
 
-template <bool EXACT>
+// M1 numerator / N denominator coefficients: the paper's (6, 4) everywhere it is
+// the default; (4, 2) for the reference's small test degrees.  Every (6, 4)
+// operation sequence is the one the round-1 kernels were verified with.
+template <bool EXACT, int M1 = 6, int N = 4>
 struct RationalX2 {
-  static constexpr int KC = 10;
-  float a[6], b[4], da[5], db[4];
+  static_assert(M1 >= 3 && M1 <= 6 && N >= 2 && N <= 4, "packed engine degrees");
+  static constexpr int KC = M1 + N;
+  static constexpr int PMAX = (M1 - 1 > N ? M1 - 1 : N);  // highest power of x in a term
+  float a[M1], b[N], da[M1 - 1], db[N];
   float one;  // opaque 1.0 (kernel parameter), see xmad2
   int goff;   // sign-guard scale (FAST): see sign_unsafe
 
   __device__ __forceinline__ void load(const float* __restrict__ ga, const float* __restrict__ gb, int g,
                                        float one_param) {
-    float ab[10];
+    float ab[KC];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) ab[k] = __ldg(ga + g * 6 + k);
+    for (int k = 0; k < M1; ++k) ab[k] = __ldg(ga + g * M1 + k);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) ab[6 + k] = __ldg(gb + g * 4 + k);
+    for (int k = 0; k < N; ++k) ab[M1 + k] = __ldg(gb + g * N + k);
     set(ab, one_param);
   }
-  // From one row a_0..a_5 || b_1..b_4 in any memory space (shared-memory tables).
+  // From one row a_0..a_m || b_1..b_n in any memory space (shared-memory tables).
   __device__ __forceinline__ void load_row(const float* ab_row, float one_param) {
-    float ab[10];
+    float ab[KC];
 #pragma unroll
-    for (int k = 0; k < 10; ++k) ab[k] = ab_row[k];
+    for (int k = 0; k < KC; ++k) ab[k] = ab_row[k];
     set(ab, one_param);
   }
-  __device__ __forceinline__ void set(const float (&ab)[10], float one_param) {
+  __device__ __forceinline__ void set(const float (&ab)[KC], float one_param) {
 #pragma unroll
-    for (int k = 0; k < 6; ++k) a[k] = ab[k];
+    for (int k = 0; k < M1; ++k) a[k] = ab[k];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) b[k] = ab[6 + k];
+    for (int k = 0; k < N; ++k) b[k] = ab[M1 + k];
     da[0] = a[1];  // 1 * a_1 is exact
 #pragma unroll
-    for (int k = 2; k < 6; ++k) da[k - 1] = __fmul_rn(a[k], float(k));  // fp32 k*a_k, as rational.py:207
+    for (int k = 2; k < M1; ++k) da[k - 1] = __fmul_rn(a[k], float(k));  // fp32 k*a_k, as rational.py:207
     db[0] = b[0];
 #pragma unroll
-    for (int k = 2; k <= 4; ++k) db[k - 1] = __fmul_rn(b[k - 1], float(k));
+    for (int k = 2; k <= N; ++k) db[k - 1] = __fmul_rn(b[k - 1], float(k));
     one = one_param;
-    // sign_unsafe threshold 2^e >= 2^-17 * (|b1| + |b2| + |b3| + |b4|), as an
-    // exponent offset in float bits; b == 0 (A == 0 exactly) disables it.
-    const float bsum = fabsf(b[0]) + fabsf(b[1]) + fabsf(b[2]) + fabsf(b[3]);
+    // sign_unsafe threshold 2^e >= 2^-17 * (|b1| + ... + |bn|), as an exponent
+    // offset in float bits; b == 0 (A == 0 exactly) disables it.  Derived for
+    // n = 4 (below); for n < 4 the Horner error bound is smaller, so the same
+    // threshold is conservative.
+    float bsum = fabsf(b[0]);
+#pragma unroll
+    for (int k = 1; k < N; ++k) bsum += fabsf(b[k]);
     const int eb = static_cast<int>((__float_as_uint(bsum) >> 23) & 0xff) - 126;  // 2^eb > bsum
     goff = bsum > 0.0f ? (eb - 17) * (1 << 23) : -0x7f000000;
   }
@@ -302,6 +311,7 @@ struct RationalX2 {
   // float bits (ALU pipe); flagged pairs recompute h with the reference's
   // separately rounded steps.  Conservative for tiny or huge |h| (wraps to
   // "unsafe").
+  // xg = x^(n-1) (x^3 at the paper's degrees).
   __device__ __forceinline__ bool sign_unsafe(float h, float x3) const {
     const float m = fmaxf(fabsf(x3), 1.0f);
     return static_cast<int>((__float_as_uint(h) & 0x7fffffffu) - static_cast<uint32_t>(goff)) <
@@ -324,17 +334,17 @@ struct RationalX2 {
 
   // Horner on a pair with scalar (broadcast) coefficients: the reference's
   // separately rounded acc = acc * x + c (ROUNDED) or FMA steps.
-  template <bool ROUNDED, int N>
-  __device__ __forceinline__ float2 horner2(const float (&c)[N], float2 x) const {
+  template <bool ROUNDED, int NC>
+  __device__ __forceinline__ float2 horner2(const float (&c)[NC], float2 x) const {
     float2 acc;
     if (ROUNDED) {
-      acc = bc(c[N - 1]);
+      acc = bc(c[NC - 1]);
 #pragma unroll
-      for (int k = N - 2; k >= 0; --k) acc = xmad2(acc, x, bc(c[k]), one);
+      for (int k = NC - 2; k >= 0; --k) acc = xmad2(acc, x, bc(c[k]), one);
     } else {
-      acc = fma2(bc(c[N - 1]), x, bc(c[N - 2]));
+      acc = fma2(bc(c[NC - 1]), x, bc(c[NC - 2]));
 #pragma unroll
-      for (int k = N - 3; k >= 0; --k) acc = fma2(acc, x, bc(c[k]));
+      for (int k = NC - 3; k >= 0; --k) acc = fma2(acc, x, bc(c[k]));
     }
     return acc;
   }
@@ -352,8 +362,8 @@ struct RationalX2 {
   }
 
   __device__ __forceinline__ float2 value(float2 x) const {
-    const float2 p = horner2<EXACT, 6>(a, x);
-    const float2 s = mul2(horner2<EXACT, 4>(b, x), x);
+    const float2 p = horner2<EXACT, M1>(a, x);
+    const float2 s = mul2(horner2<EXACT, N>(b, x), x);
     const float2 q = q_of(s);
     if (EXACT) return make_float2(__fdiv_rn(p.x, q.x), __fdiv_rn(p.y, q.y));
     return mul2(p, make_float2(rcp(q.x), rcp(q.y)));
@@ -361,12 +371,12 @@ struct RationalX2 {
 
   // FAST: A(x) = h(x) x with h by FMA Horner; `bad` collects sign_unsafe.
   __device__ __forceinline__ float2 series_fast(float2 x, float2 x3, bool& bad) const {
-    const float2 h = horner2<false, 4>(b, x);
+    const float2 h = horner2<false, N>(b, x);
     bad |= sign_unsafe(h.x, x3.x) | sign_unsafe(h.y, x3.y);
     return mul2(h, x);
   }
   // The reference's separately rounded A(x) (EXACT, and FAST's guarded pairs).
-  __device__ __forceinline__ float2 series_ref(float2 x) const { return mul2(horner2<true, 4>(b, x), x); }
+  __device__ __forceinline__ float2 series_ref(float2 x) const { return mul2(horner2<true, N>(b, x), x); }
 
   // dx and the ten coefficient terms of one pair, given A(x) = s.
   // Accumulators: float2 per coefficient (packed FFMA2, the streaming kernels)
@@ -383,11 +393,11 @@ struct RationalX2 {
   template <bool WY = false, typename ACC>
   __device__ __forceinline__ float2 grad_given(float2 x, float2 u, float2 s, float2 x2, float2 x3,
                                                ACC (&acc)[KC], float2* yv = nullptr) const {
-    const float2 p = horner2<EXACT, 6>(a, x);
+    const float2 p = horner2<EXACT, M1>(a, x);
     const float2 q = q_of(s);
     const float2 iq = make_float2(rcp(q.x), rcp(q.y));
-    const float2 dp = horner2<EXACT, 5>(da, x);
-    const float2 ds = horner2<EXACT, 4>(db, x);
+    const float2 dp = horner2<EXACT, M1 - 1>(da, x);
+    const float2 ds = horner2<EXACT, N>(db, x);
     const float2 pq = mul2(p, iq);
     if constexpr (WY) *yv = EXACT ? make_float2(__fdiv_rn(p.x, q.x), __fdiv_rn(p.y, q.y)) : pq;
     float2 dx;
@@ -402,16 +412,16 @@ struct RationalX2 {
       float2 t = mul2(u, iq);
       acc_add(acc[0], t);
 #pragma unroll
-      for (int i = 1; i < 6; ++i) {
+      for (int i = 1; i < M1; ++i) {
         t = mul2(t, x);
         acc_add(acc[i], t);
       }
       float2 v = mul2(mul2(mul2(neg2(mul2(sg, u)), pq), iq), x);
-      acc_add(acc[6], v);
+      acc_add(acc[M1], v);
 #pragma unroll
-      for (int j = 1; j < 4; ++j) {
+      for (int j = 1; j < N; ++j) {
         v = mul2(v, x);
-        acc_add(acc[6 + j], v);
+        acc_add(acc[M1 + j], v);
       }
     } else {
       const float2 t0 = mul2(u, iq);
@@ -419,18 +429,17 @@ struct RationalX2 {
       const float2 z = make_float2(neg_sign_times(s.x, pq.x), neg_sign_times(s.y, pq.y));
       dx = mul2(t0, fma2(ds, z, dp));               // (u/q) (P' - sign(A) A' P/q)
       const float2 w = mul2(t0, z);                 // -(sign(A) u/q) P/q
-      const float2 x4 = mul2(x2, x2);
-      const float2 x5 = mul2(x4, x);
+      float2 pw[PMAX + 1];                          // x^1..x^PMAX: x^4 = x^2 x^2, x^5 = x^4 x
+      pw[1] = x;
+      pw[2] = x2;
+      if constexpr (PMAX >= 3) pw[3] = x3;
+      if constexpr (PMAX >= 4) pw[4] = mul2(x2, x2);
+      if constexpr (PMAX >= 5) pw[5] = mul2(pw[4], x);
       acc_add(acc[0], t0);
-      acc_fma(acc[1], t0, x);
-      acc_fma(acc[2], t0, x2);
-      acc_fma(acc[3], t0, x3);
-      acc_fma(acc[4], t0, x4);
-      acc_fma(acc[5], t0, x5);
-      acc_fma(acc[6], w, x);
-      acc_fma(acc[7], w, x2);
-      acc_fma(acc[8], w, x3);
-      acc_fma(acc[9], w, x4);
+#pragma unroll
+      for (int i = 1; i < M1; ++i) acc_fma(acc[i], t0, pw[i]);
+#pragma unroll
+      for (int j = 0; j < N; ++j) acc_fma(acc[M1 + j], w, pw[j + 1]);
     }
     return dx;
   }
@@ -445,6 +454,7 @@ struct RationalX2 {
   // the reference's separately rounded steps (exact sign(A), rational.py:211-215,
   // 251), P by FMA Horner, 1/Q by IEEE reciprocal.
   __device__ __forceinline__ float2 lut_entry(float x) const {
+    static_assert(M1 == 6 && N == 4, "the bf16 table body is written for the paper's degrees");
     float h = b[3];
 #pragma unroll
     for (int k = 2; k >= 0; --k) h = __fadd_rn(__fmul_rn(h, x), b[k]);
@@ -461,6 +471,7 @@ struct RationalX2 {
   // wq = -sign(A)P/Q^2: 25 packed FP32 ops per pair instead of grad_given's 39, no MUFU.
   template <typename ACC>
   __device__ __forceinline__ float2 grad_lut(float2 x, float2 u, float2 iq, float2 wq, ACC (&acc)[KC]) const {
+    static_assert(M1 == 6 && N == 4, "the bf16 table body is written for the paper's degrees");
     const float2 t0 = mul2(u, iq);  // u/Q
     const float2 w = mul2(u, wq);   // -sign(A) u P/Q^2
     const float2 dp = horner2<false, 5>(da, x);

@@ -341,7 +341,8 @@ __device__ __forceinline__ uint32_t lut_slots2(uint32_t w, uint32_t c, uint32_t&
   return (d & 0x07ff07ffu) | ((d & 0x80008000u) >> 4);
 }
 
-template <typename T, bool EXACT, bool CHECK, bool DET, bool INSTR = false, bool FWD = false, bool LUT = false>
+template <typename T, bool EXACT, bool CHECK, bool DET, bool INSTR = false, bool FWD = false, bool LUT = false,
+          int M1 = 6, int N = 4>
 __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
     k_bwd_staged(const T* __restrict__ x, const T* __restrict__ dy, T* __restrict__ dx, T* __restrict__ y,
                  const typename VecIO<T, 1>::A* __restrict__ ca,
@@ -353,9 +354,9 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
   using RW = Raw16<T>;
   constexpr int W = RW::W;
   constexpr bool PK = std::is_same<A, float>::value;
-  constexpr int KC = 10;
-  static_assert(!LUT || (std::is_same<T, __nv_bfloat16>::value && !EXACT && !INSTR && !FWD),
-                "the x-factor table is the bf16 FAST backward only");
+  constexpr int KC = M1 + N;
+  static_assert(!LUT || (std::is_same<T, __nv_bfloat16>::value && !EXACT && !INSTR && !FWD && M1 == 6 && N == 4),
+                "the x-factor table is the bf16 FAST backward at the paper's degrees only");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ A red[DET ? 2 : 1][DET ? kConsumerWarps : 1][DET ? KC : 1];
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
   }
   if (threadIdx.x < 32 * kConsumerWarps) {
 #pragma unroll
-    for (int k = 0; k < 10; ++k)
+    for (int k = 0; k < KC; ++k)
       if (!LUT || (threadIdx.x & 1) == 0) sacc[acc_slot<LUT ? 1 : 0>(k)] = 0;
   }
   __syncthreads();
@@ -400,15 +401,15 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
       if (!GRKAN_PROBE_NOMEM) produce<T, 2>(src, ring, geo, row0, nr, stages, full, empty, g, maps);
     }
   } else {
-    RationalX2<EXACT> rp;
-    Rational<A, EXACT, 6, 4, true> rs;
+    RationalX2<EXACT, M1, N> rp;
+    Rational<A, EXACT, M1, N, true> rs;
     float2 acc2[KC];
     if constexpr (PK) {
       rp.load(reinterpret_cast<const float*>(ca), reinterpret_cast<const float*>(cb), g, geo.one);
 #pragma unroll
       for (int k = 0; k < KC; ++k) acc2[k] = make_float2(0.f, 0.f);
     } else {
-      rs.load(ca, cb, g, 6, 4);
+      rs.load(ca, cb, g, M1, N);
     }
     // the x-factor table after the accumulator totals: built once by the
     // consumer warps (the producer is already streaming the first stages)
@@ -568,7 +569,7 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
 // ---------------------------------------------------------------------------
 // K1 staged: forward, degrees (5, 4).
 // ---------------------------------------------------------------------------
-template <typename T, bool EXACT, bool CHECK>
+template <typename T, bool EXACT, bool CHECK, int M1 = 6, int N = 4>
 __global__ void __launch_bounds__(kFwdThreads, kFwdCtasPerSm)
     k_fwd_staged(const T* __restrict__ x, T* __restrict__ y, const typename VecIO<T, 1>::A* __restrict__ ca,
                  const typename VecIO<T, 1>::A* __restrict__ cb, Geom geo, int stages,
@@ -603,12 +604,12 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdCtasPerSm)
     }
     return;
   }
-  RationalX2<EXACT> rp;
-  Rational<A, EXACT, 6, 4, true> rs;
+  RationalX2<EXACT, M1, N> rp;
+  Rational<A, EXACT, M1, N, true> rs;
   if constexpr (PK)
     rp.load(reinterpret_cast<const float*>(ca), reinterpret_cast<const float*>(cb), g, geo.one);
   else
-    rs.load(ca, cb, g, 6, 4);
+    rs.load(ca, cb, g, M1, N);
   int sr[kFwdVPT], soff[kFwdVPT];
   int64_t goff[kFwdVPT];
   const int svecs = geo.RS * geo.V;

@@ -103,8 +103,9 @@ def test_plan_geometry(dtype, es):
         ws = N.lib().grkan_bwd_workspace_bytes(rows, d, g, 6, 4, dtype)
         acc = 8 if dtype == N.DT_F64 else 4
         assert ws >= 256 + p["ctas"] * 10 * acc
-        # generic degrees never take the staged path
-        assert not N.plan(rows, d, g, 4, 2, dtype)["staged"]
+        # the staged kernels are compiled for degrees (5, 4) and (3, 2) only
+        assert N.plan(rows, d, g, 4, 2, dtype)["staged"] == p["staged"]
+        assert not N.plan(rows, d, g, 5, 3, dtype)["staged"]
 
 
 def test_kat_b_plan_is_persistent_and_balanced():

@@ -86,7 +86,11 @@ def test_every_element_exactly_once_and_counts_match(shape, groups, m1, n, dtype
     # the counting instantiation computes what the product kernels compute
     plain = g.run_backward(x, up, params, plan, exact=True)
     assert bundle.d_x.data.tobytes() == plain.d_x.data.tobytes()
-    tol = 1e-12 if dtype == np.float64 else 1e-5
+    # The naive strategy is the Alg. 1 comparator: per-element fp32 atomicAdd in
+    # whatever order the SMs arrive, so two runs differ by its own rounding
+    # error (~1e-5 max-scaled at KAT-T; 40K-term sums) -- the inaccuracy the
+    # blocked path exists to remove.  The blocked path is run-to-run exact.
+    tol = 1e-12 if dtype == np.float64 else (1e-4 if naive else 1e-6)
     assert orc.matrix_rel(bundle.d_a, plain.d_a) <= tol and orc.matrix_rel(bundle.d_b, plain.d_b) <= tol
 
 
