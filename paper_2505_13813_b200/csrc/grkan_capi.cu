@@ -109,25 +109,47 @@ bool lut_enabled(int64_t stages_per_cta) {
   return GRKAN_LUT != 0 && stages_per_cta >= kLutMinStagesPerCta;
 }
 
-// Short row segments: the staged producers copy whole stages as 2-D tensor-map
-// boxes instead of one bulk copy per row (GRKAN_TMA2D=0: per-row copies, A/B).
-bool tma2d_enabled() {
+// Short row segments: the staged producers copy whole stages as tensor-map
+// boxes instead of one bulk copy per row (GRKAN_TMA2D=0: per-row copies,
+// =2: boxes at every row length; A/B).
+int tma2d_mode() {
   const char* v = getenv("GRKAN_TMA2D");
-  return !(v && v[0] == '0');
+  if (v && (v[0] == '0' || v[0] == '2')) return v[0] - '0';
+  return 1;
+}
+
+// The wide backward geometry (one CTA of GRKAN_WIDE_WARPS consumer warps per
+// SM, stages twice as large): measured on one B200 at 1965 MHz, KAT-B fp32
+// 308 -> 296 us, bf16 216 -> 208 us, KAT-S bf16 68 -> 66 us, but KAT-S fp32
+// 89 -> 119 us (768-byte rows: its single producer cannot issue the per-row
+// copies fast enough; with tensor-map boxes 92 us).  So: 2-byte I/O, and
+// 4-byte I/O with row segments of at least 1536 bytes.  GRKAN_WIDE=0/1 forces
+// (A/B).  Never for deterministic partials (the geometry must not depend on
+// the shard) or the fused / instrumented instantiations (wide_ok = false).
+bool wide_geometry(size_t es, int dg, bool wide_ok) {
+  if (!wide_ok || es > 4) return false;
+  const char* v = getenv("GRKAN_WIDE");
+  if (v && (v[0] == '0' || v[0] == '1')) return v[0] == '1';
+  return es == 2 || static_cast<size_t>(dg) * es >= 1536;
 }
 
 // nt = tensors streamed in (1 forward, 2 backward).  det: one partial per
 // global RB-row block (slot-major), independent of the launch geometry.
 // lut: the caller runs the bf16 FAST backward (grkan_bwd / grkan_bwd_partials).
+// wide_ok: the caller launches the plain backward (grkan_bwd), which has the
+// wide-geometry instantiations.
 Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_t es, bool vec, int nt,
-               int sms, bool det = false, bool lut = false) {
+               int sms, bool det = false, bool lut = false, bool wide_ok = false) {
   Plan p;
   const int dg = d / ng;
   const int64_t RB = det ? det_rows(d, ng, es) : 0;
   p.geo.det = det ? 1 : 0;
   p.geo.one = 1.0f;
   p.W = vec ? static_cast<int>(16 / es) : 1;
-  const int stage_vecs = nt == 2 ? grkan::kStageVecsHost : grkan::kFwdStageVecsHost;
+  const bool wide = nt == 2 && !det && vec && wide_geometry(es, dg, wide_ok);
+  const int cw = wide ? GRKAN_WIDE_WARPS : grkan::kConsumerWarpsHost;
+  const int ctas_per_sm = wide ? 1 : grkan::kBwdCtasPerSmHost;
+  const int stage_vecs = nt == 2 ? grkan::kStageVecsHost / grkan::kConsumerWarpsHost * cw : grkan::kFwdStageVecsHost;
   // staged kernels: compile-time degrees (5, 4) (the paper) and (3, 2)
   const bool staged_deg = (m1 == 6 && n == 4) || (m1 == 4 && n == 2);
   if (vec && staged_deg && dg / p.W <= stage_vecs && staged_enabled(nt, es)) {
@@ -140,18 +162,18 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
     p.stages = nt == 2 ? kStagesPerTensorPair : kStagesSingle;
     p.smem = static_cast<size_t>(p.stages) * nt * RS * dg * es;
     if (nt == 2)  // + per-lane accumulator totals [10][256] in the accumulation type
-      p.smem += static_cast<size_t>(m1 + n) * 32 * grkan::kConsumerWarpsHost * (es == 8 ? 8 : 4);
+      p.smem += static_cast<size_t>(m1 + n) * 32 * cw * (es == 8 ? 8 : 4);
     // the table build (~2 us per CTA) and the shallower ring pay off only over
     // long row runs (table v2: faster at KAT-B, 85 stages per CTA, and KAT-S, 21)
-    const int64_t stages_per_cta = nsu * RU / RS / (static_cast<int64_t>(sms) * grkan::kBwdCtasPerSmHost / ng + 1);
+    const int64_t stages_per_cta = nsu * RU / RS / (static_cast<int64_t>(sms) * ctas_per_sm / ng + 1);
     if (nt == 2 && es == 2 && lut && m1 == 6 && n == 4 && lut_enabled(stages_per_cta)) {
       // the table (two float arrays over a 16-exponent window) takes a ring
       // stage's place and the accumulator totals go one slot per lane pair, so
       // kBwdCtasPerSm CTAs stay resident
       const size_t ring = static_cast<size_t>(GRKAN_LUT_STAGES) * nt * RS * dg * es;
-      const size_t acc = static_cast<size_t>(m1 + n) * 16 * grkan::kConsumerWarpsHost * 4;
+      const size_t acc = static_cast<size_t>(m1 + n) * 16 * cw * 4;
       const size_t sm = ring + acc + 2 * 2 * grkan::kLutSignStride * sizeof(float);
-      if (kSmemPerSm / (sm + 2048) >= static_cast<size_t>(grkan::kBwdCtasPerSmHost)) {
+      if (kSmemPerSm / (sm + 2048) >= static_cast<size_t>(ctas_per_sm)) {
         p.stages = GRKAN_LUT_STAGES;
         p.smem = sm;
         p.geo.lut_ne = 16;
@@ -171,9 +193,10 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
           break;
         }
       const size_t row_bytes = static_cast<size_t>(dg) * es;
-      const bool want = nt == 2 ? (row_bytes <= GRKAN_TMA2D_MAX_ROW_BYTES || (es == 2 && GRKAN_TMA_BF16_BWD))
-                                : row_bytes <= GRKAN_TMA2D_MAX_ROW_BYTES_FWD;
-      if (tma2d_enabled() && want && ci > 0 && (static_cast<size_t>(RS) * dg * es) % 128 == 0 &&
+      const int mode = tma2d_mode();
+      const bool want = mode == 2 || (nt == 2 ? (row_bytes <= GRKAN_TMA2D_MAX_ROW_BYTES || (es == 2 && GRKAN_TMA_BF16_BWD))
+                                              : row_bytes <= GRKAN_TMA2D_MAX_ROW_BYTES_FWD);
+      if (mode != 0 && want && ci > 0 && (static_cast<size_t>(RS) * dg * es) % 128 == 0 &&
           rows < (int64_t{1} << 31)) {
         const int nbox = (RS + 255) / 256;  // box dimensions are <= 256
         if (RS % nbox == 0) {
@@ -182,14 +205,15 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
         }
       }
     }
-    const int occ_regs = nt == 2 ? grkan::kBwdCtasPerSmHost : grkan::kFwdCtasPerSmHost;
+    const int occ_regs = nt == 2 ? ctas_per_sm : grkan::kFwdCtasPerSmHost;
     int occ = static_cast<int>(kSmemPerSm / (p.smem + 2048));
     occ = occ < 1 ? 1 : (occ > occ_regs ? occ_regs : occ);
     const int64_t slots = static_cast<int64_t>(sms) * occ;
     int64_t pg = slots / ng;
     if (pg > nsu) pg = nsu;
     if (pg < 1) pg = 1;
-    p.threads = nt == 2 ? grkan::kStagedThreadsHost : grkan::kFwdThreadsHost;
+    p.threads = nt == 2 ? 32 * (cw + 1) : grkan::kFwdThreadsHost;
+    p.cw = nt == 2 ? cw : 0;
     p.geo.rows = rows;
     p.geo.d = d;
     p.geo.ng = ng;
@@ -204,7 +228,7 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
     p.geo.spb = static_cast<int32_t>(RU / RS);
     // partials per (group, coefficient) for K3 (backward: one per consumer
     // warp; deterministic: one per RB-row block)
-    p.geo.n_tiles = det ? nsu : (nt == 2 ? pg * grkan::kConsumerWarpsHost : pg);
+    p.geo.n_tiles = det ? nsu : (nt == 2 ? pg * cw : pg);
     p.ctas = rows > 0 ? pg * ng : 0;
     return p;
   }
@@ -394,8 +418,13 @@ size_t grkan_bwd_workspace_bytes(int64_t rows, int32_t d, int32_t n_groups, int3
   // (an SM count no device reaches), which bounds every plan grkan_bwd can pick.
   const int kAnySms = 1 << 20;
   const bool can_vec = vec_ok(d, n_groups, es, {});
-  const size_t a =
-      can_vec ? ws_bytes_for(make_plan(rows, d, n_groups, m1, n, es, true, 2, kAnySms), m1, n, dtype) : 0;
+  size_t a = 0;
+  if (can_vec)  // both staged geometries (make_plan picks the wide one per shape)
+    for (int wide = 0; wide < 2; ++wide) {
+      const size_t w =
+          ws_bytes_for(make_plan(rows, d, n_groups, m1, n, es, true, 2, kAnySms, false, true, wide == 1), m1, n, dtype);
+      a = w > a ? w : a;
+    }
   const size_t b = ws_bytes_for(make_plan(rows, d, n_groups, m1, n, es, false, 2, kAnySms), m1, n, dtype);
   // GRKAN_FLAG_DETERMINISTIC: one partial per global row block
   const size_t c = ws_bytes_for(make_plan(rows, d, n_groups, m1, n, es, false, 2, kAnySms, true), m1, n, dtype);
@@ -462,7 +491,7 @@ int grkan_bwd(const void* x, const void* dy, const void* a, const void* b, void*
   const bool vec = vec_ok(d, n_groups, es, {x, dy, dx});
   const bool det = (flags & GRKAN_FLAG_DETERMINISTIC) != 0;
   Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count(), det,
-                           (flags & GRKAN_FLAG_EXACT) == 0);
+                           (flags & GRKAN_FLAG_EXACT) == 0, true);
   if (!plan_fits(p)) return fail(GRKAN_ERR_GRID, "grid geometry invalid: %lld CTAs", (long long)p.ctas);
   const size_t need = ws_bytes_for(p, m1, n, dtype);
   if (ws_bytes < need)
@@ -498,7 +527,7 @@ int grkan_fwd_bwd(const void* x, const void* dy, const void* a, const void* b, v
   const size_t es = elem_size(dtype);
   const bool det = (flags & GRKAN_FLAG_DETERMINISTIC) != 0;
   const bool vec = vec_ok(d, n_groups, es, {x, dy, dx, y});
-  Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count(), det);
+  Plan p = make_plan(rows, d, n_groups, m1, n, es, vec, 2, sm_count(), det, false, true);
   if (rows == 0 || !p.staged || det) {
     // no fused instantiation for this plan: the two passes back to back (same results)
     // (grkan_bwd's CHECK_FINITE covers x, so the forward runs unchecked)

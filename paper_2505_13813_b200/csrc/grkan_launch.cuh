@@ -179,26 +179,40 @@ cudaError_t launch_bwd_t(const LaunchArgs& L) {
   }
   if (p.staged) {
     e0 = dispatch_staged<T>(L, [&](auto e, auto ck, auto m1, auto n) -> cudaError_t {
-      auto go = [&](auto det, auto fwd, auto lut) -> cudaError_t {
+      auto go = [&](auto det, auto fwd, auto lut, auto cw) -> cudaError_t {
         constexpr auto kern = k_bwd_staged<T, decltype(e)::value, decltype(ck)::value, decltype(det)::value, false,
                                            decltype(fwd)::value, decltype(lut)::value, decltype(m1)::value,
-                                           decltype(n)::value>;
+                                           decltype(n)::value, decltype(cw)::value>;
         cudaError_t ae = allow_smem<kern>(p.smem);
         if (ae != cudaSuccess) return ae;
-        kern<<<static_cast<unsigned>(p.ctas), kStagedThreads, p.smem, L.stream>>>(
+        kern<<<static_cast<unsigned>(p.ctas), staged_threads<decltype(cw)::value>(), p.smem, L.stream>>>(
             static_cast<const T*>(L.x), static_cast<const T*>(L.dy), static_cast<T*>(L.out), static_cast<T*>(L.y2),
             static_cast<const A*>(L.a), static_cast<const A*>(L.b), static_cast<A*>(L.part), p.geo,
             p.stages, L.st, L.tmx, L.tmu);
         return cudaGetLastError();
       };
       const std::false_type no;
-      if (L.y2) return go(no, std::true_type{}, no);  // fused step: per-CTA partials only
-      if constexpr (std::is_same<T, __nv_bfloat16>::value && !decltype(e)::value && decltype(m1)::value == kFixM1 &&
-                    decltype(n)::value == kFixN) {
-        if (p.geo.lut_ne > 0)  // the x-factor table (make_plan decides; sizes its shared memory)
-          return p.geo.det ? go(std::true_type{}, no, std::true_type{}) : go(no, no, std::true_type{});
+      const std::integral_constant<int, kConsumerWarps> cw0;
+      if (L.y2) {  // fused step: per-CTA partials only, the geometry grkan_bwd would pick
+        if constexpr (sizeof(T) <= 4)
+          if (p.cw == kWideWarps) return go(no, std::true_type{}, no, std::integral_constant<int, kWideWarps>{});
+        return go(no, std::true_type{}, no, cw0);
       }
-      return p.geo.det ? go(std::true_type{}, no, no) : go(no, no, no);
+      constexpr bool kPaper = decltype(m1)::value == kFixM1 && decltype(n)::value == kFixN;
+      constexpr bool kLutType = std::is_same<T, __nv_bfloat16>::value && !decltype(e)::value && kPaper;
+      if constexpr (sizeof(T) <= 4) {
+        if (p.cw == kWideWarps && !p.geo.det) {  // the wide geometry (make_plan, grkan_bwd only)
+          const std::integral_constant<int, kWideWarps> cww;
+          if constexpr (kLutType)
+            if (p.geo.lut_ne > 0) return go(no, no, std::true_type{}, cww);
+          return go(no, no, no, cww);
+        }
+      }
+      if constexpr (kLutType) {
+        if (p.geo.lut_ne > 0)  // the x-factor table (make_plan decides; sizes its shared memory)
+          return p.geo.det ? go(std::true_type{}, no, std::true_type{}, cw0) : go(no, no, std::true_type{}, cw0);
+      }
+      return p.geo.det ? go(std::true_type{}, no, no, cw0) : go(no, no, no, cw0);
     });
   } else e0 = dispatch<T>(L, [&](auto e, auto sh, auto wc, auto ck) -> cudaError_t {
     using DG = Deg<decltype(sh)::value>;

@@ -26,6 +26,13 @@ constexpr int kConsumerWarps = GRKAN_CONSUMER_WARPS;
 constexpr int kStagedThreads = 32 * (kConsumerWarps + 1);  // + 1 producer warp
 constexpr int kStageVecs = GRKAN_STAGE_VECS;               // per tensor per stage
 constexpr int kVPT = kStageVecs / (32 * kConsumerWarps);   // 3 vectors per consumer thread
+// The wide backward geometry: one CTA per SM with kWideWarps consumer warps
+// and kVPT * 32 * kWideWarps-vector stages (make_plan chooses it per shape).
+constexpr int kWideWarps = GRKAN_WIDE_WARPS;
+template <int CW>
+__host__ __device__ constexpr int staged_threads() { return 32 * (CW + 1); }
+template <int CW>
+__host__ __device__ constexpr int stage_vecs() { return kVPT * 32 * CW; }
 constexpr int kMaxStages = 8;
 // Backward CTAs per SM (register cap = 64K / (288 * MINB)).  Measured at
 // KAT-B: 2 CTAs, 4-stage ring, unrolled vectors is best for both fp32 and
@@ -33,9 +40,9 @@ constexpr int kMaxStages = 8;
 // 311 us vs 279 us -- the bf16 backward is FMA-pipe bound, not warp bound).
 // kFullStage: branch-free body for full stages -- measured 260 -> 255 us for
 // bf16 I/O but 308 -> 320 us for fp32 (KAT-B), so bf16 only.
-template <typename T>
+template <typename T, int CW = kConsumerWarps>
 struct BwdCfg {
-  static constexpr int kMinBlocks = GRKAN_BWD_CTAS;
+  static constexpr int kMinBlocks = CW == kConsumerWarps ? GRKAN_BWD_CTAS : 1;
   static constexpr bool kSerialVectors = false;
   static constexpr bool kFullStage = GRKAN_FULL_STAGE && std::is_same<T, __nv_bfloat16>::value;
 };
@@ -170,12 +177,12 @@ struct Raw16<double> {
 // (<= 6 * flush terms) at ~40 instructions per flush.  SH = 1: one slot per
 // lane pair (the pair's totals meet by one shuffle first) -- half the shared
 // memory, for the bf16 table kernel.
-template <int SH>
+template <int SH, int CW = kConsumerWarps>
 __device__ __forceinline__ int acc_slot(int k) {
-  return k * ((32 * kConsumerWarps) >> SH) + (static_cast<int>(threadIdx.x) >> SH);
+  return k * ((32 * CW) >> SH) + (static_cast<int>(threadIdx.x) >> SH);
 }
 
-template <typename A, int KC, bool PK, int SH = 0>
+template <typename A, int KC, bool PK, int SH = 0, int CW = kConsumerWarps>
 __device__ __forceinline__ void lane_flush(A (&acc)[KC], float2 (&acc2)[KC], A* __restrict__ sacc) {
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
@@ -189,37 +196,37 @@ __device__ __forceinline__ void lane_flush(A (&acc)[KC], float2 (&acc2)[KC], A* 
     }
     if constexpr (SH == 1) {
       v += __shfl_xor_sync(0xffffffffu, v, 1);
-      if ((threadIdx.x & 1) == 0) sacc[acc_slot<SH>(k)] += v;
+      if ((threadIdx.x & 1) == 0) sacc[acc_slot<SH, CW>(k)] += v;
     } else {
-      sacc[acc_slot<SH>(k)] += v;
+      sacc[acc_slot<SH, CW>(k)] += v;
     }
   }
 }
 
 // This warp's lanes' slot values for coefficient k (SH = 1: 16 slots, lanes >= 16 add 0).
-template <typename A, int SH>
+template <typename A, int SH, int CW = kConsumerWarps>
 __device__ __forceinline__ A warp_slot_value(const A* __restrict__ sacc, int k) {
   const int lane = threadIdx.x & 31;
   if constexpr (SH == 1)
-    return lane < 16 ? sacc[k * (16 * kConsumerWarps) + (threadIdx.x >> 5) * 16 + lane] : A(0);
+    return lane < 16 ? sacc[k * (16 * CW) + (threadIdx.x >> 5) * 16 + lane] : A(0);
   else
-    return sacc[acc_slot<0>(k)];
+    return sacc[acc_slot<0, CW>(k)];
 }
 
 // End of CTA: each consumer warp folds its lanes' shared-memory totals with a
 // fixed butterfly into partial slot (CTA j, warp w):
-// part[((g * KC + k) * pg + j) * 8 + w]  ->  n_tiles = pg * 8 per (group, coefficient).
-template <typename A, int KC, int SH = 0>
+// part[((g * KC + k) * pg + j) * CW + w]  ->  n_tiles = pg * CW per (group, coefficient).
+template <typename A, int KC, int SH = 0, int CW = kConsumerWarps>
 __device__ __forceinline__ void warp_store(const A* __restrict__ sacc, A* __restrict__ part, int g, int64_t j,
                                            int warp, const Geom& geo) {
   const int lane = threadIdx.x & 31;
-  const int64_t n_tiles = (int64_t)geo.pg * kConsumerWarps;
+  const int64_t n_tiles = (int64_t)geo.pg * CW;
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
-    A v = warp_slot_value<A, SH>(sacc, k);
+    A v = warp_slot_value<A, SH, CW>(sacc, k);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) part[((int64_t)g * KC + k) * n_tiles + j * kConsumerWarps + warp] = v;
+    if (lane == 0) part[((int64_t)g * KC + k) * n_tiles + j * CW + warp] = v;
   }
 }
 
@@ -342,8 +349,8 @@ __device__ __forceinline__ uint32_t lut_slots2(uint32_t w, uint32_t c, uint32_t&
 }
 
 template <typename T, bool EXACT, bool CHECK, bool DET, bool INSTR = false, bool FWD = false, bool LUT = false,
-          int M1 = 6, int N = 4>
-__global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
+          int M1 = 6, int N = 4, int CW = kConsumerWarps>
+__global__ void __launch_bounds__(staged_threads<CW>(), BwdCfg<T, CW>::kMinBlocks)
     k_bwd_staged(const T* __restrict__ x, const T* __restrict__ dy, T* __restrict__ dx, T* __restrict__ y,
                  const typename VecIO<T, 1>::A* __restrict__ ca,
                  const typename VecIO<T, 1>::A* __restrict__ cb,
@@ -357,9 +364,10 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
   constexpr int KC = M1 + N;
   static_assert(!LUT || (std::is_same<T, __nv_bfloat16>::value && !EXACT && !INSTR && !FWD && M1 == 6 && N == 4),
                 "the x-factor table is the bf16 FAST backward at the paper's degrees only");
+  static_assert(CW == kConsumerWarps || !DET, "deterministic partials use the default geometry on every rank");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
-  __shared__ A red[DET ? 2 : 1][DET ? kConsumerWarps : 1][DET ? KC : 1];
+  __shared__ A red[DET ? 2 : 1][DET ? CW : 1][DET ? KC : 1];
   pdl_launch_dependents();
 
   int g;
@@ -376,14 +384,14 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&empty[s], CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (threadIdx.x < 32 * kConsumerWarps) {
+  if (threadIdx.x < 32 * CW) {
 #pragma unroll
     for (int k = 0; k < KC; ++k)
-      if (!LUT || (threadIdx.x & 1) == 0) sacc[acc_slot<LUT ? 1 : 0>(k)] = 0;
+      if (!LUT || (threadIdx.x & 1) == 0) sacc[acc_slot<LUT ? 1 : 0, CW>(k)] = 0;
   }
   __syncthreads();
 
@@ -393,7 +401,7 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
   Checker<A> chk;
   Tally tl;
 
-  if (warp == kConsumerWarps) {
+  if (warp == CW) {
     if (lane == 0) {
       const T* const src[2] = {x, dy};
       T* const ring[2] = {sx, su};
@@ -413,17 +421,17 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
     }
     // the x-factor table after the accumulator totals: built once by the
     // consumer warps (the producer is already streaming the first stages)
-    float* const tiq = reinterpret_cast<float*>(sacc + KC * ((32 * kConsumerWarps) >> (LUT ? 1 : 0)));
+    float* const tiq = reinterpret_cast<float*>(sacc + KC * ((32 * CW) >> (LUT ? 1 : 0)));
     const uint32_t lut_base = static_cast<uint32_t>(geo.lut_e0) << 7;
     const uint32_t lut_c = geo.lut_c;  // a kernel parameter: one IADD3 per pair, not an IMAD
     if constexpr (LUT) {
-      for (int i = threadIdx.x; i < kLutSlots; i += 32 * kConsumerWarps) {
+      for (int i = threadIdx.x; i < kLutSlots; i += 32 * CW) {
         const uint32_t t = i & (kLutSignStride - 1), neg = static_cast<uint32_t>(i) >> 11;
         const float2 e = rp.lut_entry(__uint_as_float(((lut_base + t) | (neg << 15)) << 16));
         tiq[i] = e.x;
         tiq[kLutSlots + i] = e.y;
       }
-      asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * CW) : "memory");
     }
     // this thread's fixed (row, vector) slots in every stage
     int sr[kVPT], so[kVPT];
@@ -431,14 +439,14 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
     const int svecs = geo.RS * geo.V;
 #pragma unroll
     for (int j = 0; j < kVPT; ++j) {
-      const int k = threadIdx.x + j * 32 * kConsumerWarps;
+      const int k = threadIdx.x + j * 32 * CW;
       const int r = k / geo.V, c = (k - (k / geo.V) * geo.V) * W;
       sr[j] = k < svecs ? r : 0x7fffffff;  // never valid outside the stage
       so[j] = r * geo.dg + c;
       gp[j] = dx + (row0 + r) * geo.d + (int64_t)g * geo.dg + c;
     }
     const int64_t gstep = (int64_t)geo.RS * geo.d;
-    const bool full_slots = svecs == kStageVecs;  // every thread slot maps into the stage
+    const bool full_slots = svecs == stage_vecs<CW>();  // every thread slot maps into the stage
     const int slot_elems = geo.RS * geo.dg;
     const int nst = (nr + geo.RS - 1) / geo.RS;
     int slot = 0, since_flush = 0;
@@ -519,13 +527,13 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
           tl.w += W;      // dx
         }
       };
-      if (BwdCfg<T>::kFullStage && full_slots && rows_here == geo.RS) {
+      if (BwdCfg<T, CW>::kFullStage && full_slots && rows_here == geo.RS) {
         // every slot of a full stage is valid: one branch-free block the
         // scheduler can interleave across the thread's kVPT vectors
 #pragma unroll
         for (int j = 0; j < kVPT; ++j) vec(j);
       } else {
-#pragma unroll(BwdCfg<T>::kSerialVectors ? 1 : kVPT)
+#pragma unroll(BwdCfg<T, CW>::kSerialVectors ? 1 : kVPT)
         for (int j = 0; j < kVPT; ++j)
           if (sr[j] < rows_here) vec(j);
       }
@@ -537,7 +545,7 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
       // term-evaluation floor (see lane_flush).
       const bool block_end = DET && ((s + 1) % geo.spb == 0 || s + 1 == nst);
       if (++since_flush == geo.flush || s + 1 == nst || block_end) {
-        lane_flush<A, KC, PK, LUT ? 1 : 0>(acc, acc2, sacc);
+        lane_flush<A, KC, PK, LUT ? 1 : 0, CW>(acc, acc2, sacc);
         since_flush = 0;
       }
       if constexpr (DET) {
@@ -553,7 +561,7 @@ __global__ void __launch_bounds__(kStagedThreads, BwdCfg<T>::kMinBlocks)
     }
     if constexpr (!DET) {
       __syncwarp();
-      warp_store<A, KC, LUT ? 1 : 0>(sacc, part, g, tile, warp, geo);
+      warp_store<A, KC, LUT ? 1 : 0, CW>(sacc, part, g, tile, warp, geo);
     }
     if constexpr (INSTR) {
       if (lane == 0) {

@@ -58,6 +58,7 @@ inline int unroll_for_width(int W) { return W >= 2 ? 2 : 4; }
 struct Plan {
   int W = 1;          // elements per 16-byte vector (1 = scalar path)
   int threads = kBlock;
+  int cw = 0;         // staged backward: consumer warps per CTA (GRKAN_CONSUMER_WARPS or GRKAN_WIDE_WARPS)
   int64_t ctas = 0;
   Geom geo{};
   bool staged = false;  // TMA-bulk-staged persistent kernels (grkan_staged.cuh)
@@ -78,6 +79,9 @@ struct Plan {
 #endif
 #ifndef GRKAN_BWD_STAGES
 #define GRKAN_BWD_STAGES 4         // staged backward ring depth
+#endif
+#ifndef GRKAN_WIDE_WARPS
+#define GRKAN_WIDE_WARPS 16        // wide backward geometry: consumer warps of its one CTA per SM
 #endif
 #ifndef GRKAN_SIGN_GUARD
 #define GRKAN_SIGN_GUARD 1        // FAST: FMA-evaluated A(x) with the sign guard (0: reference-rounded A)
