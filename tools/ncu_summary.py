@@ -1,6 +1,7 @@
 """Summarise ncu --set full captures into profiles/ JSON.
 
     python tools/ncu_summary.py OUT.json NAME=path.ncu-rep [NAME=path.ncu-rep ...]
+    (path may also be the raw-page CSV exported on the box: ncu -i REP --page raw --csv)
 
 Keeps the metrics the docs cite: duration, DRAM bytes, pipe utilisation
 (FMA / ALU / tensor), issue activity, the top stall reasons and the global
@@ -31,7 +32,11 @@ STALLS = ["long_scoreboard", "math_pipe_throttle", "wait", "not_selected", "shor
 
 
 def summarise(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    # a .ncu-rep, or the CSV of its raw page (ncu -i REP --page raw --csv), exported on the box
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units, vals = rows[0], rows[1], rows[2]
     d = {h: (v, u) for h, u, v in zip(hdr, units, vals)}
