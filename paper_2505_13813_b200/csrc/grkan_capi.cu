@@ -166,7 +166,10 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
     // the table build (~2 us per CTA) and the shallower ring pay off only over
     // long row runs (table v2: faster at KAT-B, 85 stages per CTA, and KAT-S, 21)
     const int64_t stages_per_cta = nsu * RU / RS / (static_cast<int64_t>(sms) * ctas_per_sm / ng + 1);
-    if (nt == 2 && es == 2 && lut && m1 == 6 && n == 4 && lut_enabled(stages_per_cta)) {
+    // deterministic partials: the choice must not depend on the shard's rows
+    // (the table path rounds each term differently), so it is made on the
+    // layout alone -- on wherever it fits
+    if (nt == 2 && es == 2 && lut && m1 == 6 && n == 4 && lut_enabled(det ? kLutMinStagesPerCta : stages_per_cta)) {
       // the table (two float arrays over a 16-exponent window) takes a ring
       // stage's place and the accumulator totals go one slot per lane pair, so
       // kBwdCtasPerSm CTAs stay resident

@@ -38,6 +38,10 @@ CASES = [
     ("kat-s-fp32", (16, 197, 1536, 8, 5, 4), torch.float32),
     ("tail-bf16", (3, 67, 384, 4, 5, 4), torch.bfloat16),
     ("generic-degree", (4, 100, 256, 4, 3, 2), torch.float32),
+    # bf16 FAST at a size where the whole tensor takes the x-factor table by the
+    # row-run heuristic but the 8-way shards would not: the table choice must
+    # not depend on the shard
+    ("kat-b-bf16-table", (64, 197, 3072, 8, 5, 4), torch.bfloat16),
 ]
 
 
