@@ -98,15 +98,14 @@ int64_t det_rows(int32_t d, int32_t ng, size_t es) {
 }
 
 // bf16 FAST backward: the x-factor table (grkan_staged.cuh LUT); results agree
-// with the table-free kernel within the FAST tolerance.  GRKAN_LUT=1 in the
-// environment forces it wherever it fits (tests), =0 disables it (A/B); unset:
-// the build default over row runs of at least kLutMinStagesPerCta stages.
-constexpr int64_t kLutMinStagesPerCta = 16;
-
-bool lut_enabled(int64_t stages_per_cta) {
+// with the table-free kernel within the FAST tolerance.  The choice depends on
+// the layout only, never on the row count: the table path rounds each term
+// differently, and dx must not depend on deterministic mode or on how rows
+// are sharded.  GRKAN_LUT=0 in the environment disables it (A/B).
+bool lut_enabled() {
   const char* v = getenv("GRKAN_LUT");
   if (v && (v[0] == '0' || v[0] == '1')) return v[0] == '1';
-  return GRKAN_LUT != 0 && stages_per_cta >= kLutMinStagesPerCta;
+  return GRKAN_LUT != 0;
 }
 
 // Short row segments: the staged producers copy whole stages as tensor-map
@@ -163,13 +162,9 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
     p.smem = static_cast<size_t>(p.stages) * nt * RS * dg * es;
     if (nt == 2)  // + per-lane accumulator totals [10][256] in the accumulation type
       p.smem += static_cast<size_t>(m1 + n) * 32 * cw * (es == 8 ? 8 : 4);
-    // the table build (~2 us per CTA) and the shallower ring pay off only over
-    // long row runs (table v2: faster at KAT-B, 85 stages per CTA, and KAT-S, 21)
-    const int64_t stages_per_cta = nsu * RU / RS / (static_cast<int64_t>(sms) * ctas_per_sm / ng + 1);
-    // deterministic partials: the choice must not depend on the shard's rows
-    // (the table path rounds each term differently), so it is made on the
-    // layout alone -- on wherever it fits
-    if (nt == 2 && es == 2 && lut && m1 == 6 && n == 4 && lut_enabled(det ? kLutMinStagesPerCta : stages_per_cta)) {
+    // (measured faster at KAT-B and KAT-S; the ~1-2 us table build matters only
+    // for tensors that take a few microseconds anyway)
+    if (nt == 2 && es == 2 && lut && m1 == 6 && n == 4 && lut_enabled()) {
       // the table (two float arrays over a 16-exponent window) takes a ring
       // stage's place and the accumulator totals go one slot per lane pair, so
       // kBwdCtasPerSm CTAs stay resident

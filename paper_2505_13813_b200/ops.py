@@ -173,7 +173,9 @@ def rational_forward_backward(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor
                               workspace: torch.Tensor | None = None):
     """(y, dx, da, db): forward_tensor and backward_blocked of the same x in one pass
     (grkan_fwd_bwd: x read once, y from the backward's own P and 1/Q).  Same results as
-    rational_forward + rational_backward -- EXACT y / dx bitwise the reference's."""
+    rational_forward + rational_backward -- EXACT y / dx bitwise the reference's; bf16
+    FAST within the FAST tolerances (rational_backward's x-factor table body rounds the
+    terms differently)."""
     rows, d, ng, m1, n = _validate(x, a, b)
     if dy.shape != x.shape:
         from .errors import GridGeometryError

@@ -117,7 +117,18 @@ def test_bf16_staged_kernel_coverage_through_the_c_abi():
     assert bool((cov == 1).all())
     r, w, m = cnt.cpu().tolist()
     assert (r, w, m) == A().predicted_device_accesses(rows, d, ng, 6, 4, "bf16")
-    dx2, da2, db2 = ops.rational_backward(x, dy, a, b)
+    # the counting instantiation runs the table-free body: compare with that
+    # (the product bf16 FAST path takes the x-factor table, whose terms round differently)
+    import os
+    old = os.environ.get("GRKAN_LUT")
+    os.environ["GRKAN_LUT"] = "0"
+    try:
+        dx2, da2, db2 = ops.rational_backward(x, dy, a, b)
+    finally:
+        if old is None:
+            del os.environ["GRKAN_LUT"]
+        else:
+            os.environ["GRKAN_LUT"] = old
     assert torch.equal(dx, dx2)
     assert orc.matrix_rel(da.cpu().numpy(), da2.cpu().numpy()) <= 1e-5
 

@@ -39,8 +39,11 @@ def test_exact_bitwise_against_the_reference_restatement(shape, groups):
 @pytest.mark.parametrize("exact", [False, True])
 def test_same_results_as_the_two_passes(dtype, exact):
     """dx / da / db bitwise those of rational_backward (the same K2 accumulation, the same
-    K3 fold); y bitwise rational_forward's in EXACT mode, within 1e-5 (bf16: one ulp of
-    the output) in FAST mode (pq vs K1's P * rcp(Q) of a differently evaluated A)."""
+    K3 fold) -- except bf16 FAST, where rational_backward takes the x-factor table body
+    (terms rounded differently; the fused step has no table variant): within the FAST
+    tolerances there; y bitwise rational_forward's in EXACT mode, within 1e-5 (bf16:
+    one ulp of the output) in FAST mode (pq vs K1's P * rcp(Q) of a differently
+    evaluated A)."""
     g = torch.Generator(device="cpu").manual_seed(71)
     x = torch.randn(16, 197, 384, generator=g).to(dtype).to(DEV)
     u = torch.randn(16, 197, 384, generator=g).to(dtype).to(DEV)
@@ -50,7 +53,12 @@ def test_same_results_as_the_two_passes(dtype, exact):
     y, dx, da, db = ops().rational_forward_backward(x, u, a, b, exact=exact)
     y2 = ops().rational_forward(x, a, b, exact=exact)
     dx2, da2, db2 = ops().rational_backward(x, u, a, b, exact=exact)
-    assert torch.equal(dx, dx2) and torch.equal(da, da2) and torch.equal(db, db2)
+    if dtype == torch.bfloat16 and not exact:
+        assert orc.matrix_rel(dx.double().cpu().numpy(), dx2.double().cpu().numpy()) <= 1e-2
+        assert orc.matrix_rel(da.double().cpu().numpy(), da2.double().cpu().numpy()) <= 1e-5
+        assert orc.matrix_rel(db.double().cpu().numpy(), db2.double().cpu().numpy()) <= 1e-5
+    else:
+        assert torch.equal(dx, dx2) and torch.equal(da, da2) and torch.equal(db, db2)
     if exact:
         assert torch.equal(y, y2)
     else:
