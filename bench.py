@@ -604,7 +604,14 @@ def run_b200(args, rank, world, local_rank):
     torch.cuda.synchronize()
 
     K = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    # two events per step in the timed region: at the step boundary and between
+    # the forward and the backward (each event record drains the stream, ~1-2 us;
+    # the four per step of round 1 added ~10 us to a KAT-B step)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    evm = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    eve = [torch.cuda.Event(enable_timing=True) for _ in range(K)] if flush_buf is not None else None
+    # an exchange on the compute stream (N > 1 without the side stream): its own event
+    evc = [torch.cuda.Event(enable_timing=True) for _ in range(K)] if world > 1 and comm is None else None
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(nvml_index(dev))
@@ -620,13 +627,15 @@ def run_b200(args, rank, world, local_rank):
     for k in range(K):
         if flush_buf is not None:  # L2 flush outside the step's events (workload < L2)
             flush_buf.zero_()
-        ev[k][0].record(stream)
+        evs[k].record(stream)
         fwd()
-        ev[k][1].record(stream)
+        evm[k].record(stream)
         bwd()
-        ev[k][2].record(stream)
+        if evc is not None:
+            evc[k].record(stream)
         allreduce(timed=True)
-        ev[k][3].record(stream)
+        if eve is not None:
+            eve[k].record(stream)
     if args.collective == "allreduce":
         join_comm()
     t_end.record(stream)
@@ -637,15 +646,18 @@ def run_b200(args, rank, world, local_rank):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms_total = t_start.elapsed_time(t_end)
-    if flush_buf is not None:  # the flushes sit between the steps: sum the steps themselves
-        ms_total = sum(e[0].elapsed_time(e[3]) for e in ev)
-    fwd_ms = statistics.fmean(e[0].elapsed_time(e[1]) for e in ev)
-    bwd_ms = statistics.fmean(e[1].elapsed_time(e[2]) for e in ev)
+    ends = eve if eve is not None else evs[1:] + [t_end]
+    step_ms = [evs[k].elapsed_time(ends[k]) for k in range(K)]
+    ms_total = sum(step_ms) if eve is not None else t_start.elapsed_time(t_end)
+    fwd_ms = statistics.fmean(evs[k].elapsed_time(evm[k]) for k in range(K))
+    bwd_end = evc if evc is not None else ends
+    bwd_ms = statistics.fmean(evm[k].elapsed_time(bwd_end[k]) for k in range(K))  # K2 + K3
     if comm_ev:  # overlapped all-reduce: its own duration on the comm stream
         coll_ms = statistics.fmean(c0.elapsed_time(c1) for c0, c1 in comm_ev)
+    elif evc is not None:
+        coll_ms = statistics.fmean(evc[k].elapsed_time(ends[k]) for k in range(K))
     else:
-        coll_ms = statistics.fmean(e[2].elapsed_time(e[3]) for e in ev)
+        coll_ms = 0.0
     if world > 1:
         t = torch.tensor([ms_total, fwd_ms, bwd_ms, coll_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -662,9 +674,8 @@ def run_b200(args, rank, world, local_rank):
         same = all(torch.equal(g, allg[0]) for g in allg)
         coll_check = {"ranks": world, "bitwise_identical": same,
                       "max_abs_diff": max(float((g - allg[0]).abs().max()) for g in allg)}
-    # per-step device times (fwd start -> after the step's exchange): mean +- CI95
-    # with the normal approximation, as the reference reports (verification.py:344-349)
-    step_ms = [e[0].elapsed_time(e[3]) for e in ev]
+    # per-step device times (step boundary to step boundary): mean +- CI95 with
+    # the normal approximation, as the reference reports (verification.py:344-349)
     ci95_ms = 1.96 * statistics.stdev(step_ms) / math.sqrt(len(step_ms)) if len(step_ms) > 1 else None
     value = world * E / (ms_step / 1e3)
 
@@ -819,7 +830,8 @@ def run_b200(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_ci95": ci95_ms,
         "timing": {"hold_ms": hold_ms, "host_enqueue_ms": host_enqueue_ms,
-                   "note": "timed steps enqueued behind a device-side hold longer than the host enqueue"},
+                   "note": "timed steps enqueued behind a device-side hold longer than the host enqueue; "
+                           "two CUDA events per step (step boundary, forward | backward)"},
         "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f32" if args.dtype == "fp32" else "bf16-io/f32-math",
