@@ -19,7 +19,7 @@ per-group da/db (the path's only exchange).  Weak scaling: every rank owns a
 full KAT-B batch (B=256), so per-GPU work is fixed as N grows.
 
 ``value``  elements/s over all ranks, inputs already resident in HBM, device
-           time (CUDA events) max over ranks.  Warm-up: >= W steps and >= 150 ms;
+           time (CUDA events) max over ranks.  Warm-up: >= W steps and >= 1 s (GRKAN_BENCH_WARM_S);
            the timed K steps are enqueued behind a short device-side spin
            (--hold-ms) so host launch jitter cannot open gaps inside them;
            NVML clocks are then sampled by the (idle) host thread from the
@@ -572,8 +572,9 @@ def run_b200(args, rank, world, local_rank):
 
         bwd = fused
 
-    # warm-up: at least W steps and at least 150 ms of device work (clocks and
-    # memory settled on a fresh box), untimed.  Every step carries a collective,
+    # warm-up: at least W steps and at least WARM_S of device work (clocks and
+    # memory settled on a fresh box: the first heavy seconds of a fresh box can
+    # bring a transient sw_power_cap), untimed.  Every step carries a collective,
     # so every rank must run the same number: the time-based extension is
     # agreed across ranks (the slowest rank's count) before it runs.
     def warm(n):
@@ -588,7 +589,7 @@ def run_b200(args, rank, world, local_rank):
     t_w = time.perf_counter()
     warm(n_min)
     el = time.perf_counter() - t_w
-    extra = 0 if el >= 0.15 else int(math.ceil((0.15 - el) / max(el / n_min, 1e-6)))
+    extra = 0 if el >= WARM_S else int(math.ceil((WARM_S - el) / max(el / n_min, 1e-6)))
     if world > 1:
         t_extra = torch.tensor([extra], dtype=torch.int64, device=dev)
         dist.all_reduce(t_extra, op=dist.ReduceOp.MAX)
@@ -947,6 +948,9 @@ def run_train(args, rank, world, local_rank):
             "paper_h200_images_s": {"kat_b": 1801.75, "kat_s": 3741.91, "kat_t": 6317.90}[TRAIN_CONFIGS[args.config]],
         }), flush=True)
 
+
+# minimum warm-up of device work before the timed steps (seconds)
+WARM_S = float(os.environ.get("GRKAN_BENCH_WARM_S", "1.0"))
 
 # a rank that never arrives fails the collective (and the run) instead of hanging it
 PG_TIMEOUT = __import__("datetime").timedelta(seconds=float(os.environ.get("GRKAN_PG_TIMEOUT_S", "600")))
