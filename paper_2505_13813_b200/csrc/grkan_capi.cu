@@ -132,6 +132,17 @@ bool wide_geometry(size_t es, int dg, bool wide_ok) {
   return es == 2 || static_cast<size_t>(dg) * es >= 1536;
 }
 
+// Staged backward at >= 2 CTAs per SM: the first wave's share of stage units,
+// in 1/64 of a later CTA's (Geom::w1).  GRKAN_SKEW=<n> overrides (A/B).
+int first_wave_weight() {
+  const char* v = getenv("GRKAN_SKEW");
+  if (v && *v) {
+    const int w = atoi(v);
+    if (w >= 16 && w <= 256) return w;
+  }
+  return GRKAN_SKEW64;
+}
+
 // nt = tensors streamed in (1 forward, 2 backward).  det: one partial per
 // global RB-row block (slot-major), independent of the launch geometry.
 // lut: the caller runs the bf16 FAST backward (grkan_bwd / grkan_bwd_partials).
@@ -144,6 +155,8 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
   const int64_t RB = det ? det_rows(d, ng, es) : 0;
   p.geo.det = det ? 1 : 0;
   p.geo.one = 1.0f;
+  p.geo.w1 = 64;  // even partition unless the staged backward below skews it
+  p.geo.wave = sms;
   p.W = vec ? static_cast<int>(16 / es) : 1;
   const bool wide = nt == 2 && !det && vec && wide_geometry(es, dg, wide_ok);
   const int cw = wide ? GRKAN_WIDE_WARPS : grkan::kConsumerWarpsHost;
@@ -227,6 +240,7 @@ Plan make_plan(int64_t rows, int32_t d, int32_t ng, int32_t m1, int32_t n, size_
     // partials per (group, coefficient) for K3 (backward: one per consumer
     // warp; deterministic: one per RB-row block)
     p.geo.n_tiles = det ? nsu : (nt == 2 ? pg * cw : pg);
+    if (nt == 2 && !det && occ >= 2 && pg * ng > sms && nsu >= 4 * pg) p.geo.w1 = first_wave_weight();
     p.ctas = rows > 0 ? pg * ng : 0;
     return p;
   }

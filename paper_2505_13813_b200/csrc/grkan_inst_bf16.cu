@@ -2,3 +2,4 @@
 #include "grkan_launch.cuh"
 
 GRKAN_DEFINE_LAUNCHERS(__nv_bfloat16, bf16)
+GRKAN_PROBE_EXPORTS(bf16)

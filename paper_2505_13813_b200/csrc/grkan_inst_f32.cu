@@ -2,3 +2,4 @@
 #include "grkan_launch.cuh"
 
 GRKAN_DEFINE_LAUNCHERS(float, f32)
+GRKAN_PROBE_EXPORTS(f32)

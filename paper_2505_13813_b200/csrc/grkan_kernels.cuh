@@ -130,6 +130,34 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Diagnostic only (GRKAN_PROBE_TIMES=1 variant builds, tools/probe_times.py):
+// %globaltimer stamps per staged-backward CTA [start, first stage, warp 0 done,
+// last warp done] and K3's [first start, last end] after them.
+#if GRKAN_PROBE_TIMES
+constexpr int kProbeCtas = 4096;
+static __device__ unsigned long long g_probe_t[4 * kProbeCtas + 4];
+__device__ __forceinline__ unsigned long long probe_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define GRKAN_STAMP(i) (g_probe_t[4 * (blockIdx.x % kProbeCtas) + (i)] = probe_now())
+#define GRKAN_STAMP_MAX(i) atomicMax(&g_probe_t[4 * (blockIdx.x % kProbeCtas) + (i)], probe_now())
+#define GRKAN_PROBE_EXPORTS(SUF)                                                              \
+  extern "C" __attribute__((visibility("default"))) int grkan_probe_read_##SUF(unsigned long long* h, int n) {                      \
+    return (int)cudaMemcpyFromSymbol(h, grkan::g_probe_t, sizeof(unsigned long long) * n);  \
+  }                                                                                           \
+  extern "C" __attribute__((visibility("default"))) int grkan_probe_clear_##SUF() {                                                 \
+    static unsigned long long z[4 * grkan::kProbeCtas + 4];                                   \
+    z[4 * grkan::kProbeCtas] = ~0ull; /* K3's first start: atomicMin */                        \
+    return (int)cudaMemcpyToSymbol(grkan::g_probe_t, z, sizeof(z));                         \
+  }
+#else
+#define GRKAN_STAMP(i) ((void)0)
+#define GRKAN_STAMP_MAX(i) ((void)0)
+#define GRKAN_PROBE_EXPORTS(SUF)
+#endif
+
 // ---------------------------------------------------------------------------
 // Engine selection: packed fp32 pairs for the paper's degrees, scalar otherwise.
 // ---------------------------------------------------------------------------
@@ -416,6 +444,9 @@ __global__ void __launch_bounds__(256)
                  A* __restrict__ db, DevStatus* __restrict__ st, int64_t slot_stride,
                  unsigned long long* __restrict__ cnt) {
   pdl_wait();  // K2's partials are complete and visible after this
+#if GRKAN_PROBE_TIMES
+  if (threadIdx.x == 0) atomicMin(&g_probe_t[4 * kProbeCtas], probe_now());
+#endif
   const int kc = m1 + n;
   const int col = blockIdx.x;  // g * kc + k
   // column-major part[col * n_tiles + t] (slot_stride 1), or the deterministic
@@ -440,6 +471,9 @@ __global__ void __launch_bounds__(256)
     else
       db[(int64_t)g * n + (k - m1)] = out;
     if (nonfinite(out)) st->accum_overflow = 1;
+#if GRKAN_PROBE_TIMES
+    atomicMax(&g_probe_t[4 * kProbeCtas + 1], probe_now());
+#endif
     if (cnt) {  // instrumented: this column's partial loads and its one result store
       atomicAdd(cnt + 0, static_cast<unsigned long long>(n_tiles));
       atomicAdd(cnt + 1, 1ull);

@@ -238,8 +238,20 @@ __device__ __forceinline__ void staged_range(const Geom& geo, int& g, int64_t& j
   const int64_t bid = blockIdx.x;
   g = static_cast<int>(bid % geo.ng);
   j = bid / geo.ng;
-  const int64_t s0 = (j * geo.nsu) / geo.pg;
-  const int64_t s1 = ((j + 1) * geo.nsu) / geo.pg;
+  int64_t s0, s1;
+  if (geo.w1 == 64) {
+    s0 = (j * geo.nsu) / geo.pg;
+    s1 = ((j + 1) * geo.nsu) / geo.pg;
+  } else {  // weighted: CTAs j < J of this group are in the first wave (bid < wave)
+    const int64_t J = geo.wave > g ? (geo.wave - g + geo.ng - 1) / geo.ng : 0;
+    auto cum = [&](int64_t jj) {
+      const int64_t f = jj < J ? jj : J;
+      return f * geo.w1 + (jj - f) * 64;
+    };
+    const int64_t tot = cum(geo.pg);
+    s0 = cum(j) * geo.nsu / tot;
+    s1 = cum(j + 1) * geo.nsu / tot;
+  }
   row0 = s0 * geo.RU;
   const int64_t r1 = s1 * geo.RU < geo.rows ? s1 * geo.RU : geo.rows;
   nr = static_cast<int>(r1 - row0);
@@ -373,6 +385,7 @@ __global__ void __launch_bounds__(staged_threads<CW>(), BwdCfg<T, CW>::kMinBlock
   int g;
   int64_t tile, row0;
   int nr;
+  if (threadIdx.x == 0) GRKAN_STAMP(0);
   staged_range(geo, g, tile, row0, nr);
   if (DET) tile = row0 / geo.RU;  // first RB-row block of this CTA
   const size_t ring_elems = (size_t)stages * geo.RS * geo.dg;
@@ -428,8 +441,12 @@ __global__ void __launch_bounds__(staged_threads<CW>(), BwdCfg<T, CW>::kMinBlock
       for (int i = threadIdx.x; i < kLutSlots; i += 32 * CW) {
         const uint32_t t = i & (kLutSignStride - 1), neg = static_cast<uint32_t>(i) >> 11;
         const float2 e = rp.lut_entry(__uint_as_float(((lut_base + t) | (neg << 15)) << 16));
-        tiq[i] = e.x;
-        tiq[kLutSlots + i] = e.y;
+        if constexpr (GRKAN_LUT_PAIRED) {
+          reinterpret_cast<float2*>(tiq)[i] = e;
+        } else {
+          tiq[i] = e.x;
+          tiq[kLutSlots + i] = e.y;
+        }
       }
       asm volatile("bar.sync 1, %0;" ::"r"(32 * CW) : "memory");
     }
@@ -453,6 +470,7 @@ __global__ void __launch_bounds__(staged_threads<CW>(), BwdCfg<T, CW>::kMinBlock
     uint32_t phase = 0;
     for (int s = 0; s < nst; ++s) {
       if (!GRKAN_PROBE_NOMEM) mbar_wait(&full[slot], phase);
+      if (GRKAN_PROBE_TIMES && s == 0 && threadIdx.x == 0) GRKAN_STAMP(1);
       const int rows_here = min(geo.RS, nr - s * geo.RS);
       const T* xs = sx + slot * slot_elems;
       const T* us = su + slot * slot_elems;
@@ -471,10 +489,19 @@ __global__ void __launch_bounds__(staged_threads<CW>(), BwdCfg<T, CW>::kMinBlock
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               const uint32_t s0 = sl[i] & 0xffffu, s1 = sl[i] >> 16;
-              iq[2 * i] = tiq[s0];
-              iq[2 * i + 1] = tiq[s1];
-              wf[2 * i] = tiq[kLutSlots + s0];
-              wf[2 * i + 1] = tiq[kLutSlots + s1];
+              if constexpr (GRKAN_LUT_PAIRED) {  // one 8-byte load per element
+                const float2 e0 = reinterpret_cast<const float2*>(tiq)[s0];
+                const float2 e1 = reinterpret_cast<const float2*>(tiq)[s1];
+                iq[2 * i] = e0.x;
+                wf[2 * i] = e0.y;
+                iq[2 * i + 1] = e1.x;
+                wf[2 * i + 1] = e1.y;
+              } else {
+                iq[2 * i] = tiq[s0];
+                iq[2 * i + 1] = tiq[s1];
+                wf[2 * i] = tiq[kLutSlots + s0];
+                wf[2 * i + 1] = tiq[kLutSlots + s1];
+              }
             }
           } else {  // an x outside the window: that element evaluates the table function itself
 #pragma unroll
@@ -484,7 +511,8 @@ __global__ void __launch_bounds__(staged_threads<CW>(), BwdCfg<T, CW>::kMinBlock
               float2 en;
               if (t < static_cast<uint32_t>(kLutSignStride)) {
                 const uint32_t sidx = t | ((h >> 4) & 0x800u);
-                en = make_float2(tiq[sidx], tiq[kLutSlots + sidx]);
+                en = GRKAN_LUT_PAIRED ? reinterpret_cast<const float2*>(tiq)[sidx]
+                                      : make_float2(tiq[sidx], tiq[kLutSlots + sidx]);
               } else {
                 en = rp.lut_entry(vx[e]);
               }
@@ -563,6 +591,16 @@ __global__ void __launch_bounds__(staged_threads<CW>(), BwdCfg<T, CW>::kMinBlock
       __syncwarp();
       warp_store<A, KC, LUT ? 1 : 0, CW>(sacc, part, g, tile, warp, geo);
     }
+#if GRKAN_PROBE_TIMES
+    if (lane == 0) {
+      if (warp == 0) {  // slot 2: the SM this CTA ran on (<< 32) | its row count
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_probe_t[4 * (blockIdx.x % kProbeCtas) + 2] = (static_cast<unsigned long long>(smid) << 32) | nr;
+      }
+      GRKAN_STAMP_MAX(3);
+    }
+#endif
     if constexpr (INSTR) {
       if (lane == 0) {
         if (warp == 0) tl.r += KC;  // the CTA's coefficient row (registers afterwards)

@@ -36,6 +36,12 @@ struct Geom {
   // views [rows, d] as [rows, d / tma_ci, tma_ci] (box inner extent <= 256).
   int32_t tma_rows;
   int32_t tma_ci;
+  // staged backward at two or more CTAs per SM: the first wave of CTAs (bid <
+  // wave, one per SM) gets w1/64 of a later CTA's share of the group's stage
+  // units (the warp schedulers favour the older CTA: without it, the second CTA
+  // of every SM finished ~10 us after the first at KAT-S fp32).  w1 = 64: even.
+  int32_t w1;
+  int32_t wave;
   // instrumented launches only (grkan_bwd_instrumented; null otherwise): per-element
   // visit counts [rows * d] and element-access tallies {reads, writes, rmw}
   int32_t* cov;
@@ -109,6 +115,15 @@ struct Plan {
 #endif
 #ifndef GRKAN_PROBE_NOMEM
 #define GRKAN_PROBE_NOMEM 0       // diagnostic only: staged backward computes on unfilled shared memory
+#endif
+#ifndef GRKAN_LUT_PAIRED
+#define GRKAN_LUT_PAIRED 0        // bf16 table as (1/Q, factor) float2 pairs: one 8-byte load per element
+#endif
+#ifndef GRKAN_SKEW64
+#define GRKAN_SKEW64 64           // staged backward, >= 2 CTAs per SM: first-wave share in 1/64 units
+#endif
+#ifndef GRKAN_PROBE_TIMES
+#define GRKAN_PROBE_TIMES 0       // diagnostic only: %globaltimer stamps of the staged backward's CTAs
 #endif
 #ifndef GRKAN_FWD_CTAS
 #define GRKAN_FWD_CTAS 8
