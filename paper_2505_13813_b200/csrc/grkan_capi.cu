@@ -143,6 +143,15 @@ int first_wave_weight() {
   return GRKAN_SKEW64;
 }
 
+// The status block of a staged backward without CHECK_FINITE is zeroed by the
+// kernel's CTA 0 (Geom::zst): one stream operation less per call.
+// GRKAN_ZST=0 in the environment keeps the memset (A/B).
+bool zero_status_in_kernel(const Plan& p, uint32_t flags) {
+  if (!p.staged || (flags & GRKAN_FLAG_CHECK_FINITE) != 0) return false;
+  const char* v = getenv("GRKAN_ZST");
+  return !(v && v[0] == '0');
+}
+
 // nt = tensors streamed in (1 forward, 2 backward).  det: one partial per
 // global RB-row block (slot-major), independent of the launch geometry.
 // lut: the caller runs the bf16 FAST backward (grkan_bwd / grkan_bwd_partials).
@@ -490,10 +499,11 @@ int grkan_bwd(const void* x, const void* dy, const void* a, const void* b, void*
   if (!aligned16(ws)) return fail(GRKAN_ERR_INVALID, "workspace must be 16-byte aligned");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   DevStatus* st = reinterpret_cast<DevStatus*>(ws);
-  cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(DevStatus), s);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(status)");
+  cudaError_t e;
   const size_t as = acc_size(dtype);
   if (rows == 0) {  // nothing to fold: the gradients are exact zeros
+    e = cudaMemsetAsync(ws, 0, sizeof(DevStatus), s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(status)");
     e = cudaMemsetAsync(da, 0, static_cast<size_t>(n_groups) * m1 * as, s);
     if (e == cudaSuccess && n > 0) e = cudaMemsetAsync(db, 0, static_cast<size_t>(n_groups) * n * as, s);
     return e == cudaSuccess ? GRKAN_OK : cuda_fail(e, "cudaMemsetAsync(da/db)");
@@ -508,6 +518,11 @@ int grkan_bwd(const void* x, const void* dy, const void* a, const void* b, void*
   const size_t need = ws_bytes_for(p, m1, n, dtype);
   if (ws_bytes < need)
     return fail(GRKAN_ERR_INVALID, "workspace too small: %zu < %zu bytes", ws_bytes, need);
+  p.geo.zst = zero_status_in_kernel(p, flags);
+  if (!p.geo.zst) {
+    e = cudaMemsetAsync(ws, 0, sizeof(DevStatus), s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(status)");
+  }
   LaunchArgs L{};
   L.plan = &p;
   L.x = x;
@@ -555,8 +570,12 @@ int grkan_fwd_bwd(const void* x, const void* dy, const void* a, const void* b, v
   const size_t need = ws_bytes_for(p, m1, n, dtype);
   if (ws_bytes < need) return fail(GRKAN_ERR_INVALID, "workspace too small: %zu < %zu bytes", ws_bytes, need);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(DevStatus), s);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(status)");
+  p.geo.zst = zero_status_in_kernel(p, flags);
+  if (!p.geo.zst) {
+    cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(DevStatus), s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(status)");
+  }
+  cudaError_t e;
   LaunchArgs L{};
   L.plan = &p;
   L.x = x;

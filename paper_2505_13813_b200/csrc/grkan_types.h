@@ -42,6 +42,10 @@ struct Geom {
   // of every SM finished ~10 us after the first at KAT-S fp32).  w1 = 64: even.
   int32_t w1;
   int32_t wave;
+  // staged backward without CHECK_FINITE: CTA 0 zeroes the status block at its
+  // start instead of a cudaMemsetAsync before the launch (no other K2 CTA
+  // writes it, K3 writes it only after griddepcontrol.wait, i.e. after K2)
+  int32_t zst;
   // instrumented launches only (grkan_bwd_instrumented; null otherwise): per-element
   // visit counts [rows * d] and element-access tallies {reads, writes, rmw}
   int32_t* cov;
@@ -117,7 +121,7 @@ struct Plan {
 #define GRKAN_PROBE_NOMEM 0       // diagnostic only: staged backward computes on unfilled shared memory
 #endif
 #ifndef GRKAN_LUT_PAIRED
-#define GRKAN_LUT_PAIRED 0        // bf16 table as (1/Q, factor) float2 pairs: one 8-byte load per element
+#define GRKAN_LUT_PAIRED 1        // bf16 table as (1/Q, factor) float2 pairs: one 8-byte load per element (0: two arrays)
 #endif
 #ifndef GRKAN_SKEW64
 #define GRKAN_SKEW64 64           // staged backward, >= 2 CTAs per SM: first-wave share in 1/64 units
