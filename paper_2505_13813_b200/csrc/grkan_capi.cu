@@ -152,24 +152,6 @@ bool zero_status_in_kernel(const Plan& p, uint32_t flags) {
   return !(v && v[0] == '0');
 }
 
-// K3 folded into the staged K2 (Geom::fold): per-CTA partials, at most
-// kFoldMaxGroups groups (their arrival counters sit in the workspace header
-// after the status block).  Measured 1.3-3.3 us SLOWER per backward than the
-// PDL-launched K3 (every CTA's fence waits for its streaming dx stores to
-// drain, then the last CTA folds serially): off unless GRKAN_FOLD=1.
-void plan_fold(Plan& p, void* ws, void* da, void* db) {
-  static std::atomic<uint32_t> seq{0x5eed0001u};
-  const char* v = getenv("GRKAN_FOLD");
-  if (!p.staged || p.geo.det || p.geo.ng > grkan::kFoldMaxGroups || !(v && v[0] == '1')) return;
-  uint32_t s = seq.fetch_add(1);
-  if (s == 0) s = seq.fetch_add(1);  // 0 is the reset value
-  p.geo.fold = 1;
-  p.geo.seq = s;
-  p.geo.ctr = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 16);
-  p.geo.gda = da;
-  p.geo.gdb = db;
-}
-
 // nt = tensors streamed in (1 forward, 2 backward).  det: one partial per
 // global RB-row block (slot-major), independent of the launch geometry.
 // lut: the caller runs the bf16 FAST backward (grkan_bwd / grkan_bwd_partials).
@@ -541,7 +523,6 @@ int grkan_bwd(const void* x, const void* dy, const void* a, const void* b, void*
     e = cudaMemsetAsync(ws, 0, sizeof(DevStatus), s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(status)");
   }
-  plan_fold(p, ws, da, db);
   LaunchArgs L{};
   L.plan = &p;
   L.x = x;
@@ -594,7 +575,6 @@ int grkan_fwd_bwd(const void* x, const void* dy, const void* a, const void* b, v
     cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(DevStatus), s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(status)");
   }
-  plan_fold(p, ws, da, db);
   cudaError_t e;
   LaunchArgs L{};
   L.plan = &p;

@@ -224,7 +224,7 @@ cudaError_t launch_bwd_t(const LaunchArgs& L) {
             L.m1, L.n, L.st);
     return cudaGetLastError();
   });
-  if (e0 != cudaSuccess || L.partials_only || p.geo.fold) return e0;  // fold: K2's last CTAs ran K3
+  if (e0 != cudaSuccess || L.partials_only) return e0;
   return launch_reduce_t<A>(static_cast<const A*>(L.part), p.geo.n_tiles, p.geo.det ? (int64_t)p.geo.ng * (L.m1 + L.n) : 1,
                             p.geo.ng, L.m1, L.n, static_cast<A*>(L.da), static_cast<A*>(L.db), L.st, L.stream);
 }

@@ -230,80 +230,6 @@ __device__ __forceinline__ void warp_store(const A* __restrict__ sacc, A* __rest
   }
 }
 
-// K3 folded into K2 (Geom::fold; grkan_bwd / grkan_fwd_bwd, per-CTA partials,
-// ng <= kFoldMaxGroups): every CTA publishes its partials and arrives on its
-// group's counter; the group's last CTA folds the group's KC columns with K3's
-// arithmetic, in K3's order (256-thread column teams: thread t sums tiles
-// t, t + 256, ... in fp64, fixed butterfly, warps 0..7 in order), so da/db are
-// bitwise what k_bwd_reduce gives.  The counter (ws header) carries the launch
-// sequence number in its high word -- a stale or never-zeroed value starts
-// over -- and the last CTA resets it (CUDA-graph replays reuse the number).
-// Saves K3's launch (~0.85 us gap + 2.3 us, tools/probe_times.py).
-__device__ __forceinline__ bool fold_arrive(unsigned long long* c, uint32_t seq, int total) {
-  unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(c);
-  for (;;) {
-    const unsigned long long nv =
-        static_cast<uint32_t>(cur >> 32) == seq ? cur + 1 : ((static_cast<unsigned long long>(seq) << 32) | 1ull);
-    const unsigned long long prev = atomicCAS(c, cur, nv);
-    if (prev == cur) {
-      if (static_cast<uint32_t>(nv) != static_cast<uint32_t>(total)) return false;
-      atomicExch(c, 0ull);
-      return true;
-    }
-    cur = prev;
-  }
-}
-
-template <typename A, int KC, int M1, int CW>
-__device__ __noinline__ void fold_if_last(const A* __restrict__ part, int g, const Geom& geo, DevStatus* st) {
-  static_assert(CW % 8 == 0, "column teams of 256 consumer threads");
-  constexpr int H = CW / 8;                // column teams
-  constexpr int KPT = (KC + H - 1) / H;    // columns per team
-  __shared__ int last;
-  __shared__ double red[KC][8];
-  __threadfence();  // this thread's partial stores before the arrival
-  asm volatile("bar.sync 1, %0;" ::"r"(32 * CW) : "memory");
-  if (threadIdx.x == 0) last = fold_arrive(geo.ctr + g, geo.seq, geo.pg) ? 1 : 0;
-  asm volatile("bar.sync 1, %0;" ::"r"(32 * CW) : "memory");
-  if (!last) return;
-  __threadfence();
-  const int team = threadIdx.x >> 8, t0 = threadIdx.x & 255;
-  const int64_t n_tiles = geo.n_tiles;
-  double sum[KPT];
-#pragma unroll
-  for (int i = 0; i < KPT; ++i) sum[i] = 0.0;
-  const A* base = part + (int64_t)g * KC * n_tiles;
-  for (int64_t t = t0; t < n_tiles; t += 256) {
-#pragma unroll
-    for (int i = 0; i < KPT; ++i) {
-      const int k = team + i * H;
-      if (k < KC) sum[i] += static_cast<double>(__ldcg(base + (int64_t)k * n_tiles + t));
-    }
-  }
-  const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & 7;
-#pragma unroll
-  for (int i = 0; i < KPT; ++i) {
-    double v = sum[i];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    const int k = team + i * H;
-    if (lane == 0 && k < KC) red[k][w] = v;
-  }
-  asm volatile("bar.sync 1, %0;" ::"r"(32 * CW) : "memory");
-  if (threadIdx.x < KC) {
-    const int k = threadIdx.x;
-    double tot = 0.0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) tot += red[k][j];
-    const A out = static_cast<A>(tot);
-    if (k < M1)
-      static_cast<A*>(geo.gda)[(int64_t)g * M1 + k] = out;
-    else
-      static_cast<A*>(geo.gdb)[(int64_t)g * (KC - M1) + (k - M1)] = out;
-    if (nonfinite(out)) st->accum_overflow = 1;
-  }
-}
-
 // Persistent, statically balanced partition: CTA (g, j) of pg per group owns
 // stage units [j*nsu/pg, (j+1)*nsu/pg) of group g -- every CTA gets the same
 // number of RS-row stages to within one, so there is no tail wave.  Linear
@@ -668,9 +594,6 @@ __global__ void __launch_bounds__(staged_threads<CW>(), BwdCfg<T, CW>::kMinBlock
     if constexpr (!DET) {
       __syncwarp();
       warp_store<A, KC, LUT ? 1 : 0, CW>(sacc, part, g, tile, warp, geo);
-    }
-    if constexpr (!DET && !INSTR) {
-      if (geo.fold) fold_if_last<A, KC, M1, CW>(part, g, geo, st);
     }
 #if GRKAN_PROBE_TIMES
     if (lane == 0) {

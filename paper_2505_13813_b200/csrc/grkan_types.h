@@ -46,13 +46,6 @@ struct Geom {
   // start instead of a cudaMemsetAsync before the launch (no other K2 CTA
   // writes it, K3 writes it only after griddepcontrol.wait, i.e. after K2)
   int32_t zst;
-  // K3 folded into K2 (grkan_staged.cuh fold_if_last): per-group arrival
-  // counters in the workspace header, the launch's sequence number, da / db
-  int32_t fold;
-  uint32_t seq;
-  unsigned long long* ctr;
-  void* gda;
-  void* gdb;
   // instrumented launches only (grkan_bwd_instrumented; null otherwise): per-element
   // visit counts [rows * d] and element-access tallies {reads, writes, rmw}
   int32_t* cov;
@@ -130,7 +123,6 @@ struct Plan {
 #ifndef GRKAN_LUT_PAIRED
 #define GRKAN_LUT_PAIRED 1        // bf16 table as (1/Q, factor) float2 pairs: one 8-byte load per element (0: two arrays)
 #endif
-constexpr int kFoldMaxGroups = 30;  // arrival counters in the 256-byte workspace header after the status
 #ifndef GRKAN_SKEW64
 #define GRKAN_SKEW64 64           // staged backward, >= 2 CTAs per SM: first-wave share in 1/64 units
 #endif
