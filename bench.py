@@ -323,9 +323,28 @@ class ClockSampler:
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
         except Exception:
             self._nv = None
+        self.temp_start = None
         if self._nv is not None:  # the first queries are slow (NVML lazy init): not inside the region
             self._sample()
             self.samples, self.power_mw, self.power_inst_mw, self.reasons = [], [], [], 0
+            self.temp_start = self._temps()
+
+    def _temps(self):
+        """GPU and HBM temperature (C), read outside the timed region: HBM refreshes
+        more often when hot, which costs bandwidth without any clock-event reason."""
+        nv = self._nv
+        out = {}
+        try:
+            out["gpu"] = nv.nvmlDeviceGetTemperature(self._h, nv.NVML_TEMPERATURE_GPU)
+        except Exception:
+            pass
+        try:
+            fv = nv.nvmlDeviceGetFieldValues(self._h, [getattr(nv, "NVML_FI_DEV_MEMORY_TEMP", 82)])[0]
+            if fv.nvmlReturn == 0:
+                out["mem"] = int(fv.value.uiVal)
+        except Exception:
+            pass
+        return out
 
     def _run(self):
         nv = self._nv
@@ -385,6 +404,8 @@ class ClockSampler:
             out["power_limit_w"] = self._nv.nvmlDeviceGetEnforcedPowerLimit(self._h) / 1e3
         except Exception:
             pass
+        if self.temp_start is not None:
+            out["temp_c"] = {"before": self.temp_start, "after": self._temps()}
         return out
 
 
