@@ -309,6 +309,7 @@ class ClockSampler:
 
     def __init__(self, index):
         self.samples = []
+        self.mem_mhz = []
         self.power_mw = []
         self.power_inst_mw = []
         self.reasons = 0
@@ -327,6 +328,7 @@ class ClockSampler:
         if self._nv is not None:  # the first queries are slow (NVML lazy init): not inside the region
             self._sample()
             self.samples, self.power_mw, self.power_inst_mw, self.reasons = [], [], [], 0
+            self.mem_mhz = []
             self.temp_start = self._temps()
 
     def _temps(self):
@@ -356,6 +358,7 @@ class ClockSampler:
         nv = self._nv
         try:
             self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+            self.mem_mhz.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_MEM))
             self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
             self.power_mw.append(nv.nvmlDeviceGetPowerUsage(self._h))
         except Exception:
@@ -404,6 +407,9 @@ class ClockSampler:
             out["power_limit_w"] = self._nv.nvmlDeviceGetEnforcedPowerLimit(self._h) / 1e3
         except Exception:
             pass
+        if self.mem_mhz:
+            out["mem_mhz"] = statistics.median(self.mem_mhz)
+            out["mem_mhz_min"] = min(self.mem_mhz)
         if self.temp_start is not None:
             out["temp_c"] = {"before": self.temp_start, "after": self._temps()}
         return out
