@@ -1,0 +1,10 @@
+# Fresh box: the driver's order (GPU tests, smoke, default line) then the default line twice more,
+# with the HBM clock (clocks.mem_mhz) and temperatures in each line.
+TAG=${1:-s4f1}
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu_${TAG}.txt 2>&1; tail -1 gpurun_out/pytest_gpu_${TAG}.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_${TAG}.txt 2>&1; tail -1 gpurun_out/smoke_${TAG}.txt
+for i in 1 2 3; do
+  timeout 900 python bench.py > gpurun_out/bench_${TAG}_default_$i.json 2> gpurun_out/bench_${TAG}_default_$i.err
+  python -c "import json; d=json.load(open('gpurun_out/bench_${TAG}_default_$i.json')); k=d['kernels']; c=d['clocks']; print('run $i value %.3e fwd %.1f bwd %.1f' % (d['value'], k['fwd_us'], k['bwd_us']), c['sm_mhz'], c.get('mem_mhz'), c.get('mem_mhz_min'), c['reasons'], c.get('temp_c'))"
+done
