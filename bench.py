@@ -434,6 +434,15 @@ def run_b200(args, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    # diagnostic (profiles/r2/s4/temp): GRKAN_BENCH_PREALLOC_GB=N maps, touches and
+    # releases N GB before the workload's own buffers are allocated
+    pre_gb = float(os.environ.get("GRKAN_BENCH_PREALLOC_GB", "0"))
+    if pre_gb > 0:
+        tmp = torch.empty(int(pre_gb * 2**30), dtype=torch.uint8, device=dev)
+        tmp.fill_(0)
+        torch.cuda.synchronize()
+        del tmp
+        torch.cuda.empty_cache()
     shape = workload(args)
     batch, seq, dim, groups = shape
     if args.scaling == "strong":
