@@ -449,14 +449,6 @@ def run_b200(args, rank, world, local_rank):
         del tmp
         torch.cuda.empty_cache()
     shape = workload(args)
-    # The CPU reference leg runs before the GPU measurement: measured on fresh
-    # boxes, the fp32 KAT-B step ran ~5% slower (3.04 vs 3.20e11, same SM / HBM
-    # clocks and temperatures) in every process until a multi-threaded host
-    # phase like this one had run (profiles/r2/s4/temp/).
-    cpu_pre = None
-    if world == 1 and not args.no_cpu_baseline:
-        sb = min(args.cpu_sample_batch, shape[0])
-        cpu_pre = (sb,) + tuple(cpu_reference_rate(args, shape, sb, args.cpu_passes))
     batch, seq, dim, groups = shape
     if args.scaling == "strong":
         batch = max(1, batch // world)
@@ -921,8 +913,9 @@ def run_b200(args, rank, world, local_rank):
             "bwd_us": alg1_us, "speedup_of_staged_bwd": alg1_us / (bwd_ms * 1e3),
             "note": "paper: FlashKAT bwd 140.5x faster than KAT's atomic bwd on RTX 4060 Ti (PAPER.md:402)"},
     }
-    if cpu_pre is not None:
-        sb, rate, workers, times, kind, what = cpu_pre
+    if world == 1 and not args.no_cpu_baseline:
+        sb = min(args.cpu_sample_batch, shape[0])
+        rate, workers, times, kind, what = cpu_reference_rate(args, shape, sb, args.cpu_passes)
         line["cpu_baseline"] = {
             "value": rate, "unit": UNIT, "cores": workers, "kind": kind, "cpu_model": cpu_model(),
             "sample": "%s with B=%d (E=%d): %s, forward_tensor + backward_blocked (block %d, %d threads), "
